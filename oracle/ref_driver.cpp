@@ -1,0 +1,218 @@
+// ref_driver.cpp -- extern "C" shim over the UNMODIFIED reference sources.
+//
+// TEST / BASELINE INFRASTRUCTURE ONLY.  oracle/Makefile compiles this file
+// together with /root/reference/proj/src/*.cpp (in place, read-only) into
+// oracle/_ref/libems_ref.so.  It lets the Python tests and bench.py's
+// reference arm call the reference's own operator API:
+//   prefill_attention      proj/src/scoring.cpp:93-103
+//   three_step_scores      proj/src/reference.cpp:51-98
+//   init_score_state       proj/src/scoring.cpp:154-162
+//   compress_prefill       proj/src/compressor.cpp:163-242
+//   cache_dump_json        proj/src/cache.cpp:114-150
+//   make_engine / prefill  proj/src/engine.cpp:26-82
+//   gen_synthetic          proj/src/trace.cpp:414-429
+// No reference code is copied here; everything is a call into it.
+#include <cstdint>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include <omp.h>
+
+#include "ems/compressor.hpp"
+#include "ems/engine.hpp"
+#include "ems/errors.hpp"
+#include "ems/policies.hpp"
+#include "ems/reference.hpp"
+#include "ems/scoring.hpp"
+#include "ems/trace.hpp"
+
+namespace {
+
+thread_local std::string g_err;
+thread_local std::string g_json;
+
+ems::Matrix to_matrix(const double* p, std::size_t rows, std::size_t cols) {
+    ems::Matrix m(rows, cols);
+    std::memcpy(m.data.data(), p, sizeof(double) * rows * cols);
+    return m;
+}
+
+ems::CompressionConfig make_config(int64_t n_budget, int64_t l_win, double tau, double gamma,
+                                   int64_t kernel, int32_t zero_class) {
+    ems::CompressionConfig c;
+    c.n_budget = static_cast<std::size_t>(n_budget);
+    c.l_win = static_cast<std::size_t>(l_win);
+    c.tau = tau;
+    c.gamma = gamma;
+    c.kernel_size = static_cast<std::size_t>(kernel);
+    c.eviction = zero_class ? ems::EvictionRealization::zero_class
+                            : ems::EvictionRealization::explicit_removal;
+    return c;
+}
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const ems::DegenerateInputError& e) {
+        g_err = e.what();
+        return 2;
+    } catch (const ems::CorruptionError& e) {
+        g_err = e.what();
+        return 3;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return 1;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 4;
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ems_ref_last_error() { return g_err.c_str(); }
+const char* ems_ref_last_json() { return g_json.c_str(); }
+int ems_ref_max_threads() { return omp_get_max_threads(); }
+
+int ems_ref_prefill_attention(const double* q, const double* k, const double* v, int64_t n,
+                              int64_t d, int64_t l_win, double* out, double* glo, double* loc) {
+    return guarded([&] {
+        const auto Q = to_matrix(q, n, d), K = to_matrix(k, n, d);
+        if (v != nullptr) {
+            const auto V = to_matrix(v, n, d);
+            const ems::PrefillAttention pa = ems::prefill_attention(Q, K, V, l_win);
+            if (out) std::memcpy(out, pa.outputs.data.data(), sizeof(double) * n * d);
+            std::memcpy(glo, pa.glo.data(), sizeof(double) * n);
+            std::memcpy(loc, pa.loc.data(), sizeof(double) * n);
+        } else {
+            const ems::PrefillScores ps = ems::prefill_scores(Q, K, l_win);
+            std::memcpy(glo, ps.glo.data(), sizeof(double) * n);
+            std::memcpy(loc, ps.loc.data(), sizeof(double) * n);
+        }
+    });
+}
+
+int ems_ref_three_step_scores(const double* q, const double* k, int64_t n, int64_t d,
+                              int64_t l_win, double* glo, double* loc) {
+    return guarded([&] {
+        const ems::PrefillScores ps =
+            ems::reference::three_step_scores(to_matrix(q, n, d), to_matrix(k, n, d), l_win);
+        std::memcpy(glo, ps.glo.data(), sizeof(double) * n);
+        std::memcpy(loc, ps.loc.data(), sizeof(double) * n);
+    });
+}
+
+int ems_ref_effective_score(const double* glo, const double* loc_past, const double* loc_cur,
+                            int64_t n, int64_t kernel, double* out) {
+    return guarded([&] {
+        ems::ScoreState s;
+        s.glo.assign(glo, glo + n);
+        s.loc_past.assign(loc_past, loc_past + n);
+        s.loc_cur.assign(loc_cur, loc_cur + n);
+        const ems::Vector p = ems::effective_score(s, kernel);
+        std::memcpy(out, p.data(), sizeof(double) * n);
+    });
+}
+
+// compress_prefill on one head; the resulting HeadCacheState is returned as
+// cache_dump_json text (fetch with ems_ref_last_json).
+int ems_ref_compress_prefill(const double* k_raw, const double* v_raw, const double* glo,
+                             const double* loc, int64_t n, int64_t d, int64_t n_budget,
+                             int64_t l_win, double tau, double gamma, int64_t kernel,
+                             int32_t zero_class) {
+    return guarded([&] {
+        const auto cfg = make_config(n_budget, l_win, tau, gamma, kernel, zero_class);
+        const ems::ScoreState s = ems::init_score_state(ems::Vector(glo, glo + n),
+                                                        ems::Vector(loc, loc + n), l_win);
+        const ems::HeadCacheState cache =
+            ems::compress_prefill(to_matrix(k_raw, n, d), to_matrix(v_raw, n, d), s, cfg);
+        g_json = ems::cache_dump_json(cache);
+    });
+}
+
+// The timed composition of the reference arm for one KV
+// unit: per query head prefill_attention in parallel over heads (engine.cpp:65),
+// GQA mean (contract D2), init_score_state, compress_prefill.  q_rot [G][n][d].
+int ems_ref_prefill_unit(const double* q_rot, const double* k_rot, const double* k_raw,
+                         const double* v, int64_t G, int64_t n, int64_t d, int64_t n_budget,
+                         int64_t l_win, double tau, double gamma, int64_t kernel,
+                         int32_t zero_class, double* glo_out, double* loc_out, int32_t dump) {
+    return guarded([&] {
+        const auto cfg = make_config(n_budget, l_win, tau, gamma, kernel, zero_class);
+        const auto K = to_matrix(k_rot, n, d), V = to_matrix(v, n, d);
+        const std::size_t l_win_eff = std::min<std::size_t>(l_win, n);
+        std::vector<ems::PrefillAttention> pa(G);
+        std::vector<std::string> errs(G);
+#pragma omp parallel for schedule(static)
+        for (int64_t h = 0; h < G; ++h) {
+            try {
+                pa[h] = ems::prefill_attention(to_matrix(q_rot + h * n * d, n, d), K, V, l_win_eff);
+            } catch (const std::exception& e) {
+                errs[h] = e.what();
+            }
+        }
+        for (auto& e : errs)
+            if (!e.empty()) throw std::invalid_argument(e);
+        ems::Vector glo(n, 0.0), loc(n, 0.0);
+        for (int64_t h = 0; h < G; ++h)
+            for (int64_t j = 0; j < n; ++j) glo[j] += pa[h].glo[j], loc[j] += pa[h].loc[j];
+        for (int64_t j = 0; j < n; ++j) glo[j] /= double(G), loc[j] /= double(G);
+        if (glo_out) std::memcpy(glo_out, glo.data(), sizeof(double) * n);
+        if (loc_out) std::memcpy(loc_out, loc.data(), sizeof(double) * n);
+        const ems::ScoreState s = ems::init_score_state(glo, loc, l_win);
+        const ems::HeadCacheState cache = ems::policy_prefill_compress(
+            ems::PolicyHandle{ems::PolicyKind::ems}, to_matrix(k_raw, n, d), V, s, cfg);
+        if (dump) g_json = ems::cache_dump_json(cache);
+    });
+}
+
+// engine::prefill with the EMS policy over raw per-head blocks [H][n][d]
+// (RoPE applied inside, engine.cpp:68-69); dumps head `dump_head`'s cache.
+int ems_ref_engine_prefill(const double* q, const double* k, const double* v, int64_t H,
+                           int64_t n, int64_t d, int64_t n_budget, int64_t l_win, double tau,
+                           double gamma, int64_t kernel, int32_t zero_class, double rope_base,
+                           int64_t dump_head) {
+    return guarded([&] {
+        const auto cfg = make_config(n_budget, l_win, tau, gamma, kernel, zero_class);
+        ems::EngineState e =
+            ems::make_engine(H, d, ems::PolicyHandle{ems::PolicyKind::ems}, cfg, rope_base);
+        std::vector<ems::Matrix> qb, kb, vb;
+        for (int64_t h = 0; h < H; ++h) {
+            qb.push_back(to_matrix(q + h * n * d, n, d));
+            kb.push_back(to_matrix(k + h * n * d, n, d));
+            vb.push_back(to_matrix(v + h * n * d, n, d));
+        }
+        ems::prefill(e, qb, kb, vb);
+        g_json = ems::cache_dump_json(e.heads[dump_head]);
+    });
+}
+
+// gen_synthetic prefill step, blocks laid out [H][n][d] (fp64 holding f32 values).
+int ems_ref_gen_synthetic(int32_t kind, uint64_t seed, int64_t tokens, int64_t heads, int64_t dim,
+                          int64_t decode_steps, double level, double perturb, double* q, double* k,
+                          double* v) {
+    return guarded([&] {
+        ems::SynthParams p;
+        p.tokens = tokens;
+        p.heads = heads;
+        p.dim = dim;
+        p.decode_steps = decode_steps;
+        p.level = level;
+        p.perturb = perturb;
+        const ems::Trace t = ems::gen_synthetic(static_cast<ems::SynthKind>(kind), seed, p);
+        const ems::TraceStep& s = t.steps.at(0);
+        for (int64_t h = 0; h < heads; ++h) {
+            std::memcpy(q + h * tokens * dim, s.q[h].data.data(), sizeof(double) * tokens * dim);
+            std::memcpy(k + h * tokens * dim, s.k[h].data.data(), sizeof(double) * tokens * dim);
+            std::memcpy(v + h * tokens * dim, s.v[h].data.data(), sizeof(double) * tokens * dim);
+        }
+    });
+}
+
+}  // extern "C"
