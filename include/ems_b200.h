@@ -1,0 +1,187 @@
+/*
+ * ems_b200.h -- C ABI of the B200-native EMS prefill-compress path.
+ *
+ * This is the drop-in boundary for the reference's prefill hot path
+ * (SURVEY.md section 8b).  The reference binds these operations as C++
+ * functions on fp64 per-head matrices; here they are batched, stream-ordered,
+ * device-pointer entry points over contiguous [B][H][L][d] tensors, so each
+ * (b, h) slice is byte-for-byte a reference `Matrix` (proj/include/ems/types.hpp:13-34)
+ * in fp32 or bf16.  include/ems_b200/ems.hpp restores the reference's exact
+ * C++ signatures on top of this ABI; INTEGRATION.md shows the bindings.
+ *
+ *   reference entry point (file:line)                          replaced by
+ *   ---------------------------------------------------------  -------------------------
+ *   prefill_attention   proj/include/ems/scoring.hpp:52-54      ems_score (out_o != NULL)
+ *   prefill_scores      proj/include/ems/scoring.hpp:48-49      ems_score (out_o == NULL)
+ *   global/local_score_prefill  scoring.hpp:40-45               ems_score
+ *   combine_glo_loc + effective_score  scoring.hpp:58,66        ems_select (prologue)
+ *   init_score_state    scoring.hpp:70                          implicit: loc -> loc_past
+ *   partition_tokens    proj/include/ems/compressor.hpp:14-25   ems_select
+ *   redundancy_cross    proj/include/ems/analysis.hpp:19-20     ems_redundancy_cross / ems_merge
+ *   assign_merge_destinations  compressor.hpp:29               ems_merge
+ *   weighted_merge      compressor.hpp:32-51                    ems_compact (merge epilogue)
+ *   compress_prefill    compressor.hpp:58-60                    ems_select+ems_merge+ems_compact
+ *   engine prefill (score -> compress)  proj/src/engine.cpp:42-82  ems_prefill_compress
+ *
+ * Conventions
+ *  - A "unit" is one (b, h_kv) with its G = heads_q / heads_kv query heads;
+ *    unit u = b * heads_kv + h_kv.  Units are independent (no collective).
+ *  - All pointers are caller-owned device memory; nothing is allocated inside
+ *    the hot path.  Query ems_workspace_bytes() once and pass a workspace of
+ *    at least that size (16-byte aligned).  Calls are asynchronous on `stream`.
+ *  - Inputs are pre-rotated Q/K for scoring and raw (pre-RoPE) K plus V for the
+ *    merge (contract D3).
+ *  - GQA (contract D2): per-unit glo/loc are the MEAN over the unit's G query
+ *    heads of each head's column sums.
+ *  - Status codes mirror the reference's exceptions (proj/include/ems/errors.hpp):
+ *    std::invalid_argument -> EMS_INVALID_ARGUMENT, DegenerateInputError ->
+ *    EMS_DEGENERATE_INPUT, CorruptionError -> EMS_CORRUPTION.  Host-detectable
+ *    errors return immediately; data-dependent ones (zero global mass, LUT
+ *    integrity) are recorded in the workspace and returned by ems_sync_status().
+ *  - Reentrant: no global mutable state except the thread-local error string.
+ */
+#ifndef EMS_B200_H
+#define EMS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#include <cuda_runtime_api.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EMS_B200_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define EMS_API __attribute__((visibility("default")))
+#else
+#define EMS_API
+#endif
+
+typedef enum {
+    EMS_OK = 0,
+    EMS_INVALID_ARGUMENT = 1,
+    EMS_DEGENERATE_INPUT = 2,
+    EMS_CORRUPTION = 3,
+    EMS_CUDA_ERROR = 4,
+    EMS_UNSUPPORTED = 5,
+} ems_status;
+
+typedef enum { EMS_F32 = 0, EMS_BF16 = 1 } ems_dtype;
+
+/* Score-pass implementation.  AUTO picks the tcgen05 kernels for bf16 with
+ * head_dim 128 and the SIMT kernels otherwise (fp32 has no tcgen05 MMA kind
+ * that keeps the 1e-4 contract; SURVEY.md section 7 "fp32 config 1"). */
+typedef enum { EMS_SCORE_AUTO = 0, EMS_SCORE_SIMT = 1, EMS_SCORE_TCGEN05 = 2 } ems_score_impl;
+
+/* Problem descriptor: shapes + CompressionConfig (proj/include/ems/cache.hpp:20-39). */
+typedef struct {
+    int32_t batch;
+    int32_t heads_q;
+    int32_t heads_kv;        /* heads_q % heads_kv == 0 */
+    int32_t seq_len;         /* L: prompt tokens */
+    int32_t head_dim;        /* d: even, <= 128 (SIMT) / == 128 (tcgen05) */
+    int32_t dtype;           /* ems_dtype of Q/K/V, O and the cache K/V */
+    int32_t l_win;           /* CompressionConfig::l_win (scores use min(l_win, L)) */
+    int32_t n_budget;        /* CompressionConfig::n_budget */
+    double tau;              /* merge threshold in [0, 1] */
+    double gamma;            /* merge magnification >= 1 */
+    int32_t kernel_size;     /* odd pooling window */
+    int32_t zero_class;      /* 1: EvictionRealization::zero_class, 0: explicit_removal */
+    int32_t key_only;        /* 0: R = cos_k*cos_v (reference); 1: key cosine only (D1) */
+    int32_t score_impl;      /* ems_score_impl */
+    int64_t first_position;  /* logical position of token 0 */
+} ems_desc;
+
+/* Per-unit capacities of the compressed cache (fixed-size SoA). */
+typedef struct {
+    int32_t units;
+    int32_t centers;   /* n_budget - l_win */
+    int32_t locals;    /* n_budget (keep-all path stores up to n_budget tokens) */
+    int32_t lut;       /* (n_budget - l_win) + floor((gamma - 1) * n_budget) */
+    int32_t tbm;       /* floor((gamma - 1) * n_budget) */
+} ems_cache_dims;
+
+/* The compressed per-unit cache, device SoA (flattened HeadCacheState,
+ * proj/include/ems/cache.hpp:41-111).  [u][...] with the capacities above.
+ * Keys/values in the desc dtype; scores fp32 triples (glo, loc_past, loc_cur). */
+typedef struct {
+    void* center_key;       /* [u][centers][d] unit-norm key (slot order = position order) */
+    float* center_norm;     /* [u][centers]    preserved key norm */
+    void* center_value;     /* [u][centers][d] */
+    int32_t* center_pos;    /* [u][centers] */
+    float* center_score;    /* [u][centers][3] */
+    void* local_key;        /* [u][locals][d]  raw key */
+    void* local_value;      /* [u][locals][d] */
+    int32_t* local_pos;     /* [u][locals] */
+    float* local_score;     /* [u][locals][3] */
+    int32_t* lut_pos;       /* [u][lut] sorted by position */
+    int32_t* lut_slot;      /* [u][lut] center slot, -1 = zero class */
+    int32_t* counts;        /* [u][4] = n_centers, n_locals, n_lut, compressed */
+} ems_cache;
+
+/* Intermediate per-unit buffers shared by the staged entry points. */
+typedef struct {
+    float* pooled;        /* [u][L]  effective score (combine + mean-pool), fp32 */
+    int8_t* cls;          /* [u][L]  0 irrelevant, 1 to-be-merged, 2 important, 3 local */
+    int32_t* imp_idx;     /* [u][centers] important token indices, ascending (slot order) */
+    int32_t* tbm_idx;     /* [u][tbm]     TBM token indices, ascending */
+    int32_t* part_counts; /* [u][4] = n_imp, n_tbm, n_irrelevant, n_local */
+    int32_t* dest;        /* [u][tbm]     merge destination slot or -1 (zero class) */
+} ems_stage;
+
+EMS_API int ems_abi_version(void);
+EMS_API const char* ems_last_error(void);
+EMS_API const char* ems_status_string(int status);
+
+EMS_API int ems_validate(const ems_desc* desc);
+EMS_API int ems_cache_dims_for(const ems_desc* desc, ems_cache_dims* out);
+EMS_API size_t ems_workspace_bytes(const ems_desc* desc);
+
+/* (1) Score pass: causal attention O (optional) plus GQA-mean column sums.
+ *   q_rot [B][Hq][L][d], k_rot/v [B][Hkv][L][d]  (dtype)
+ *   out_o [B][Hq][L][d] (dtype, may be NULL -> score only; v may then be NULL)
+ *   lse   [B][Hq][L] fp32 natural-log row log-sum-exp (may be NULL)
+ *   glo, loc [B][Hkv][L] fp32 */
+EMS_API int ems_score(const ems_desc* desc, const void* q_rot, const void* k_rot, const void* v,
+              void* out_o, float* lse, float* glo, float* loc, void* workspace,
+              size_t workspace_bytes, cudaStream_t stream);
+
+/* (2) Select: align + combine + pool + radix top-k + classify + index lists. */
+EMS_API int ems_select(const ems_desc* desc, const float* glo, const float* loc, const ems_stage* stage,
+               void* workspace, size_t workspace_bytes, cudaStream_t stream);
+
+/* (3) Merge assignment: R = cos_k*cos_v (TBM x centers) on raw K/V, argmax with
+ * ties to the lower column, tau threshold -> stage->dest. */
+EMS_API int ems_merge(const ems_desc* desc, const void* k_raw, const void* v, const ems_stage* stage,
+              void* workspace, size_t workspace_bytes, cudaStream_t stream);
+
+/* (4) Compact: centers (unit key, norm, value, position, scores), weighted merge
+ * of TBM members into their centers, locals, position-sorted LUT. */
+EMS_API int ems_compact(const ems_desc* desc, const void* k_raw, const void* v, const float* glo,
+                const float* loc, const ems_stage* stage, const ems_cache* cache,
+                void* workspace, size_t workspace_bytes, cudaStream_t stream);
+
+/* Whole path (1)-(4); stage may be NULL (then workspace-backed). */
+EMS_API int ems_prefill_compress(const ems_desc* desc, const void* q_rot, const void* k_rot,
+                         const void* k_raw, const void* v, void* out_o, float* lse, float* glo,
+                         float* loc, const ems_stage* stage, const ems_cache* cache,
+                         void* workspace, size_t workspace_bytes, cudaStream_t stream);
+
+/* Standalone redundancy_cross (analysis.hpp:19-20) for one pair of token groups:
+ * k_rows/v_rows [n_rows][d], k_cols/v_cols [n_cols][d] (dtype) -> r [n_rows][n_cols] fp32. */
+EMS_API int ems_redundancy_cross(int32_t dtype, int32_t d, const void* k_rows, const void* v_rows,
+                         int32_t n_rows, const void* k_cols, const void* v_cols, int32_t n_cols,
+                         int32_t key_only, float* r, cudaStream_t stream);
+
+/* Synchronises `stream` and returns the first data-dependent error the kernels
+ * recorded in the workspace (EMS_DEGENERATE_INPUT, EMS_CORRUPTION) or EMS_OK. */
+EMS_API int ems_sync_status(const ems_desc* desc, void* workspace, cudaStream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* EMS_B200_H */

@@ -1,0 +1,415 @@
+// capi.cu -- the extern "C" boundary (include/ems_b200.h): validation, workspace
+// layout and the launch sequence of the four kernels.  No allocation, no host
+// synchronisation on the hot path; everything is stream-ordered.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+#include "common.cuh"
+
+namespace ems {
+
+cudaError_t score_simt(const Dims& dm, int dtype, const void* q, const void* k, const void* v,
+                       void* o, float* lse, float* glo, float* loc, cudaStream_t s);
+cudaError_t score_tc(const Dims& dm, const void* q, const void* k, const void* v, void* o,
+                     float* lse, float* glo, float* loc, void* ws, cudaStream_t s);
+size_t score_tc_workspace(const Dims& dm);
+bool score_tc_supported(const Dims& dm, int dtype);
+cudaError_t launch_select(const Dims& dm, int l_win, int n_imp, int n_tbm, int kernel,
+                          const float* glo, const float* loc, const ems_stage& sg,
+                          DevStatus* status, cudaStream_t s);
+cudaError_t launch_merge_assign(const Dims& dm, int dtype, const void* k, const void* v,
+                                const ems_stage& sg, double tau, int key_only, float* inv_kc,
+                                float* inv_vc, float* inv_kt, float* inv_vt, cudaStream_t s);
+cudaError_t launch_merge_scatter(const Dims& dm, int dtype, const void* k, const void* v,
+                                 const float* glo, const float* loc, const ems_stage& sg,
+                                 int32_t* ws_count, int32_t* ws_members, const ems_cache& cache,
+                                 cudaStream_t s);
+cudaError_t launch_compact(const Dims& dm, int dtype, const void* k, const void* v,
+                           const float* glo, const float* loc, const ems_stage& sg,
+                           const ems_cache& c, int zero_class, int64_t first_pos, cudaStream_t s);
+cudaError_t launch_keep_all(const Dims& dm, int dtype, const void* k, const void* v,
+                            const float* glo, const float* loc, const ems_stage& sg,
+                            const ems_cache& c, int64_t first_pos, cudaStream_t s);
+cudaError_t launch_redundancy_cross(int dtype, int d, const void* kr, const void* vr, int nr,
+                                    const void* kc, const void* vc, int nc, int key_only,
+                                    float* r, cudaStream_t s);
+
+namespace {
+thread_local char g_err[1024] = "";
+}
+
+void set_error(const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+Dims make_dims(const ems_desc& d) {
+    Dims m;
+    m.B = d.batch;
+    m.Hq = d.heads_q;
+    m.Hkv = d.heads_kv;
+    m.G = d.heads_kv > 0 ? d.heads_q / d.heads_kv : 0;
+    m.L = d.seq_len;
+    m.d = d.head_dim;
+    m.units = d.batch * d.heads_kv;
+    m.lwin_scores = d.l_win < d.seq_len ? d.l_win : d.seq_len;  // engine.cpp:63
+    m.cap_c = d.n_budget - d.l_win;                                // cache.hpp:32
+    m.cap_l = d.n_budget;
+    m.cap_tbm = (int)((d.gamma - 1.0) * (double)d.n_budget);     // cache.hpp:33-35
+    m.cap_lut = m.cap_c + m.cap_tbm;
+    m.esize = d.dtype == EMS_F32 ? 4 : 2;
+    return m;
+}
+
+namespace {
+
+constexpr size_t kAlign = 256;
+size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+// Workspace carve-up.  Offsets are deterministic functions of the descriptor.
+struct Layout {
+    size_t status, lse, glo, loc, pooled, cls, imp, tbm, pcount, dest, inv, cnt, mem, tc, total;
+};
+
+Layout layout(const ems_desc& d) {
+    const Dims m = make_dims(d);
+    Layout l{};
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        const size_t o = off;
+        off += align_up(bytes);
+        return o;
+    };
+    const size_t U = (size_t)m.units, L = (size_t)m.L;
+    l.status = take(sizeof(DevStatus));
+    l.lse = take(sizeof(float) * (size_t)m.B * m.Hq * L);
+    l.glo = take(sizeof(float) * U * L);
+    l.loc = take(sizeof(float) * U * L);
+    l.pooled = take(sizeof(float) * U * L);
+    l.cls = take(U * L);
+    l.imp = take(sizeof(int32_t) * U * (size_t)m.cap_c);
+    l.tbm = take(sizeof(int32_t) * U * (size_t)(m.cap_tbm > 0 ? m.cap_tbm : 1));
+    l.pcount = take(sizeof(int32_t) * U * 4);
+    l.dest = take(sizeof(int32_t) * U * (size_t)(m.cap_tbm > 0 ? m.cap_tbm : 1));
+    l.inv = take(sizeof(float) * U * 2 * (size_t)(m.cap_c + m.cap_tbm));
+    l.cnt = take(sizeof(int32_t) * U * (size_t)(m.cap_c + 1));
+    l.mem = take(sizeof(int32_t) * U * (size_t)(m.cap_tbm > 0 ? m.cap_tbm : 1));
+    l.tc = take(score_tc_workspace(m));
+    l.total = off;
+    return l;
+}
+
+template <class P>
+P* at(void* ws, size_t off) {
+    return reinterpret_cast<P*>(static_cast<char*>(ws) + off);
+}
+
+ems_stage default_stage(const ems_desc& d, void* ws) {
+    const Layout l = layout(d);
+    ems_stage s;
+    s.pooled = at<float>(ws, l.pooled);
+    s.cls = at<int8_t>(ws, l.cls);
+    s.imp_idx = at<int32_t>(ws, l.imp);
+    s.tbm_idx = at<int32_t>(ws, l.tbm);
+    s.part_counts = at<int32_t>(ws, l.pcount);
+    s.dest = at<int32_t>(ws, l.dest);
+    return s;
+}
+
+int check_ws(const ems_desc* d, void* ws, size_t bytes) {
+    const size_t need = layout(*d).total;
+    if (ws == nullptr || bytes < need) {
+        set_error("workspace too small: need %zu bytes, got %zu", need, bytes);
+        return EMS_INVALID_ARGUMENT;
+    }
+    if (reinterpret_cast<uintptr_t>(ws) % 16 != 0) {
+        set_error("workspace must be 16-byte aligned");
+        return EMS_INVALID_ARGUMENT;
+    }
+    return EMS_OK;
+}
+
+bool supported_dim(int d) {
+    return d == 8 || d == 16 || d == 32 || d == 64 || d == 96 || d == 128;
+}
+
+int kernel_eff(const ems_desc& d) {  // clamp_kernel, compressor.cpp:29-34
+    if (d.kernel_size <= d.seq_len) return d.kernel_size;
+    return (d.seq_len % 2 == 1) ? d.seq_len : d.seq_len - 1;
+}
+
+bool use_tc(const ems_desc& d) {
+    const Dims m = make_dims(d);
+    if (d.score_impl == EMS_SCORE_SIMT) return false;
+    return score_tc_supported(m, d.dtype);
+}
+
+int run_score(const ems_desc* desc, const void* q, const void* k, const void* v, void* o,
+              float* lse, float* glo, float* loc, void* ws, cudaStream_t s) {
+    const Dims m = make_dims(*desc);
+    const Layout l = layout(*desc);
+    float* lse_buf = lse ? lse : at<float>(ws, l.lse);
+    cudaError_t e;
+    if (use_tc(*desc)) {
+        e = score_tc(m, q, k, v, o, lse_buf, glo, loc, at<void>(ws, l.tc), s);
+    } else {
+        if (desc->score_impl == EMS_SCORE_TCGEN05) {
+            set_error("tcgen05 score pass unsupported for this shape/dtype");
+            return EMS_UNSUPPORTED;
+        }
+        e = score_simt(m, desc->dtype, q, k, v, o, lse_buf, glo, loc, s);
+    }
+    if (e != cudaSuccess) {
+        set_error("score launch: %s", cudaGetErrorString(e));
+        return EMS_CUDA_ERROR;
+    }
+    return EMS_OK;
+}
+
+int run_select(const ems_desc* desc, const float* glo, const float* loc, const ems_stage& sg,
+               void* ws, cudaStream_t s) {
+    const Dims m = make_dims(*desc);
+    const int n_cand = m.L - desc->l_win;
+    const int n_imp = m.cap_c < n_cand ? m.cap_c : n_cand;                     // :64
+    const int n_tbm = m.cap_tbm < n_cand - n_imp ? m.cap_tbm : n_cand - n_imp;  // :65
+    cudaError_t e = launch_select(m, desc->l_win, n_imp, n_tbm, kernel_eff(*desc), glo, loc, sg,
+                                  at<DevStatus>(ws, layout(*desc).status), s);
+    if (e != cudaSuccess) {
+        set_error("select launch: %s", cudaGetErrorString(e));
+        return EMS_CUDA_ERROR;
+    }
+    return EMS_OK;
+}
+
+int run_merge(const ems_desc* desc, const void* k_raw, const void* v, const ems_stage& sg,
+              void* ws, cudaStream_t s) {
+    const Dims m = make_dims(*desc);
+    if (m.cap_tbm <= 0) return EMS_OK;
+    const Layout l = layout(*desc);
+    float* inv = at<float>(ws, l.inv);
+    const size_t U = m.units;
+    float* inv_kc = inv;
+    float* inv_vc = inv_kc + U * m.cap_c;
+    float* inv_kt = inv_vc + U * m.cap_c;
+    float* inv_vt = inv_kt + U * m.cap_tbm;
+    cudaError_t e = launch_merge_assign(m, desc->dtype, k_raw, v, sg, desc->tau, desc->key_only,
+                                        inv_kc, inv_vc, inv_kt, inv_vt, s);
+    if (e != cudaSuccess) {
+        set_error("merge launch: %s", cudaGetErrorString(e));
+        return EMS_CUDA_ERROR;
+    }
+    return EMS_OK;
+}
+
+int run_compact(const ems_desc* desc, const void* k_raw, const void* v, const float* glo,
+                const float* loc, const ems_stage& sg, const ems_cache& c, void* ws,
+                cudaStream_t s) {
+    const Dims m = make_dims(*desc);
+    const Layout l = layout(*desc);
+    cudaError_t e;
+    if (m.L <= desc->n_budget) {
+        e = launch_keep_all(m, desc->dtype, k_raw, v, glo, loc, sg, c, desc->first_position, s);
+    } else {
+        ems_stage sg2 = sg;
+        if (m.cap_tbm <= 0) sg2.dest = at<int32_t>(ws, l.dest);  // never read (no TBM tokens)
+        e = launch_compact(m, desc->dtype, k_raw, v, glo, loc, sg2, c, desc->zero_class,
+                           desc->first_position, s);
+        if (e == cudaSuccess && m.cap_tbm > 0)
+            e = launch_merge_scatter(m, desc->dtype, k_raw, v, glo, loc, sg, at<int32_t>(ws, l.cnt),
+                                     at<int32_t>(ws, l.mem), c, s);
+    }
+    if (e != cudaSuccess) {
+        set_error("compact launch: %s", cudaGetErrorString(e));
+        return EMS_CUDA_ERROR;
+    }
+    return EMS_OK;
+}
+
+}  // namespace
+}  // namespace ems
+
+using namespace ems;
+
+extern "C" {
+
+int ems_abi_version(void) { return EMS_B200_ABI_VERSION; }
+const char* ems_last_error(void) { return g_err; }
+
+const char* ems_status_string(int status) {
+    switch (status) {
+        case EMS_OK: return "ok";
+        case EMS_INVALID_ARGUMENT: return "invalid argument";
+        case EMS_DEGENERATE_INPUT: return "degenerate input";
+        case EMS_CORRUPTION: return "corruption";
+        case EMS_CUDA_ERROR: return "cuda error";
+        case EMS_UNSUPPORTED: return "unsupported";
+        default: return "unknown";
+    }
+}
+
+int ems_validate(const ems_desc* d) {
+    if (d == nullptr) {
+        set_error("null descriptor");
+        return EMS_INVALID_ARGUMENT;
+    }
+    if (d->batch <= 0 || d->heads_q <= 0 || d->heads_kv <= 0 || d->heads_q % d->heads_kv != 0) {
+        set_error("bad head/batch shape (B=%d Hq=%d Hkv=%d)", d->batch, d->heads_q, d->heads_kv);
+        return EMS_INVALID_ARGUMENT;
+    }
+    if (d->seq_len <= 0) {  // prefill: empty prompt (engine.cpp:49-51)
+        set_error("empty prompt");
+        return EMS_INVALID_ARGUMENT;
+    }
+    if (!supported_dim(d->head_dim)) {
+        set_error("head_dim %d unsupported (8,16,32,64,96,128)", d->head_dim);
+        return EMS_INVALID_ARGUMENT;
+    }
+    if (d->dtype != EMS_F32 && d->dtype != EMS_BF16) {
+        set_error("dtype must be EMS_F32 or EMS_BF16");
+        return EMS_INVALID_ARGUMENT;
+    }
+    // CompressionConfig::validate, proj/src/cache.cpp:12-28
+    if (d->n_budget <= 0 || d->l_win <= 0 || d->n_budget <= d->l_win) {
+        set_error("CompressionConfig: require n_budget > l_win > 0");
+        return EMS_INVALID_ARGUMENT;
+    }
+    if (!(d->tau >= 0.0 && d->tau <= 1.0)) {
+        set_error("CompressionConfig: tau must be in [0, 1]");
+        return EMS_INVALID_ARGUMENT;
+    }
+    if (!(d->gamma >= 1.0)) {
+        set_error("CompressionConfig: gamma must be >= 1");
+        return EMS_INVALID_ARGUMENT;
+    }
+    if (d->kernel_size <= 0 || d->kernel_size % 2 == 0) {
+        set_error("CompressionConfig: kernel_size must be odd");
+        return EMS_INVALID_ARGUMENT;
+    }
+    if (d->score_impl < 0 || d->score_impl > 2) {
+        set_error("bad score_impl");
+        return EMS_INVALID_ARGUMENT;
+    }
+    if ((long long)d->seq_len + d->first_position > 0x7fffffffLL || d->first_position < 0) {
+        set_error("positions must fit int32");
+        return EMS_INVALID_ARGUMENT;
+    }
+    return EMS_OK;
+}
+
+int ems_cache_dims_for(const ems_desc* d, ems_cache_dims* out) {
+    if (int rc = ems_validate(d)) return rc;
+    const Dims m = make_dims(*d);
+    out->units = m.units;
+    out->centers = m.cap_c;
+    out->locals = m.cap_l;
+    out->lut = m.cap_lut;
+    out->tbm = m.cap_tbm;
+    return EMS_OK;
+}
+
+size_t ems_workspace_bytes(const ems_desc* d) {
+    if (ems_validate(d) != EMS_OK) return 0;
+    return layout(*d).total;
+}
+
+int ems_score(const ems_desc* d, const void* q, const void* k, const void* v, void* out_o,
+              float* lse, float* glo, float* loc, void* ws, size_t ws_bytes, cudaStream_t s) {
+    if (int rc = ems_validate(d)) return rc;
+    if (int rc = check_ws(d, ws, ws_bytes)) return rc;
+    if (!q || !k || !glo || !loc || (out_o && !v)) {
+        set_error("ems_score: null tensor");
+        return EMS_INVALID_ARGUMENT;
+    }
+    return run_score(d, q, k, v, out_o, lse, glo, loc, ws, s);
+}
+
+int ems_select(const ems_desc* d, const float* glo, const float* loc, const ems_stage* st,
+               void* ws, size_t ws_bytes, cudaStream_t s) {
+    if (int rc = ems_validate(d)) return rc;
+    if (int rc = check_ws(d, ws, ws_bytes)) return rc;
+    if (d->seq_len <= d->n_budget) {
+        set_error("ems_select: prompt fits the budget (keep-all path has no partition)");
+        return EMS_INVALID_ARGUMENT;
+    }
+    EMS_CUDA_CHECK(cudaMemsetAsync(ws, 0, sizeof(DevStatus), s));
+    const ems_stage sg = st ? *st : default_stage(*d, ws);
+    return run_select(d, glo, loc, sg, ws, s);
+}
+
+int ems_merge(const ems_desc* d, const void* k_raw, const void* v, const ems_stage* st, void* ws,
+              size_t ws_bytes, cudaStream_t s) {
+    if (int rc = ems_validate(d)) return rc;
+    if (int rc = check_ws(d, ws, ws_bytes)) return rc;
+    const ems_stage sg = st ? *st : default_stage(*d, ws);
+    return run_merge(d, k_raw, v, sg, ws, s);
+}
+
+int ems_compact(const ems_desc* d, const void* k_raw, const void* v, const float* glo,
+                const float* loc, const ems_stage* st, const ems_cache* c, void* ws,
+                size_t ws_bytes, cudaStream_t s) {
+    if (int rc = ems_validate(d)) return rc;
+    if (int rc = check_ws(d, ws, ws_bytes)) return rc;
+    if (!c) {
+        set_error("ems_compact: null cache");
+        return EMS_INVALID_ARGUMENT;
+    }
+    const ems_stage sg = st ? *st : default_stage(*d, ws);
+    return run_compact(d, k_raw, v, glo, loc, sg, *c, ws, s);
+}
+
+int ems_prefill_compress(const ems_desc* d, const void* q_rot, const void* k_rot,
+                         const void* k_raw, const void* v, void* out_o, float* lse, float* glo,
+                         float* loc, const ems_stage* st, const ems_cache* c, void* ws,
+                         size_t ws_bytes, cudaStream_t s) {
+    if (int rc = ems_validate(d)) return rc;
+    if (int rc = check_ws(d, ws, ws_bytes)) return rc;
+    if (!q_rot || !k_rot || !k_raw || !v || !c) {
+        set_error("ems_prefill_compress: null tensor");
+        return EMS_INVALID_ARGUMENT;
+    }
+    const Layout l = layout(*d);
+    EMS_CUDA_CHECK(cudaMemsetAsync(ws, 0, sizeof(DevStatus), s));
+    float* g = glo ? glo : at<float>(ws, l.glo);
+    float* lc = loc ? loc : at<float>(ws, l.loc);
+    const ems_stage sg = st ? *st : default_stage(*d, ws);
+    if (int rc = run_score(d, q_rot, k_rot, v, out_o, lse, g, lc, ws, s)) return rc;
+    if (d->seq_len > d->n_budget) {  // policies.cpp:136-138: keep-all when n <= n_budget
+        if (int rc = run_select(d, g, lc, sg, ws, s)) return rc;
+        if (int rc = run_merge(d, k_raw, v, sg, ws, s)) return rc;
+    }
+    return run_compact(d, k_raw, v, g, lc, sg, *c, ws, s);
+}
+
+int ems_redundancy_cross(int32_t dtype, int32_t d, const void* k_rows, const void* v_rows,
+                         int32_t n_rows, const void* k_cols, const void* v_cols, int32_t n_cols,
+                         int32_t key_only, float* r, cudaStream_t s) {
+    if ((dtype != EMS_F32 && dtype != EMS_BF16) || !supported_dim(d) || n_rows < 0 || n_cols < 0) {
+        set_error("ems_redundancy_cross: bad arguments");
+        return EMS_INVALID_ARGUMENT;
+    }
+    if (n_rows == 0 || n_cols == 0) return EMS_OK;
+    cudaError_t e = launch_redundancy_cross(dtype, d, k_rows, v_rows, n_rows, k_cols, v_cols,
+                                            n_cols, key_only, r, s);
+    if (e != cudaSuccess) {
+        set_error("redundancy_cross launch: %s", cudaGetErrorString(e));
+        return EMS_CUDA_ERROR;
+    }
+    return EMS_OK;
+}
+
+int ems_sync_status(const ems_desc* d, void* ws, cudaStream_t s) {
+    (void)d;
+    EMS_CUDA_CHECK(cudaStreamSynchronize(s));
+    DevStatus st;
+    EMS_CUDA_CHECK(cudaMemcpy(&st, ws, sizeof(st), cudaMemcpyDeviceToHost));
+    if (st.code != 0) {
+        set_error("device reported %s in unit %d", ems_status_string(st.code), st.unit);
+        return st.code;
+    }
+    return EMS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,101 @@
+// common.cuh -- shared helpers for the EMS sm_100a kernels.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "ems_b200.h"
+
+namespace ems {
+
+constexpr int kWarp = 32;
+
+// Device-side status word (first 16 bytes of the workspace).
+struct DevStatus {
+    int32_t code;  // first error recorded (atomicCAS from 0)
+    int32_t unit;
+    int32_t pad[2];
+};
+
+__device__ __forceinline__ void record_status(DevStatus* st, int code, int unit) {
+    if (atomicCAS(&st->code, 0, code) == 0) st->unit = unit;
+}
+
+template <typename T>
+struct Elem;
+template <>
+struct Elem<float> {
+    static __device__ __forceinline__ float load(const float* p) { return *p; }
+    static __device__ __forceinline__ float to_float(float x) { return x; }
+    static __device__ __forceinline__ float from_float(float x) { return x; }
+};
+template <>
+struct Elem<__nv_bfloat16> {
+    static __device__ __forceinline__ float load(const __nv_bfloat16* p) {
+        return __bfloat162float(*p);
+    }
+    static __device__ __forceinline__ float to_float(__nv_bfloat16 x) { return __bfloat162float(x); }
+    static __device__ __forceinline__ __nv_bfloat16 from_float(float x) {
+        return __float2bfloat16_rn(x);
+    }
+};
+
+template <typename T>
+__device__ __forceinline__ float ld(const T* p) {
+    return Elem<T>::load(p);
+}
+template <typename T>
+__device__ __forceinline__ void st(T* p, float x) {
+    *p = Elem<T>::from_float(x);
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// Host-side helpers shared by the launchers.
+struct Dims {
+    int B, Hq, Hkv, G, L, d, units;
+    int lwin_scores;   // min(l_win, L)
+    int cap_c, cap_l, cap_lut, cap_tbm;
+    size_t esize;      // bytes per element of the dtype
+};
+
+Dims make_dims(const ems_desc& d);
+
+void set_error(const char* fmt, ...);
+
+#define EMS_CUDA_CHECK(expr)                                                          \
+    do {                                                                              \
+        cudaError_t _e = (expr);                                                      \
+        if (_e != cudaSuccess) {                                                      \
+            ::ems::set_error("%s:%d %s: %s", __FILE__, __LINE__, #expr,               \
+                             cudaGetErrorString(_e));                                 \
+            return EMS_CUDA_ERROR;                                                    \
+        }                                                                             \
+    } while (0)
+
+#define EMS_LAUNCH_CHECK()                                                            \
+    do {                                                                              \
+        cudaError_t _e = cudaGetLastError();                                          \
+        if (_e != cudaSuccess) {                                                      \
+            ::ems::set_error("%s:%d launch: %s", __FILE__, __LINE__,                  \
+                             cudaGetErrorString(_e));                                 \
+            return EMS_CUDA_ERROR;                                                    \
+        }                                                                             \
+    } while (0)
+
+}  // namespace ems

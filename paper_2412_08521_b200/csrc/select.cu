@@ -1,0 +1,219 @@
+// select.cu -- kernel (2): scale alignment + combine + mean-pool + exact top-k
+// partition of the candidate tokens, one CTA per unit.
+//
+// Reference semantics (all per head/unit):
+//   effective_score  proj/src/scoring.cpp:146-152 ->
+//     combine_glo_loc  scoring.cpp:105-124: align = sum(loc)/sum(glo) over ALL L tokens,
+//                      s_i = max(glo_i * align, loc_i);  sum(glo) <= 0 -> DegenerateInputError
+//     mean_pool_1d     numerics.cpp:62-82: centred window, truncated at the edges
+//   clamp_kernel       compressor.cpp:29-34 (done on the host)
+//   partition_tokens   compressor.cpp:48-74: candidates [0, L-w); stable sort by
+//                      pooled desc (ties -> lower index); top n_imp important, next
+//                      n_tbm to-be-merged, rest irrelevant; each set ascending.
+//
+// The stable-sort order is reproduced exactly by ranking the unique 64-bit key
+//   key_i = (bits(pooled_i as f32) << 32) | (0xFFFFFFFF - i)
+// (pooled >= 0, so f32 bit patterns order like the values; the low word breaks
+// ties toward the lower index).  An MSD radix select (8 passes of 8 bits, two
+// targets at once) finds the n_imp-th and (n_imp+n_tbm)-th largest keys; every
+// token is then classified by comparison, and ascending index lists come out of
+// a block-wide prefix sum.  Integer histograms make the result deterministic.
+#include "common.cuh"
+
+namespace ems {
+
+namespace {
+
+constexpr int kSelThreads = 1024;
+constexpr int kSelWarps = kSelThreads / 32;
+
+__device__ __forceinline__ unsigned long long sel_key(const float* pooled, int i) {
+    return ((unsigned long long)__float_as_uint(pooled[i]) << 32) |
+           (unsigned long long)(0xFFFFFFFFu - (unsigned)i);
+}
+
+// Block-wide fixed-order sum of per-thread doubles (deterministic).
+__device__ double block_sum(double v, double* sh) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    v = warp_sum(v);
+    if (lane == 0) sh[warp] = v;
+    __syncthreads();
+    double t = 0.0;
+    if (warp == 0) {
+        t = lane < kSelWarps ? sh[lane] : 0.0;
+        t = warp_sum(t);
+        if (lane == 0) sh[0] = t;
+    }
+    __syncthreads();
+    t = sh[0];
+    __syncthreads();
+    return t;
+}
+
+// Given a 256-bin histogram and a 1-based rank `rem` counted from the top bin,
+// returns the bin holding that rank and the count strictly above it (one warp).
+__device__ void find_bin(const int* hist, int rem, int* out_bin, int* out_above) {
+    const int lane = threadIdx.x & 31;
+    // lane l owns bins 255-8l ... 248-8l (descending)
+    int c[8], tot = 0;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) c[t] = hist[255 - 8 * lane - t], tot += c[t];
+    int incl = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int n = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += n;
+    }
+    const int excl = incl - tot;
+    const unsigned ballot = __ballot_sync(0xffffffffu, excl < rem && rem <= incl);
+    const int owner = __ffs(ballot) - 1;
+    if (lane == owner) {
+        int run = excl;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+            if (run < rem && rem <= run + c[t]) {
+                *out_bin = 255 - 8 * lane - t;
+                *out_above = run;
+                break;
+            }
+            run += c[t];
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kSelThreads) select_kernel(
+    const float* __restrict__ glo, const float* __restrict__ loc, int L, int l_win, int n_imp,
+    int n_tbm, int kernel, float* __restrict__ pooled_all, int8_t* __restrict__ cls_all,
+    int32_t* __restrict__ imp_idx_all, int32_t* __restrict__ tbm_idx_all,
+    int32_t* __restrict__ counts_all, int cap_c, int cap_tbm, DevStatus* status) {
+    __shared__ double sh[32];
+    __shared__ int hist[2][256];
+    __shared__ int sel_bin[2], sel_above[2];
+    __shared__ int scan[2][kSelThreads];
+    __shared__ int degenerate;
+    const int u = blockIdx.x;
+    const int tid = threadIdx.x;
+    const float* g = glo + (size_t)u * L;
+    const float* lo = loc + (size_t)u * L;
+    float* pooled = pooled_all + (size_t)u * L;
+
+    // 1. alignment sums over all L tokens (fp64)
+    double sg = 0.0, sl = 0.0;
+    for (int i = tid; i < L; i += kSelThreads) sg += (double)g[i], sl += (double)lo[i];
+    sg = block_sum(sg, sh);
+    sl = block_sum(sl, sh);
+    if (tid == 0) degenerate = !(sg > 0.0);
+    __syncthreads();
+    if (degenerate) {
+        if (tid == 0) record_status(status, EMS_DEGENERATE_INPUT, u);
+        return;
+    }
+    const double align = sl / sg;
+
+    // 2. combine + centred mean pool with truncated edges (fp64), stored as f32
+    const int half = kernel / 2;
+    for (int i = tid; i < L; i += kSelThreads) {
+        const int a = max(0, i - half), bnd = min(L - 1, i + half);
+        double acc = 0.0;
+        for (int jj = a; jj <= bnd; ++jj) {
+            const double x = (double)g[jj] * align, y = (double)lo[jj];
+            acc += x > y ? x : y;
+        }
+        pooled[i] = (float)(acc / (double)(bnd - a + 1));
+    }
+    __syncthreads();
+
+    // 3. radix select of the k1-th and k2-th largest candidate keys
+    const int n_cand = L - l_win;
+    const int k1 = n_imp, k2 = n_imp + n_tbm;
+    unsigned long long pre[2] = {0ull, 0ull};
+    int rem[2] = {k1, k2};
+    for (int pass = 0; pass < 8; ++pass) {
+        const int shift = 56 - 8 * pass;
+        const unsigned long long hi_mask = pass == 0 ? 0ull : (~0ull << (shift + 8));
+        for (int e = tid; e < 512; e += kSelThreads) (&hist[0][0])[e] = 0;
+        __syncthreads();
+        for (int i = tid; i < n_cand; i += kSelThreads) {
+            const unsigned long long key = sel_key(pooled, i);
+            const int bin = (int)((key >> shift) & 255ull);
+            if ((key & hi_mask) == pre[0]) atomicAdd(&hist[0][bin], 1);
+            if ((key & hi_mask) == pre[1]) atomicAdd(&hist[1][bin], 1);
+        }
+        __syncthreads();
+        const int warp = tid >> 5;
+        if (warp < 2) find_bin(hist[warp], rem[warp], &sel_bin[warp], &sel_above[warp]);
+        __syncthreads();
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+            pre[t] |= (unsigned long long)sel_bin[t] << shift;
+            rem[t] -= sel_above[t];
+        }
+        __syncthreads();
+    }
+    const unsigned long long T1 = pre[0];
+    const unsigned long long T2 = n_tbm > 0 ? pre[1] : pre[0];
+
+    // 4. classify + ascending index lists via a block-wide exclusive scan
+    int8_t* cls = cls_all + (size_t)u * L;
+    int32_t* imp_idx = imp_idx_all + (size_t)u * cap_c;
+    int32_t* tbm_idx = tbm_idx_all + (size_t)u * cap_tbm;
+    const int per = (L + kSelThreads - 1) / kSelThreads;
+    const int s0 = min(L, tid * per), s1 = min(L, s0 + per);
+    int ci = 0, ct = 0;
+    for (int i = s0; i < s1; ++i) {
+        if (i < n_cand) {
+            const unsigned long long key = sel_key(pooled, i);
+            ci += key >= T1;
+            ct += (key < T1 && key >= T2);
+        }
+    }
+    scan[0][tid] = ci;
+    scan[1][tid] = ct;
+    __syncthreads();
+    // Hillis-Steele inclusive scan (1024 entries, two arrays)
+    for (int o = 1; o < kSelThreads; o <<= 1) {
+        const int a = tid >= o ? scan[0][tid - o] : 0;
+        const int b = tid >= o ? scan[1][tid - o] : 0;
+        __syncthreads();
+        scan[0][tid] += a;
+        scan[1][tid] += b;
+        __syncthreads();
+    }
+    int ri = scan[0][tid] - ci, rt = scan[1][tid] - ct;
+    for (int i = s0; i < s1; ++i) {
+        int8_t c = 3;
+        if (i < n_cand) {
+            const unsigned long long key = sel_key(pooled, i);
+            if (key >= T1) {
+                c = 2;
+                imp_idx[ri++] = i;
+            } else if (key >= T2) {
+                c = 1;
+                tbm_idx[rt++] = i;
+            } else {
+                c = 0;
+            }
+        }
+        cls[i] = c;
+    }
+    if (tid == 0) {
+        int32_t* cnt = counts_all + 4 * u;
+        cnt[0] = n_imp;
+        cnt[1] = n_tbm;
+        cnt[2] = n_cand - n_imp - n_tbm;
+        cnt[3] = l_win;
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_select(const Dims& dm, int l_win, int n_imp, int n_tbm, int kernel,
+                          const float* glo, const float* loc, const ems_stage& sg,
+                          DevStatus* status, cudaStream_t s) {
+    select_kernel<<<dm.units, kSelThreads, 0, s>>>(glo, loc, dm.L, l_win, n_imp, n_tbm, kernel,
+                                                   sg.pooled, sg.cls, sg.imp_idx, sg.tbm_idx,
+                                                   sg.part_counts, dm.cap_c, dm.cap_tbm, status);
+    return cudaGetLastError();
+}
+
+}  // namespace ems

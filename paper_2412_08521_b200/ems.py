@@ -1,0 +1,309 @@
+"""Python front-end over the C ABI (include/ems_b200.h) of libems_b200.so.
+
+PyTorch supplies device memory and the current stream; all compute runs in the
+hand-written sm_100a kernels of libems_b200.so.  There is no fallback: if the
+library (or a GPU) is missing, every entry point raises.
+
+The functions mirror the reference operator API (proj/include/ems/*.hpp):
+``prefill_attention`` / ``prefill_scores`` (scoring.hpp:48-54),
+``redundancy_cross`` (analysis.hpp:19-20) and ``compress_prefill`` /
+``prefill`` (compressor.hpp:58-60, engine.cpp:42-82), batched over
+[B][H][L][d] tensors.  Errors map to the reference's exception types.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import torch
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libems_b200.so")
+
+EMS_F32, EMS_BF16 = 0, 1
+SCORE_IMPL = {"auto": 0, "simt": 1, "tcgen05": 2}
+
+
+class EmsError(RuntimeError):
+    pass
+
+
+class InvalidArgument(EmsError, ValueError):
+    """std::invalid_argument in the reference."""
+
+
+class DegenerateInputError(EmsError):
+    """ems::DegenerateInputError (proj/include/ems/errors.hpp:11-16)."""
+
+
+class CorruptionError(EmsError):
+    """ems::CorruptionError (proj/include/ems/errors.hpp:32-36)."""
+
+
+class CudaError(EmsError):
+    pass
+
+
+class Unsupported(EmsError):
+    pass
+
+
+_ERR = {1: InvalidArgument, 2: DegenerateInputError, 3: CorruptionError, 4: CudaError, 5: Unsupported}
+
+
+class Desc(C.Structure):
+    _fields_ = [("batch", C.c_int32), ("heads_q", C.c_int32), ("heads_kv", C.c_int32),
+                ("seq_len", C.c_int32), ("head_dim", C.c_int32), ("dtype", C.c_int32),
+                ("l_win", C.c_int32), ("n_budget", C.c_int32), ("tau", C.c_double),
+                ("gamma", C.c_double), ("kernel_size", C.c_int32), ("zero_class", C.c_int32),
+                ("key_only", C.c_int32), ("score_impl", C.c_int32), ("first_position", C.c_int64)]
+
+
+class CacheDims(C.Structure):
+    _fields_ = [("units", C.c_int32), ("centers", C.c_int32), ("locals", C.c_int32),
+                ("lut", C.c_int32), ("tbm", C.c_int32)]
+
+
+class CCache(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in ("center_key", "center_norm", "center_value", "center_pos",
+                                          "center_score", "local_key", "local_value", "local_pos",
+                                          "local_score", "lut_pos", "lut_slot", "counts")]
+
+
+class CStage(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in ("pooled", "cls", "imp_idx", "tbm_idx", "part_counts",
+                                          "dest")]
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load libems_b200.so; fail loudly when it is absent (no CPU fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_2412_08521_b200.build`")
+        L = C.CDLL(LIB_PATH)
+        L.ems_last_error.restype = C.c_char_p
+        L.ems_status_string.restype = C.c_char_p
+        L.ems_workspace_bytes.restype = C.c_size_t
+        L.ems_workspace_bytes.argtypes = [C.POINTER(Desc)]
+        L.ems_validate.argtypes = [C.POINTER(Desc)]
+        L.ems_cache_dims_for.argtypes = [C.POINTER(Desc), C.POINTER(CacheDims)]
+        vp, fp = C.c_void_p, C.c_void_p
+        L.ems_score.argtypes = [C.POINTER(Desc), vp, vp, vp, vp, fp, fp, fp, vp, C.c_size_t, vp]
+        L.ems_select.argtypes = [C.POINTER(Desc), fp, fp, C.POINTER(CStage), vp, C.c_size_t, vp]
+        L.ems_merge.argtypes = [C.POINTER(Desc), vp, vp, C.POINTER(CStage), vp, C.c_size_t, vp]
+        L.ems_compact.argtypes = [C.POINTER(Desc), vp, vp, fp, fp, C.POINTER(CStage),
+                                  C.POINTER(CCache), vp, C.c_size_t, vp]
+        L.ems_prefill_compress.argtypes = [C.POINTER(Desc), vp, vp, vp, vp, vp, fp, fp, fp,
+                                           C.POINTER(CStage), C.POINTER(CCache), vp, C.c_size_t, vp]
+        L.ems_redundancy_cross.argtypes = [C.c_int32, C.c_int32, vp, vp, C.c_int32, vp, vp,
+                                           C.c_int32, C.c_int32, fp, vp]
+        L.ems_sync_status.argtypes = [C.POINTER(Desc), vp, vp]
+        _lib = L
+    return _lib
+
+
+def _check(rc: int) -> None:
+    if rc != 0:
+        msg = lib().ems_last_error().decode()
+        raise _ERR.get(rc, EmsError)(msg or f"status {rc}")
+
+
+def _p(t: torch.Tensor | None):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+@dataclass(frozen=True)
+class EmsConfig:
+    """CompressionConfig (proj/include/ems/cache.hpp:20-39) plus the D1 similarity flag."""
+    n_budget: int = 256
+    l_win: int = 32
+    tau: float = 0.6
+    gamma: float = 4.0
+    kernel_size: int = 7
+    zero_class: bool = True
+    key_only: bool = False
+
+    def center_capacity(self) -> int:
+        return self.n_budget - self.l_win
+
+    def tbm_target(self) -> int:
+        return int((self.gamma - 1.0) * float(self.n_budget))
+
+
+def _dtype_code(t: torch.dtype) -> int:
+    if t == torch.float32:
+        return EMS_F32
+    if t == torch.bfloat16:
+        return EMS_BF16
+    raise InvalidArgument(f"unsupported dtype {t} (float32 or bfloat16)")
+
+
+def make_desc(B: int, Hq: int, Hkv: int, L: int, d: int, dtype: torch.dtype, cfg: EmsConfig,
+              score_impl: str = "auto", first_position: int = 0) -> Desc:
+    return Desc(B, Hq, Hkv, L, d, _dtype_code(dtype), cfg.l_win, cfg.n_budget, float(cfg.tau),
+                float(cfg.gamma), cfg.kernel_size, int(cfg.zero_class), int(cfg.key_only),
+                SCORE_IMPL[score_impl], first_position)
+
+
+class Plan:
+    """Pre-allocated buffers for one problem shape: workspace, stage, cache, scores.
+
+    Construct once, then ``run`` as often as needed (no allocation on the hot path)."""
+
+    def __init__(self, B: int, Hq: int, Hkv: int, L: int, d: int, dtype: torch.dtype,
+                 cfg: EmsConfig, device=None, score_impl: str = "auto", want_out: bool = True,
+                 want_lse: bool = False, first_position: int = 0):
+        self.device = torch.device(device or "cuda")
+        self.desc = make_desc(B, Hq, Hkv, L, d, dtype, cfg, score_impl, first_position)
+        self.cfg, self.dtype = cfg, dtype
+        L_ = lib()
+        _check(L_.ems_validate(C.byref(self.desc)))
+        dims = CacheDims()
+        _check(L_.ems_cache_dims_for(C.byref(self.desc), C.byref(dims)))
+        self.dims = dims
+        U = dims.units
+        dev = self.device
+        nbytes = L_.ems_workspace_bytes(C.byref(self.desc))
+        self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+        mk = lambda *s, dt=torch.float32: torch.zeros(s, dtype=dt, device=dev)  # noqa: E731
+        self.glo = mk(B, Hkv, L)
+        self.loc = mk(B, Hkv, L)
+        self.out = torch.empty((B, Hq, L, d), dtype=dtype, device=dev) if want_out else None
+        self.lse = mk(B, Hq, L) if want_lse else None
+        tb = max(dims.tbm, 1)
+        self.stage = dict(pooled=mk(U, L), cls=mk(U, L, dt=torch.int8),
+                          imp_idx=mk(U, dims.centers, dt=torch.int32),
+                          tbm_idx=mk(U, tb, dt=torch.int32),
+                          part_counts=mk(U, 4, dt=torch.int32), dest=mk(U, tb, dt=torch.int32))
+        self.cache = dict(center_key=mk(U, dims.centers, d, dt=dtype),
+                          center_norm=mk(U, dims.centers),
+                          center_value=mk(U, dims.centers, d, dt=dtype),
+                          center_pos=mk(U, dims.centers, dt=torch.int32),
+                          center_score=mk(U, dims.centers, 3),
+                          local_key=mk(U, dims.locals, d, dt=dtype),
+                          local_value=mk(U, dims.locals, d, dt=dtype),
+                          local_pos=mk(U, dims.locals, dt=torch.int32),
+                          local_score=mk(U, dims.locals, 3),
+                          lut_pos=mk(U, max(dims.lut, 1), dt=torch.int32),
+                          lut_slot=mk(U, max(dims.lut, 1), dt=torch.int32),
+                          counts=mk(U, 4, dt=torch.int32))
+        self._cstage = CStage(*[_p(self.stage[f]) for f, _ in CStage._fields_])
+        self._ccache = CCache(*[_p(self.cache[f]) for f, _ in CCache._fields_])
+
+    def _check_inputs(self, q_rot, k_rot, k_raw, v):
+        D = self.desc
+        want_q = (D.batch, D.heads_q, D.seq_len, D.head_dim)
+        want_k = (D.batch, D.heads_kv, D.seq_len, D.head_dim)
+        for name, t, shp in (("q_rot", q_rot, want_q), ("k_rot", k_rot, want_k),
+                             ("k_raw", k_raw, want_k), ("v", v, want_k)):
+            if t is None:
+                continue
+            if tuple(t.shape) != shp or t.dtype != self.dtype or not t.is_contiguous() \
+                    or t.device != self.device and t.device.type != "cuda":
+                raise InvalidArgument(f"{name}: want contiguous {shp} {self.dtype} on cuda, got "
+                                      f"{tuple(t.shape)} {t.dtype} {t.device}")
+
+    def run(self, q_rot, k_rot, k_raw, v, stream=None) -> None:
+        """Whole path (ems_prefill_compress), asynchronous on the current stream."""
+        self._check_inputs(q_rot, k_rot, k_raw, v)
+        _check(lib().ems_prefill_compress(C.byref(self.desc), _p(q_rot), _p(k_rot), _p(k_raw), _p(v),
+                                          _p(self.out), _p(self.lse), _p(self.glo), _p(self.loc),
+                                          C.byref(self._cstage), C.byref(self._ccache),
+                                          _p(self.workspace), self.workspace.numel(),
+                                          _stream(stream)))
+
+    def score(self, q_rot, k_rot, v=None, stream=None) -> None:
+        self._check_inputs(q_rot, k_rot, None, v)
+        _check(lib().ems_score(C.byref(self.desc), _p(q_rot), _p(k_rot), _p(v),
+                               _p(self.out) if v is not None else None, _p(self.lse), _p(self.glo),
+                               _p(self.loc), _p(self.workspace), self.workspace.numel(),
+                               _stream(stream)))
+
+    def select(self, stream=None) -> None:
+        _check(lib().ems_select(C.byref(self.desc), _p(self.glo), _p(self.loc), C.byref(self._cstage),
+                                _p(self.workspace), self.workspace.numel(), _stream(stream)))
+
+    def merge(self, k_raw, v, stream=None) -> None:
+        _check(lib().ems_merge(C.byref(self.desc), _p(k_raw), _p(v), C.byref(self._cstage),
+                               _p(self.workspace), self.workspace.numel(), _stream(stream)))
+
+    def compact(self, k_raw, v, stream=None) -> None:
+        _check(lib().ems_compact(C.byref(self.desc), _p(k_raw), _p(v), _p(self.glo), _p(self.loc),
+                                 C.byref(self._cstage), C.byref(self._ccache), _p(self.workspace),
+                                 self.workspace.numel(), _stream(stream)))
+
+    def sync_status(self, stream=None) -> None:
+        """Synchronise and raise the first data-dependent error the kernels recorded."""
+        _check(lib().ems_sync_status(C.byref(self.desc), _p(self.workspace), _stream(stream)))
+
+    def unit_cache(self, u: int) -> dict:
+        """Host copy of unit u's compressed cache, trimmed to its counts."""
+        cnt = self.cache["counts"][u].tolist()
+        nc, nl, nu, comp = cnt
+        g = lambda k: self.cache[k][u].cpu()  # noqa: E731
+        return dict(compressed=bool(comp),
+                    unit_key=g("center_key")[:nc].double().numpy(),
+                    key_norm=g("center_norm")[:nc].double().numpy(),
+                    value=g("center_value")[:nc].double().numpy(),
+                    position=g("center_pos")[:nc].long().numpy(),
+                    score=g("center_score")[:nc].double().numpy(),
+                    local_key=g("local_key")[:nl].double().numpy(),
+                    local_value=g("local_value")[:nl].double().numpy(),
+                    local_position=g("local_pos")[:nl].long().numpy(),
+                    local_score=g("local_score")[:nl].double().numpy(),
+                    lut_position=g("lut_pos")[:nu].long().numpy(),
+                    lut_slot=g("lut_slot")[:nu].numpy())
+
+
+# -- reference-shaped conveniences ----------------------------------------------------
+def prefill_compress(q_rot, k_rot, k_raw, v, cfg: EmsConfig, want_out=True, score_impl="auto",
+                     first_position=0) -> Plan:
+    """engine::prefill's score -> compress sequence (engine.cpp:42-82) on [B][H][L][d] tensors.
+    Returns the Plan holding O, glo/loc, the stage buffers and the compressed cache."""
+    B, Hq, L, d = q_rot.shape
+    Hkv = k_rot.shape[1]
+    plan = Plan(B, Hq, Hkv, L, d, q_rot.dtype, cfg, q_rot.device, score_impl, want_out,
+                first_position=first_position)
+    plan.run(q_rot, k_rot, k_raw, v)
+    plan.sync_status()
+    return plan
+
+
+def prefill_attention(q_rot, k_rot, v, l_win: int, score_impl="auto"):
+    """prefill_attention (scoring.hpp:52-54), batched + GQA-mean: returns (O, glo, loc)."""
+    B, Hq, L, d = q_rot.shape
+    cfg = EmsConfig(n_budget=max(l_win + 1, 2), l_win=max(l_win, 1), gamma=1.0, kernel_size=1)
+    plan = Plan(B, Hq, k_rot.shape[1], L, d, q_rot.dtype, cfg, q_rot.device, score_impl, True)
+    plan.score(q_rot, k_rot, v)
+    torch.cuda.current_stream().synchronize()
+    return plan.out, plan.glo, plan.loc
+
+
+def prefill_scores(q_rot, k_rot, l_win: int, score_impl="auto"):
+    """prefill_scores (scoring.hpp:48-49): returns (glo, loc)."""
+    B, Hq, L, d = q_rot.shape
+    cfg = EmsConfig(n_budget=max(l_win + 1, 2), l_win=max(l_win, 1), gamma=1.0, kernel_size=1)
+    plan = Plan(B, Hq, k_rot.shape[1], L, d, q_rot.dtype, cfg, q_rot.device, score_impl, False)
+    plan.score(q_rot, k_rot, None)
+    torch.cuda.current_stream().synchronize()
+    return plan.glo, plan.loc
+
+
+def redundancy_cross(k_rows, v_rows, k_cols, v_cols, key_only=False) -> torch.Tensor:
+    """redundancy_cross (analysis.hpp:19-20) on device tensors [n][d] -> fp32 [n_rows][n_cols]."""
+    nr, d = k_rows.shape
+    nc = k_cols.shape[0]
+    r = torch.empty((nr, nc), dtype=torch.float32, device=k_rows.device)
+    _check(lib().ems_redundancy_cross(_dtype_code(k_rows.dtype), d, _p(k_rows), _p(v_rows), nr,
+                                      _p(k_cols), _p(v_cols), nc, int(key_only), _p(r), _stream()))
+    return r

@@ -1,0 +1,184 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle on identical inputs.
+
+Bars (BASELINE.json north_star; see tests/parity.py):
+  * important / TBM sets bit-exact outside the 1e-5 cut band,
+  * merge destinations identical outside the 1e-5 R band,
+  * merged K/V and scores within 2e-2 (bf16) / 1e-4 (fp32) per-row relative error,
+  * glo/loc within SCORE_RTOL of the fp64 oracle (the scores feed the cut).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+from oracle.oracle import Cache, Config  # noqa: E402
+from paper_2412_08521_b200 import ems  # noqa: E402
+from paper_2412_08521_b200.inputs import CONFIGS, make_unit_np, rope_np, round_to  # noqa: E402
+from tests.parity import compare_unit  # noqa: E402
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+SCORE_RTOL = {"f32": 2e-5, "bf16": 2e-5}
+
+
+def _tdt(dtype):
+    return torch.float32 if dtype == "f32" else torch.bfloat16
+
+
+def run_gpu(units, dtype, cfg: Config, score_impl="auto"):
+    """units: list of UnitInputs-like (q_rot [G,n,d], k_rot, k_raw, v [n,d]) -> Plan (B=1, H_kv=U)."""
+    dev = torch.device("cuda")
+    t = lambda a: torch.tensor(np.stack(a), dtype=torch.float64).to(_tdt(dtype)).to(dev)  # noqa: E731
+    G, n, d = units[0].q_rot.shape
+    q = t([u.q_rot for u in units]).reshape(1, len(units) * G, n, d).contiguous()
+    kr = t([u.k_rot for u in units]).reshape(1, len(units), n, d).contiguous()
+    kw = t([u.k_raw for u in units]).reshape(1, len(units), n, d).contiguous()
+    v = t([u.v for u in units]).reshape(1, len(units), n, d).contiguous()
+    ecfg = ems.EmsConfig(cfg.n_budget, cfg.l_win, cfg.tau, cfg.gamma, cfg.kernel_size,
+                         cfg.zero_class, cfg.key_only)
+    plan = ems.prefill_compress(q, kr, kw, v, ecfg, want_out=True, score_impl=score_impl)
+    torch.cuda.synchronize()
+    return plan
+
+
+class U:  # minimal UnitInputs
+    def __init__(self, q_rot, k_rot, k_raw, v):
+        self.q_rot, self.k_rot, self.k_raw, self.v = q_rot, k_rot, k_raw, v
+
+
+def check_unit(plan, u, unit_in, ref_cache: Cache, glo_ref, loc_ref, dtype, cfg: Config, oracle,
+               out_ref=None):
+    n = unit_in.k_raw.shape[0]
+    glo = plan.glo[0, u].double().cpu().numpy()
+    loc = plan.loc[0, u].double().cpu().numpy()
+    g_err = np.max(np.abs(glo - glo_ref) / np.maximum(glo_ref, 1e-30))
+    l_mask = loc_ref > 1e-6
+    l_err = np.max(np.abs(loc - loc_ref)[l_mask] / loc_ref[l_mask]) if l_mask.any() else 0.0
+    assert g_err <= SCORE_RTOL[dtype], f"glo rel err {g_err}"
+    assert l_err <= SCORE_RTOL[dtype] * 10, f"loc rel err {l_err}"
+    if out_ref is not None:
+        G = unit_in.q_rot.shape[0]
+        o = plan.out[0, u * G:(u + 1) * G].double().cpu().numpy()
+        tol = 1e-4 if dtype == "f32" else 2e-2
+        err = np.max(np.linalg.norm(o - out_ref, axis=-1) / np.maximum(np.linalg.norm(out_ref, axis=-1), 1e-30))
+        assert err <= tol, f"attention output rel err {err}"
+    # reference R on the reference's own TBM set, for the destination exclusion band
+    r_ref, tbm_ref = None, None
+    if ref_cache.compressed and "cls" in ref_cache.extra:
+        cls = ref_cache.extra["cls"]
+        tbm_ref = np.nonzero(cls == 1)[0]
+        imp_ref = np.nonzero(cls == 2)[0]
+        if len(tbm_ref):
+            r_ref = oracle.redundancy_cross(unit_in.k_raw[tbm_ref], unit_in.v[tbm_ref],
+                                            unit_in.k_raw[imp_ref], unit_in.v[imp_ref], cfg.key_only)
+    pooled_ref = ref_cache.extra.get("pooled")
+    if pooled_ref is None:
+        pooled_ref = oracle.effective_score(glo_ref, loc_ref, np.zeros(n), min(cfg.kernel_size, n))
+    return compare_unit(plan.unit_cache(u), ref_cache, dtype, pooled_ref, cfg, n, r_ref, tbm_ref)
+
+
+# ---------------------------------------------------------------------------------------
+def test_gpu_golden_cache(oracle):
+    """The reference's golden fixture, through the GPU path (fp32 inputs, d = 8)."""
+    tr = np.load(os.path.join(GOLDEN, "golden_trace.npz"))
+    with open(os.path.join(GOLDEN, "golden_cache.json")) as f:
+        want = Cache.from_dump_json(f.read())
+    cfg = Config(n_budget=12, l_win=4, tau=0.6, gamma=2.0, kernel_size=3)
+    units = []
+    for h in range(2):
+        q_rot = round_to(rope_np(tr["q"][h], 10000.0), "f32")
+        k_rot = round_to(rope_np(tr["k"][h], 10000.0), "f32")
+        units.append(U(q_rot[None], k_rot, tr["k"][h], tr["v"][h]))
+    plan = run_gpu(units, "f32", cfg)
+    ref0 = oracle.prefill_unit(units[0].q_rot, units[0].k_rot, units[0].k_raw, units[0].v, cfg)
+    rep = check_unit(plan, 0, units[0], ref0, ref0.extra["glo"], ref0.extra["loc"], "f32", cfg, oracle)
+    # and directly against the fixture
+    got = plan.unit_cache(0)
+    np.testing.assert_array_equal(got["position"], want.position)
+    np.testing.assert_array_equal(got["lut_position"], want.lut_position)
+    np.testing.assert_array_equal(got["lut_slot"], want.lut_slot)
+    np.testing.assert_allclose(got["unit_key"], want.unit_key, rtol=1e-4, atol=1e-6)
+    np.testing.assert_allclose(got["score"], want.score, rtol=1e-4, atol=1e-7)
+    assert rep["excluded_tokens"] == 0
+
+
+with open(os.path.join(GOLDEN, "ref_cases.json")) as _f:
+    REF_META = json.load(_f)
+
+
+@pytest.mark.parametrize("name", sorted(REF_META))
+def test_gpu_reference_cases(name, oracle):
+    """Reference-generated fixtures (tests/golden/make_golden.py): merges, zero class,
+    explicit removal, keep-all, gamma = 1, tau = 0, GQA, bf16."""
+    meta = REF_META[name]
+    arr = np.load(os.path.join(GOLDEN, "ref_cases.npz"))
+    cfg = Config(**meta["config"])
+    u = U(arr[f"{name}/q_rot"], arr[f"{name}/k_rot"], arr[f"{name}/k_raw"], arr[f"{name}/v"])
+    plan = run_gpu([u], meta["dtype"], cfg)
+    ref = oracle.prefill_unit(u.q_rot, u.k_rot, u.k_raw, u.v, cfg)  # pinned == reference
+    ref_json = Cache.from_dump_json(meta["cache_json"])
+    np.testing.assert_array_equal(ref.lut_position, ref_json.lut_position)
+    check_unit(plan, 0, u, ref, arr[f"{name}/glo"], arr[f"{name}/loc"], meta["dtype"], cfg, oracle,
+               out_ref=arr[f"{name}/out"])
+
+
+def _cfg_of(w):
+    return Config(n_budget=w.n_budget, l_win=w.l_win, tau=w.tau, gamma=w.gamma,
+                  kernel_size=w.kernel_size)
+
+
+@pytest.mark.parametrize("wname,L,n_units", [("cfg1", None, 8), ("cfgM", 2048, 2), ("cfg3", 4096, 1),
+                                             ("cfg4", 2048, 4), ("cfg2", 2048, 2)])
+def test_gpu_configs_vs_oracle(wname, L, n_units, oracle):
+    """BASELINE configs (config 1 in full; the others at oracle-tractable L)."""
+    w = CONFIGS[wname]
+    units = [make_unit_np(w, seed=7, seq_len=L, unit=u) for u in range(n_units)]
+    cfg = _cfg_of(w)
+    plan = run_gpu(units, w.dtype, cfg)
+    reps = []
+    for i, un in enumerate(units):
+        ref = oracle.prefill_unit(un.q_rot, un.k_rot, un.k_raw, un.v, cfg)
+        reps.append(check_unit(plan, i, un, ref, ref.extra["glo"], ref.extra["loc"], w.dtype, cfg,
+                               oracle))
+    if wname == "cfgM":
+        assert all(r["merged"] > 0 and r["zero_class"] > 0 for r in reps), reps
+
+
+def test_gpu_determinism():
+    w = CONFIGS["cfgM"]
+    units = [make_unit_np(w, seed=3, seq_len=1024, unit=u) for u in range(2)]
+    a = run_gpu(units, w.dtype, _cfg_of(w))
+    b = run_gpu(units, w.dtype, _cfg_of(w))
+    for k in a.cache:
+        assert torch.equal(a.cache[k], b.cache[k]), k
+    assert torch.equal(a.glo, b.glo) and torch.equal(a.loc, b.loc)
+    assert torch.equal(a.out, b.out)
+
+
+def test_gpu_degenerate_input_raises():
+    """combine_glo_loc: zero global mass -> DegenerateInputError (scoring.cpp:115-117)."""
+    cfg = ems.EmsConfig(n_budget=8, l_win=2, gamma=2.0, kernel_size=3)
+    plan = ems.Plan(1, 1, 1, 64, 16, torch.float32, cfg, "cuda", want_out=False)
+    plan.glo.zero_()
+    plan.loc.fill_(1.0)
+    plan.select()
+    with pytest.raises(ems.DegenerateInputError):
+        plan.sync_status()
+
+
+def test_gpu_redundancy_cross_matches_oracle(oracle):
+    rng = np.random.default_rng(5)
+    kr, vr = rng.standard_normal((37, 64)), rng.standard_normal((37, 64))
+    kc, vc = rng.standard_normal((21, 64)), rng.standard_normal((21, 64))
+    kc[3] = 0.0  # zero-norm token -> similarity 0
+    kr[5], vr[5] = kc[7] * 2.0, vc[7] * 0.5  # duplicate direction -> R = 1
+    dev = torch.device("cuda")
+    T = lambda a: torch.tensor(a, dtype=torch.float32, device=dev)  # noqa: E731
+    r = ems.redundancy_cross(T(kr), T(vr), T(kc), T(vc)).cpu().numpy()
+    want = oracle.redundancy_cross(kr, vr, kc, vc)
+    np.testing.assert_allclose(r, want, atol=2e-6)
+    assert abs(r[5, 7] - 1.0) < 1e-5 and np.all(r[:, 3] == 0.0)
