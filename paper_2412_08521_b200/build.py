@@ -29,6 +29,10 @@ def sources():
     return sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cu"))
 
 
+SELFTEST_SRC = os.path.join(ROOT, "tests", "csrc", "tc_selftest.cu")
+SELFTEST_LIB = os.path.join(ROOT, "tests", "_build", "libems_selftest.so")
+
+
 def headers():
     hs = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
     hs += [os.path.join(INCLUDE, "ems_b200.h")]
@@ -60,7 +64,22 @@ def build(force: bool = False, verbose: bool = False) -> str:
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+    build_selftest(force)
     return LIB
+
+
+def build_selftest(force: bool = False) -> str:
+    """Test-only library exercising the tcgen05/TMA primitives (tests/csrc)."""
+    if not os.path.exists(SELFTEST_SRC):
+        return ""
+    os.makedirs(os.path.dirname(SELFTEST_LIB), exist_ok=True)
+    newest = max(os.path.getmtime(p) for p in [SELFTEST_SRC, *headers()])
+    if force or not os.path.exists(SELFTEST_LIB) or os.path.getmtime(SELFTEST_LIB) < newest:
+        cmd = [NVCC, *ARCH, *FLAGS, "-shared", SELFTEST_SRC, "-o", SELFTEST_LIB]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"selftest build failed:\n{r.stdout}\n{r.stderr}")
+    return SELFTEST_LIB
 
 
 if __name__ == "__main__":
