@@ -1,12 +1,556 @@
-// score_tc.cu -- tcgen05/TMEM/TMA score pass (bf16, head_dim 128).  Placeholder
-// until the tensor-core kernels land; AUTO falls back to the SIMT pass.
+// score_tc.cu -- the tcgen05/TMEM/TMA score pass for bf16, head_dim 128, L % 128 == 0.
+//
+// Two warp-specialised kernels:
+//
+// (P1) fwd_tc: causal FlashAttention forward, Q-stationary.  One CTA owns two
+//      128-row query tiles ("slots") that share one KV head (two heads of a GQA
+//      group, or two consecutive tiles when G == 1) and streams K/V tiles through
+//      a 2-stage TMA ring.  S_t = Q_t K^T (SS MMA, M=N=128, K=128) lands in TMEM;
+//      a softmax warpgroup per slot turns its row into P = exp2(S*c - m_ref) with
+//      a lazily-updated reference max (rescale only when the max grows by > 8 in
+//      log2 units), writes P as packed bf16 back into TMEM over S, and the MMA warp
+//      accumulates O_t += P_t V (TS MMA, A from TMEM, V MN-major).  MMA order
+//      S0 S1 | PV0 S0' | PV1 S1' | ... keeps the tensor core busy while the two
+//      softmax warpgroups alternate.  Outputs: O (bf16), row LSE in log2 units
+//      (workspace, feeds P2) and optionally natural-log LSE.
+//
+// (P2) colsum_tc: KV-stationary column sums ("modifying the loop order",
+//      PAPER.md:620).  One CTA owns a 128-key tile K_J of one unit and loops over
+//      every (query head h of the unit's group, query tile I >= J):
+//      S^T = K_J Q_I^T (M = keys on TMEM lanes, N = 128 queries), so each thread
+//      owns one key and the column sum over queries is an in-thread row sum of
+//      p = exp2(s*c - lse2_i) -- exactly normalised with P1's LSE, no atomics.
+//      Two warpgroups alternate over a 4-deep TMEM ring; per-item fp32 sums are
+//      accumulated in fp64 and the two warpgroups' partials are combined in a
+//      fixed order, so glo/loc are deterministic.  glo, loc = GQA mean (D2).
+//
+// Reference semantics: streaming_pass, proj/src/scoring.cpp:20-64.
+#include <cuda.h>
+
 #include "common.cuh"
+#include "tc.cuh"
+#include "tmap.h"
 
 namespace ems {
-size_t score_tc_workspace(const Dims&) { return 0; }
-bool score_tc_supported(const Dims&, int) { return false; }
-cudaError_t score_tc(const Dims&, const void*, const void*, const void*, void*, float*, float*,
-                     float*, void*, cudaStream_t) {
-    return cudaErrorNotSupported;
+
+namespace {
+
+using namespace tc;
+
+constexpr int kD = 128;            // head_dim
+constexpr int kTile = 128;         // rows per Q / K / V tile
+constexpr int kTileBytes = kTile * kD * 2;  // 32 KB (two 16 KB SW128 boxes)
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+constexpr float kRescaleThresh = 8.0f;  // log2 units
+
+// smem operand address of K-step k (16 elements) for a K-major 128x128 SW128 tile
+__device__ __forceinline__ uint32_t kmajor_addr(uint32_t base, int k) {
+    return base + (k >> 2) * 16384 + (k & 3) * 32;
 }
+
+__device__ __forceinline__ uint32_t tmem_lane_addr(uint32_t base, int warp_in_wg) {
+    return base + ((uint32_t)(warp_in_wg * 32) << 16);
+}
+
+// ============================================================================ P1
+struct FwdArgs {
+    int L, Hq, Hkv, G, nT;         // nT = L / 128
+    int units;
+    float c;                       // log2(e) / sqrt(d)
+    __nv_bfloat16* out;            // [B*Hq][L][128] (may be null)
+    float* lse2;                   // [B*Hq][L] log2-domain LSE (always)
+    float* lse_nat;                // [B*Hq][L] natural LSE (may be null)
+};
+
+constexpr int kFwdStages = 2;
+constexpr int kFwdThreads = 384;   // w0 TMA, w1 MMA, w2-3 spare, w4-7 softmax slot 0, w8-11 slot 1
+constexpr size_t kFwdSmem = 1024 + (2 + 2 * kFwdStages) * kTileBytes;
+
+struct FwdBars {
+    uint64_t q_full;
+    uint64_t k_full[kFwdStages], v_full[kFwdStages], kv_empty[kFwdStages];
+    uint64_t s_full[2], p_full[2], o_full[2];
+    uint32_t tmem_base;
+};
+
+// Work item -> (plane of slot 0, plane of slot 1, tile of slot 0, tile of slot 1, unit)
+__device__ __forceinline__ void fwd_item(const FwdArgs& a, int bid, int& plane0, int& plane1,
+                                         int& tile0, int& tile1, int& unit) {
+    if (a.G >= 2) {
+        const int pairs = a.G / 2;
+        const int per_tile = a.units * pairs;
+        const int I = a.nT - 1 - bid / per_tile;  // heaviest tiles first
+        const int rem = bid % per_tile;
+        unit = rem / pairs;
+        const int hp = rem % pairs;
+        const int b = unit / a.Hkv, hk = unit % a.Hkv;
+        plane0 = b * a.Hq + hk * a.G + 2 * hp;
+        plane1 = plane0 + 1;
+        tile0 = tile1 = I;
+    } else {
+        const int npair = a.nT / 2;
+        const int p = npair - 1 - bid / a.units;
+        unit = bid % a.units;
+        const int b = unit / a.Hkv, hk = unit % a.Hkv;
+        plane0 = plane1 = b * a.Hq + hk;  // G == 1: query head == kv head
+        tile0 = 2 * p;
+        tile1 = 2 * p + 1;
+    }
+}
+
+__global__ void __launch_bounds__(kFwdThreads, 1)
+    fwd_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
+                  const __grid_constant__ CUtensorMap tv, const FwdArgs a) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+    uint8_t* sq = sm;                                  // 2 x 32 KB
+    uint8_t* sk = sq + 2 * kTileBytes;                 // stages x 32 KB
+    uint8_t* sv = sk + kFwdStages * kTileBytes;        // stages x 32 KB
+    __shared__ FwdBars bars;
+
+    const int tid = threadIdx.x, warp = tid >> 5;
+    int plane[2], tile[2], unit;
+    fwd_item(a, blockIdx.x, plane[0], plane[1], tile[0], tile[1], unit);
+    const int jmax = max(tile[0], tile[1]);
+
+    if (warp == 0) {
+        tmem_alloc<512>(&bars.tmem_base);
+    } else if (warp == 1 && elect_one()) {
+        mbar_init(&bars.q_full, 1);
+        for (int s = 0; s < kFwdStages; ++s) {
+            mbar_init(&bars.k_full[s], 1);
+            mbar_init(&bars.v_full[s], 1);
+            mbar_init(&bars.kv_empty[s], 1);
+        }
+        for (int t = 0; t < 2; ++t) {
+            mbar_init(&bars.s_full[t], 1);
+            mbar_init(&bars.p_full[t], 128);
+            mbar_init(&bars.o_full[t], 1);
+        }
+        fence_barrier_init();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = bars.tmem_base;
+    // TMEM columns: S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512); P_t aliases S_t[0,64)
+    const uint32_t tS[2] = {tmem, tmem + 128};
+    const uint32_t tO[2] = {tmem + 256, tmem + 384};
+
+    if (warp == 0) {
+        // ---------------------------------------------------------------- TMA producer
+        if (elect_one()) {
+            tma_prefetch(&tq);
+            tma_prefetch(&tk);
+            tma_prefetch(&tv);
+            mbar_expect_tx(&bars.q_full, 2 * kTileBytes);
+            for (int t = 0; t < 2; ++t) {
+                uint8_t* dst = sq + t * kTileBytes;
+                tma_load_3d(dst, &tq, &bars.q_full, 0, tile[t] * kTile, plane[t]);
+                tma_load_3d(dst + 16384, &tq, &bars.q_full, 64, tile[t] * kTile, plane[t]);
+            }
+            for (int j = 0; j <= jmax; ++j) {
+                const int s = j % kFwdStages;
+                if (j >= kFwdStages) mbar_wait(&bars.kv_empty[s], ((j / kFwdStages) - 1) & 1);
+                uint8_t* dk = sk + s * kTileBytes;
+                uint8_t* dv = sv + s * kTileBytes;
+                mbar_expect_tx(&bars.k_full[s], kTileBytes);
+                tma_load_3d(dk, &tk, &bars.k_full[s], 0, j * kTile, unit);
+                tma_load_3d(dk + 16384, &tk, &bars.k_full[s], 64, j * kTile, unit);
+                mbar_expect_tx(&bars.v_full[s], kTileBytes);
+                tma_load_3d(dv, &tv, &bars.v_full[s], 0, j * kTile, unit);
+                tma_load_3d(dv + 16384, &tv, &bars.v_full[s], 64, j * kTile, unit);
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------------------------------------------------------- MMA issuer
+        if (elect_one()) {
+            const uint32_t id_s = idesc_bf16(128, 128, 0, 0);   // Q (K-major) x K^T (K-major)
+            const uint32_t id_o = idesc_bf16(128, 128, 0, 1);   // P (TMEM) x V (MN-major)
+            auto issue_s = [&](int t, int j) {
+                const int s = j % kFwdStages;
+                const uint32_t qa = smem_u32(sq + t * kTileBytes);
+                const uint32_t ka = smem_u32(sk + s * kTileBytes);
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    mma_ss(tS[t], sdesc(kmajor_addr(qa, k), 16, 1024),
+                           sdesc(kmajor_addr(ka, k), 16, 1024), id_s, k > 0);
+                mma_commit(&bars.s_full[t]);
+            };
+            auto issue_pv = [&](int t, int j) {
+                const int s = j % kFwdStages;
+                const uint32_t va = smem_u32(sv + s * kTileBytes);
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    mma_ts(tO[t], tS[t] + k * 8, sdesc(va + k * 2048, 16384, 1024), id_o,
+                           (j > 0 || k > 0) ? 1u : 0u);
+                mma_commit(&bars.o_full[t]);
+            };
+            mbar_wait(&bars.q_full, 0);
+            mbar_wait(&bars.k_full[0], 0);
+            tc_fence_after();
+            issue_s(0, 0);
+            issue_s(1, 0);
+            for (int j = 0; j <= jmax; ++j) {
+                const int s = j % kFwdStages;
+                const uint32_t sp = (j / kFwdStages) & 1;
+                bool v_ready = false, k_next_ready = false;
+                for (int t = 0; t < 2; ++t) {
+                    if (j > tile[t]) continue;
+                    mbar_wait(&bars.p_full[t], j & 1);
+                    if (!v_ready) {
+                        mbar_wait(&bars.v_full[s], sp);
+                        v_ready = true;
+                    }
+                    tc_fence_after();
+                    issue_pv(t, j);
+                    if (j + 1 <= tile[t]) {
+                        if (!k_next_ready) {
+                            const int s1 = (j + 1) % kFwdStages;
+                            mbar_wait(&bars.k_full[s1], ((j + 1) / kFwdStages) & 1);
+                            k_next_ready = true;
+                            tc_fence_after();
+                        }
+                        issue_s(t, j + 1);
+                    }
+                }
+                mma_commit(&bars.kv_empty[s]);
+            }
+        }
+    } else if (warp >= 4) {
+        // ---------------------------------------------------------------- softmax slots
+        const int t = (warp - 4) >> 2;          // slot
+        const int wi = warp & 3;                // warp within the warpgroup == TMEM subpartition
+        const int m = wi * 32 + (tid & 31);     // row within the tile
+        const int I = tile[t];
+        const uint32_t sS = tmem_lane_addr(tS[t], wi);
+        const uint32_t sO = tmem_lane_addr(tO[t], wi);
+        float m_ref = -INFINITY, l = 0.f;
+        for (int j = 0; j <= I; ++j) {
+            mbar_wait(&bars.s_full[t], j & 1);
+            tc_fence_after();
+            uint32_t r[4][32];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) tmem_ld32(sS + c * 32, r[c]);
+            tmem_ld_wait();
+            if (j == I) {  // diagonal tile: key n > query m is masked
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+#pragma unroll
+                    for (int x = 0; x < 32; ++x)
+                        if (c * 32 + x > m) r[c][x] = __float_as_uint(-INFINITY);
+            }
+            float mx = -INFINITY;
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+#pragma unroll
+                for (int x = 0; x < 32; ++x) mx = fmaxf(mx, __uint_as_float(r[c][x]));
+            const float mx2 = mx * a.c;
+            const bool need = mx2 > m_ref + kRescaleThresh;
+            const bool warp_need = __any_sync(0xffffffffu, need);
+            const float new_m = need ? mx2 : m_ref;
+            const float corr = need ? ex2(m_ref - new_m) : 1.f;
+            m_ref = new_m;
+            l *= corr;
+            float rs = 0.f;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                uint32_t pk[16];
+#pragma unroll
+                for (int x = 0; x < 16; ++x) {
+                    const float p0 = ex2(fmaf(__uint_as_float(r[c][2 * x]), a.c, -m_ref));
+                    const float p1 = ex2(fmaf(__uint_as_float(r[c][2 * x + 1]), a.c, -m_ref));
+                    rs += p0 + p1;
+                    pk[x] = pack_bf16(p0, p1);
+                }
+                tmem_st16(sS + c * 16, pk);
+            }
+            l += rs;
+            if (warp_need && j > 0) {  // rescale O_t once PV(j-1) has landed (rare)
+                mbar_wait(&bars.o_full[t], (j - 1) & 1);
+                tc_fence_after();
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    uint32_t o[32];
+                    tmem_ld32(sO + c * 32, o);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int x = 0; x < 32; ++x) o[x] = __float_as_uint(__uint_as_float(o[x]) * corr);
+                    tmem_st32(sO + c * 32, o);
+                }
+            }
+            tmem_st_wait();
+            tc_fence_before();
+            mbar_arrive(&bars.p_full[t]);
+        }
+        // epilogue: O / l -> bf16, LSE
+        mbar_wait(&bars.o_full[t], I & 1);
+        tc_fence_after();
+        const size_t row = (size_t)plane[t] * a.L + (size_t)I * kTile + m;
+        const float inv = 1.f / l;
+        if (a.out) {
+            uint4* dst = reinterpret_cast<uint4*>(a.out + row * kD);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                uint32_t o[32];
+                tmem_ld32(sO + c * 32, o);
+                tmem_ld_wait();
+#pragma unroll
+                for (int x = 0; x < 4; ++x) {
+                    uint4 v;
+                    v.x = pack_bf16(__uint_as_float(o[8 * x + 0]) * inv, __uint_as_float(o[8 * x + 1]) * inv);
+                    v.y = pack_bf16(__uint_as_float(o[8 * x + 2]) * inv, __uint_as_float(o[8 * x + 3]) * inv);
+                    v.z = pack_bf16(__uint_as_float(o[8 * x + 4]) * inv, __uint_as_float(o[8 * x + 5]) * inv);
+                    v.w = pack_bf16(__uint_as_float(o[8 * x + 6]) * inv, __uint_as_float(o[8 * x + 7]) * inv);
+                    dst[c * 4 + x] = v;
+                }
+            }
+        }
+        const float lse2 = m_ref + __log2f(l);
+        a.lse2[row] = lse2;
+        if (a.lse_nat) a.lse_nat[row] = lse2 * kLn2;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc<512>(tmem);
+}
+
+// ============================================================================ P2
+struct ColArgs {
+    int L, Hq, Hkv, G, nT, units, lwin;
+    float c;
+    const float* lse2;     // [B*Hq][L]
+    float* glo;            // [units][L]
+    float* loc;
+};
+
+constexpr int kColQStages = 4;
+constexpr int kColBufs = 4;           // TMEM S^T ring (4 x 128 columns)
+constexpr int kColThreads = 384;      // w0 TMA, w1 MMA, w4-7 colsum A, w8-11 colsum B
+constexpr size_t kColSmem = 1024 + (1 + kColQStages) * kTileBytes + kColBufs * 512 + 2 * 128 * 16;
+
+struct ColBars {
+    uint64_t k_full;
+    uint64_t q_full[kColQStages], q_empty[kColQStages];
+    uint64_t s_full[kColBufs], s_empty[kColBufs], l_full[kColBufs];
+    uint32_t tmem_base;
+};
+
+__global__ void __launch_bounds__(kColThreads, 1)
+    colsum_tc_kernel(const __grid_constant__ CUtensorMap tk, const __grid_constant__ CUtensorMap tq,
+                     const ColArgs a) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+    uint8_t* skt = sm;                                   // K_J, 32 KB
+    uint8_t* sq = skt + kTileBytes;                      // Q ring
+    float* slse = reinterpret_cast<float*>(sq + kColQStages * kTileBytes);   // [bufs][128]
+    double* spart = reinterpret_cast<double*>(slse + kColBufs * 128);        // [2][128]
+    __shared__ ColBars bars;
+
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const int J = blockIdx.x / a.units;     // key tile (heaviest first)
+    const int unit = blockIdx.x % a.units;
+    const int b = unit / a.Hkv, hk = unit % a.Hkv;
+    const int n_items = a.G * (a.nT - J);   // item i -> head h = i / (nT-J), tile I = J + i % (nT-J)
+    const int span = a.nT - J;
+
+    if (warp == 0) {
+        tmem_alloc<512>(&bars.tmem_base);
+    } else if (warp == 1 && elect_one()) {
+        mbar_init(&bars.k_full, 1);
+        for (int s = 0; s < kColQStages; ++s) {
+            mbar_init(&bars.q_full[s], 1);
+            mbar_init(&bars.q_empty[s], 1);
+        }
+        for (int s = 0; s < kColBufs; ++s) {
+            mbar_init(&bars.s_full[s], 1);
+            mbar_init(&bars.s_empty[s], 128);
+            mbar_init(&bars.l_full[s], 1);
+        }
+        fence_barrier_init();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = bars.tmem_base;
+
+    if (warp == 0) {
+        if (elect_one()) {
+            tma_prefetch(&tk);
+            tma_prefetch(&tq);
+            mbar_expect_tx(&bars.k_full, kTileBytes);
+            tma_load_3d(skt, &tk, &bars.k_full, 0, J * kTile, unit);
+            tma_load_3d(skt + 16384, &tk, &bars.k_full, 64, J * kTile, unit);
+            for (int i = 0; i < n_items; ++i) {
+                const int h = i / span, I = J + i % span;
+                const int plane = b * a.Hq + hk * a.G + h;
+                const int s = i % kColQStages, bb = i % kColBufs;
+                if (i >= kColQStages) mbar_wait(&bars.q_empty[s], ((i / kColQStages) - 1) & 1);
+                uint8_t* dq = sq + s * kTileBytes;
+                mbar_expect_tx(&bars.q_full[s], kTileBytes);
+                tma_load_3d(dq, &tq, &bars.q_full[s], 0, I * kTile, plane);
+                tma_load_3d(dq + 16384, &tq, &bars.q_full[s], 64, I * kTile, plane);
+                if (i >= kColBufs) mbar_wait(&bars.s_empty[bb], ((i / kColBufs) - 1) & 1);
+                mbar_expect_tx(&bars.l_full[bb], 512);
+                bulk_load(slse + bb * 128, a.lse2 + (size_t)plane * a.L + (size_t)I * kTile, 512,
+                          &bars.l_full[bb]);
+            }
+        }
+    } else if (warp == 1) {
+        if (elect_one()) {
+            const uint32_t id_s = idesc_bf16(128, 128, 0, 0);  // K_J (K-major) x Q^T (K-major)
+            const uint32_t ka = smem_u32(skt);
+            mbar_wait(&bars.k_full, 0);
+            for (int i = 0; i < n_items; ++i) {
+                const int s = i % kColQStages, bb = i % kColBufs;
+                mbar_wait(&bars.q_full[s], (i / kColQStages) & 1);
+                if (i >= kColBufs) mbar_wait(&bars.s_empty[bb], ((i / kColBufs) - 1) & 1);
+                tc_fence_after();
+                const uint32_t qa = smem_u32(sq + s * kTileBytes);
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    mma_ss(tmem + bb * 128, sdesc(kmajor_addr(ka, k), 16, 1024),
+                           sdesc(kmajor_addr(qa, k), 16, 1024), id_s, k > 0);
+                mma_commit(&bars.s_full[bb]);
+                mma_commit(&bars.q_empty[s]);
+            }
+        }
+    } else if (warp >= 4) {
+        const int g = (warp - 4) >> 2;          // colsum warpgroup 0/1 -> items i = g, g+2, ...
+        const int wi = warp & 3;
+        const int mrow = wi * 32 + (tid & 31);  // key within the tile
+        const int loc_start = a.L - a.lwin;
+        double acc_g = 0.0, acc_l = 0.0;
+        for (int i = g; i < n_items; i += 2) {
+            const int I = J + i % span;
+            const int bb = i % kColBufs;
+            const uint32_t ph = (i / kColBufs) & 1;
+            mbar_wait(&bars.l_full[bb], ph);
+            mbar_wait(&bars.s_full[bb], ph);
+            tc_fence_after();
+            const uint32_t sa = tmem_lane_addr(tmem + bb * 128, wi);
+            const float* lb = slse + bb * 128;
+            const bool diag = (I == J);
+            const bool has_loc = (I * kTile + kTile > loc_start);
+            float sg[4], sl = 0.f;
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2) {
+                uint32_t r[2][32];
+                tmem_ld32(sa + h2 * 64, r[0]);
+                tmem_ld32(sa + h2 * 64 + 32, r[1]);
+                tmem_ld_wait();
+#pragma unroll
+                for (int cc = 0; cc < 2; ++cc) {
+                    const int c = 2 * h2 + cc;
+                    float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+                    for (int x = 0; x < 32; x += 4) {
+                        const float4 lv = *reinterpret_cast<const float4*>(lb + c * 32 + x);
+                        float p[4];
+                        p[0] = ex2(fmaf(__uint_as_float(r[cc][x + 0]), a.c, -lv.x));
+                        p[1] = ex2(fmaf(__uint_as_float(r[cc][x + 1]), a.c, -lv.y));
+                        p[2] = ex2(fmaf(__uint_as_float(r[cc][x + 2]), a.c, -lv.z));
+                        p[3] = ex2(fmaf(__uint_as_float(r[cc][x + 3]), a.c, -lv.w));
+                        if (diag) {
+#pragma unroll
+                            for (int e = 0; e < 4; ++e)
+                                if (c * 32 + x + e < mrow) p[e] = 0.f;   // query < key
+                        }
+                        if (has_loc) {
+#pragma unroll
+                            for (int e = 0; e < 4; ++e)
+                                if (I * kTile + c * 32 + x + e >= loc_start) sl += p[e];
+                        }
+                        s0 += p[0] + p[1];
+                        s1 += p[2] + p[3];
+                    }
+                    sg[c] = s0 + s1;
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(&bars.s_empty[bb]);
+            acc_g += (double)((sg[0] + sg[1]) + (sg[2] + sg[3]));
+            acc_l += (double)sl;
+        }
+        // combine the two warpgroups in a fixed order: (A + B) / G
+        if (g == 1) {
+            spart[mrow] = acc_g;
+            spart[128 + mrow] = acc_l;
+        }
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        if (g == 0) {
+            const double tg = acc_g + spart[mrow], tl = acc_l + spart[128 + mrow];
+            const size_t o = (size_t)unit * a.L + (size_t)J * kTile + mrow;
+            a.glo[o] = (float)(tg / a.G);
+            a.loc[o] = (float)(tl / a.G);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc<512>(tmem);
+}
+
+}  // namespace
+
+bool score_tc_supported(const Dims& dm, int dtype) {
+    if (dtype != EMS_BF16 || dm.d != kD || dm.L % kTile != 0) return false;
+    if (dm.G == 1 && (dm.L / kTile) % 2 != 0) return false;
+    if (dm.G > 1 && dm.G % 2 != 0) return false;
+    int dev = 0, major = 0, minor = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return false;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+    return major == 10 && minor == 0 && encode_fn() != nullptr;
+}
+
+size_t score_tc_workspace(const Dims& dm) { return sizeof(float) * (size_t)dm.B * dm.Hq * dm.L; }
+
+cudaError_t score_tc(const Dims& dm, const void* q, const void* k, const void* v, void* o,
+                     float* lse, float* glo, float* loc, void* ws, cudaStream_t s) {
+    const int planes_q = dm.B * dm.Hq, planes_kv = dm.B * dm.Hkv;
+    CUtensorMap tq, tk, tv;
+    if (!make_tmap_bf16_3d(&tq, q, kD, dm.L, planes_q, kTile) ||
+        !make_tmap_bf16_3d(&tk, k, kD, dm.L, planes_kv, kTile) ||
+        !make_tmap_bf16_3d(&tv, v ? v : k, kD, dm.L, planes_kv, kTile))
+        return cudaErrorInvalidValue;
+    float* lse2 = static_cast<float*>(ws);
+    FwdArgs fa;
+    fa.L = dm.L;
+    fa.Hq = dm.Hq;
+    fa.Hkv = dm.Hkv;
+    fa.G = dm.G;
+    fa.nT = dm.L / kTile;
+    fa.units = dm.units;
+    fa.c = kLog2e / sqrtf((float)kD);
+    fa.out = static_cast<__nv_bfloat16*>(o);
+    fa.lse2 = lse2;
+    fa.lse_nat = lse;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFwdSmem);
+        cudaFuncSetAttribute(colsum_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)kColSmem);
+        attr_set = true;
+    }
+    const int n_fwd = dm.G >= 2 ? fa.nT * dm.units * (dm.G / 2) : (fa.nT / 2) * dm.units;
+    fwd_tc_kernel<<<n_fwd, kFwdThreads, kFwdSmem, s>>>(tq, tk, tv, fa);
+    ColArgs ca;
+    ca.L = dm.L;
+    ca.Hq = dm.Hq;
+    ca.Hkv = dm.Hkv;
+    ca.G = dm.G;
+    ca.nT = fa.nT;
+    ca.units = dm.units;
+    ca.lwin = dm.lwin_scores;
+    ca.c = fa.c;
+    ca.lse2 = lse2;
+    ca.glo = glo;
+    ca.loc = loc;
+    colsum_tc_kernel<<<fa.nT * dm.units, kColThreads, kColSmem, s>>>(tk, tq, ca);
+    return cudaGetLastError();
+}
+
 }  // namespace ems
