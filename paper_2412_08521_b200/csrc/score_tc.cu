@@ -14,21 +14,13 @@
 //      softmax warpgroups alternate.  Outputs: O (bf16), row LSE in log2 units
 //      (workspace, feeds P2) and optionally natural-log LSE.
 //
-// (P2) colsum_tc: KV-stationary column sums ("modifying the loop order",
-//      PAPER.md:620).  One CTA owns a 128-key tile K_J of one unit and loops over
-//      every (query head h of the unit's group, query tile I >= J):
-//      S^T = K_J Q_I^T (M = keys on TMEM lanes, N = 128 queries), so each thread
-//      owns one key and the column sum over queries is an in-thread row sum of
-//      p = exp2(s*c - lse2_i) -- exactly normalised with P1's LSE, no atomics.
-//      Two warpgroups alternate over a 4-deep TMEM ring; per-item fp32 sums are
-//      accumulated in fp64 and the two warpgroups' partials are combined in a
-//      fixed order, so glo/loc are deterministic.  glo, loc = GQA mean (D2).
+// (P2) colsum_tc.cu: KV-stationary column sums (glo, loc) normalised with P1's LSE.
 //
 // Reference semantics: streaming_pass, proj/src/scoring.cpp:20-64.
 #include <cuda.h>
+#include <stdlib.h>
 
-#include "common.cuh"
-#include "tc.cuh"
+#include "score_tc.cuh"
 #include "tmap.h"
 
 namespace ems {
@@ -36,22 +28,9 @@ namespace ems {
 namespace {
 
 using namespace tc;
+using namespace sc;
 
-constexpr int kD = 128;            // head_dim
-constexpr int kTile = 128;         // rows per Q / K / V tile
-constexpr int kTileBytes = kTile * kD * 2;  // 32 KB (two 16 KB SW128 boxes)
-constexpr float kLog2e = 1.4426950408889634f;
-constexpr float kLn2 = 0.6931471805599453f;
 constexpr float kRescaleThresh = 8.0f;  // log2 units
-
-// smem operand address of K-step k (16 elements) for a K-major 128x128 SW128 tile
-__device__ __forceinline__ uint32_t kmajor_addr(uint32_t base, int k) {
-    return base + (k >> 2) * 16384 + (k & 3) * 32;
-}
-
-__device__ __forceinline__ uint32_t tmem_lane_addr(uint32_t base, int warp_in_wg) {
-    return base + ((uint32_t)(warp_in_wg * 32) << 16);
-}
 
 // ============================================================================ P1
 struct FwdArgs {
@@ -309,184 +288,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             }
         }
         const float lse2 = m_ref + __log2f(l);
-        a.lse2[row] = lse2;
+        a.lse2[row] = -lse2;  // stored negated: P2 computes s*c + nlse2 with one FFMA
         if (a.lse_nat) a.lse_nat[row] = lse2 * kLn2;
-    }
-    tc_fence_before();
-    __syncthreads();
-    if (warp == 0) tmem_dealloc<512>(tmem);
-}
-
-// ============================================================================ P2
-struct ColArgs {
-    int L, Hq, Hkv, G, nT, units, lwin;
-    float c;
-    const float* lse2;     // [B*Hq][L]
-    float* glo;            // [units][L]
-    float* loc;
-};
-
-constexpr int kColQStages = 4;
-constexpr int kColBufs = 4;           // TMEM S^T ring (4 x 128 columns)
-constexpr int kColThreads = 384;      // w0 TMA, w1 MMA, w4-7 colsum A, w8-11 colsum B
-constexpr size_t kColSmem = 1024 + (1 + kColQStages) * kTileBytes + kColBufs * 512 + 2 * 128 * 16;
-
-struct ColBars {
-    uint64_t k_full;
-    uint64_t q_full[kColQStages], q_empty[kColQStages];
-    uint64_t s_full[kColBufs], s_empty[kColBufs], l_full[kColBufs];
-    uint32_t tmem_base;
-};
-
-__global__ void __launch_bounds__(kColThreads, 1)
-    colsum_tc_kernel(const __grid_constant__ CUtensorMap tk, const __grid_constant__ CUtensorMap tq,
-                     const ColArgs a) {
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
-    uint8_t* skt = sm;                                   // K_J, 32 KB
-    uint8_t* sq = skt + kTileBytes;                      // Q ring
-    float* slse = reinterpret_cast<float*>(sq + kColQStages * kTileBytes);   // [bufs][128]
-    double* spart = reinterpret_cast<double*>(slse + kColBufs * 128);        // [2][128]
-    __shared__ ColBars bars;
-
-    const int tid = threadIdx.x, warp = tid >> 5;
-    const int J = blockIdx.x / a.units;     // key tile (heaviest first)
-    const int unit = blockIdx.x % a.units;
-    const int b = unit / a.Hkv, hk = unit % a.Hkv;
-    const int n_items = a.G * (a.nT - J);   // item i -> head h = i / (nT-J), tile I = J + i % (nT-J)
-    const int span = a.nT - J;
-
-    if (warp == 0) {
-        tmem_alloc<512>(&bars.tmem_base);
-    } else if (warp == 1 && elect_one()) {
-        mbar_init(&bars.k_full, 1);
-        for (int s = 0; s < kColQStages; ++s) {
-            mbar_init(&bars.q_full[s], 1);
-            mbar_init(&bars.q_empty[s], 1);
-        }
-        for (int s = 0; s < kColBufs; ++s) {
-            mbar_init(&bars.s_full[s], 1);
-            mbar_init(&bars.s_empty[s], 128);
-            mbar_init(&bars.l_full[s], 1);
-        }
-        fence_barrier_init();
-    }
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem = bars.tmem_base;
-
-    if (warp == 0) {
-        if (elect_one()) {
-            tma_prefetch(&tk);
-            tma_prefetch(&tq);
-            mbar_expect_tx(&bars.k_full, kTileBytes);
-            tma_load_3d(skt, &tk, &bars.k_full, 0, J * kTile, unit);
-            tma_load_3d(skt + 16384, &tk, &bars.k_full, 64, J * kTile, unit);
-            for (int i = 0; i < n_items; ++i) {
-                const int h = i / span, I = J + i % span;
-                const int plane = b * a.Hq + hk * a.G + h;
-                const int s = i % kColQStages, bb = i % kColBufs;
-                if (i >= kColQStages) mbar_wait(&bars.q_empty[s], ((i / kColQStages) - 1) & 1);
-                uint8_t* dq = sq + s * kTileBytes;
-                mbar_expect_tx(&bars.q_full[s], kTileBytes);
-                tma_load_3d(dq, &tq, &bars.q_full[s], 0, I * kTile, plane);
-                tma_load_3d(dq + 16384, &tq, &bars.q_full[s], 64, I * kTile, plane);
-                if (i >= kColBufs) mbar_wait(&bars.s_empty[bb], ((i / kColBufs) - 1) & 1);
-                mbar_expect_tx(&bars.l_full[bb], 512);
-                bulk_load(slse + bb * 128, a.lse2 + (size_t)plane * a.L + (size_t)I * kTile, 512,
-                          &bars.l_full[bb]);
-            }
-        }
-    } else if (warp == 1) {
-        if (elect_one()) {
-            const uint32_t id_s = idesc_bf16(128, 128, 0, 0);  // K_J (K-major) x Q^T (K-major)
-            const uint32_t ka = smem_u32(skt);
-            mbar_wait(&bars.k_full, 0);
-            for (int i = 0; i < n_items; ++i) {
-                const int s = i % kColQStages, bb = i % kColBufs;
-                mbar_wait(&bars.q_full[s], (i / kColQStages) & 1);
-                if (i >= kColBufs) mbar_wait(&bars.s_empty[bb], ((i / kColBufs) - 1) & 1);
-                tc_fence_after();
-                const uint32_t qa = smem_u32(sq + s * kTileBytes);
-#pragma unroll
-                for (int k = 0; k < 8; ++k)
-                    mma_ss(tmem + bb * 128, sdesc(kmajor_addr(ka, k), 16, 1024),
-                           sdesc(kmajor_addr(qa, k), 16, 1024), id_s, k > 0);
-                mma_commit(&bars.s_full[bb]);
-                mma_commit(&bars.q_empty[s]);
-            }
-        }
-    } else if (warp >= 4) {
-        const int g = (warp - 4) >> 2;          // colsum warpgroup 0/1 -> items i = g, g+2, ...
-        const int wi = warp & 3;
-        const int mrow = wi * 32 + (tid & 31);  // key within the tile
-        const int loc_start = a.L - a.lwin;
-        double acc_g = 0.0, acc_l = 0.0;
-        for (int i = g; i < n_items; i += 2) {
-            const int I = J + i % span;
-            const int bb = i % kColBufs;
-            const uint32_t ph = (i / kColBufs) & 1;
-            mbar_wait(&bars.l_full[bb], ph);
-            mbar_wait(&bars.s_full[bb], ph);
-            tc_fence_after();
-            const uint32_t sa = tmem_lane_addr(tmem + bb * 128, wi);
-            const float* lb = slse + bb * 128;
-            const bool diag = (I == J);
-            const bool has_loc = (I * kTile + kTile > loc_start);
-            float sg[4], sl = 0.f;
-#pragma unroll
-            for (int h2 = 0; h2 < 2; ++h2) {
-                uint32_t r[2][32];
-                tmem_ld32(sa + h2 * 64, r[0]);
-                tmem_ld32(sa + h2 * 64 + 32, r[1]);
-                tmem_ld_wait();
-#pragma unroll
-                for (int cc = 0; cc < 2; ++cc) {
-                    const int c = 2 * h2 + cc;
-                    float s0 = 0.f, s1 = 0.f;
-#pragma unroll
-                    for (int x = 0; x < 32; x += 4) {
-                        const float4 lv = *reinterpret_cast<const float4*>(lb + c * 32 + x);
-                        float p[4];
-                        p[0] = ex2(fmaf(__uint_as_float(r[cc][x + 0]), a.c, -lv.x));
-                        p[1] = ex2(fmaf(__uint_as_float(r[cc][x + 1]), a.c, -lv.y));
-                        p[2] = ex2(fmaf(__uint_as_float(r[cc][x + 2]), a.c, -lv.z));
-                        p[3] = ex2(fmaf(__uint_as_float(r[cc][x + 3]), a.c, -lv.w));
-                        if (diag) {
-#pragma unroll
-                            for (int e = 0; e < 4; ++e)
-                                if (c * 32 + x + e < mrow) p[e] = 0.f;   // query < key
-                        }
-                        if (has_loc) {
-#pragma unroll
-                            for (int e = 0; e < 4; ++e)
-                                if (I * kTile + c * 32 + x + e >= loc_start) sl += p[e];
-                        }
-                        s0 += p[0] + p[1];
-                        s1 += p[2] + p[3];
-                    }
-                    sg[c] = s0 + s1;
-                }
-            }
-            tc_fence_before();
-            mbar_arrive(&bars.s_empty[bb]);
-            acc_g += (double)((sg[0] + sg[1]) + (sg[2] + sg[3]));
-            acc_l += (double)sl;
-        }
-        // combine the two warpgroups in a fixed order: (A + B) / G
-        if (g == 1) {
-            spart[mrow] = acc_g;
-            spart[128 + mrow] = acc_l;
-        }
-        asm volatile("bar.sync 1, 256;" ::: "memory");
-        if (g == 0) {
-            const double tg = acc_g + spart[mrow], tl = acc_l + spart[128 + mrow];
-            const size_t o = (size_t)unit * a.L + (size_t)J * kTile + mrow;
-            a.glo[o] = (float)(tg / a.G);
-            a.loc[o] = (float)(tl / a.G);
-        }
     }
     tc_fence_before();
     __syncthreads();
@@ -516,7 +319,7 @@ cudaError_t score_tc(const Dims& dm, const void* q, const void* k, const void* v
         !make_tmap_bf16_3d(&tk, k, kD, dm.L, planes_kv, kTile) ||
         !make_tmap_bf16_3d(&tv, v ? v : k, kD, dm.L, planes_kv, kTile))
         return cudaErrorInvalidValue;
-    float* lse2 = static_cast<float*>(ws);
+    float* nlse2 = static_cast<float*>(ws);
     FwdArgs fa;
     fa.L = dm.L;
     fa.Hq = dm.Hq;
@@ -526,13 +329,11 @@ cudaError_t score_tc(const Dims& dm, const void* q, const void* k, const void* v
     fa.units = dm.units;
     fa.c = kLog2e / sqrtf((float)kD);
     fa.out = static_cast<__nv_bfloat16*>(o);
-    fa.lse2 = lse2;
+    fa.lse2 = nlse2;
     fa.lse_nat = lse;
     static bool attr_set = false;
     if (!attr_set) {
         cudaFuncSetAttribute(fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFwdSmem);
-        cudaFuncSetAttribute(colsum_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)kColSmem);
         attr_set = true;
     }
     const int n_fwd = dm.G >= 2 ? fa.nT * dm.units * (dm.G / 2) : (fa.nT / 2) * dm.units;
@@ -546,11 +347,10 @@ cudaError_t score_tc(const Dims& dm, const void* q, const void* k, const void* v
     ca.units = dm.units;
     ca.lwin = dm.lwin_scores;
     ca.c = fa.c;
-    ca.lse2 = lse2;
+    ca.nlse2 = nlse2;
     ca.glo = glo;
     ca.loc = loc;
-    colsum_tc_kernel<<<fa.nT * dm.units, kColThreads, kColSmem, s>>>(tk, tq, ca);
-    return cudaGetLastError();
+    return launch_colsum_tc(ca, tk, tq, s);
 }
 
 }  // namespace ems

@@ -179,6 +179,19 @@ __device__ __forceinline__ uint32_t elect_one() {
     return pred;
 }
 
+__device__ __forceinline__ float4 lds128(uint32_t saddr) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(saddr));
+    return v;
+}
+__device__ __forceinline__ float lds32(uint32_t saddr) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(saddr));
+    return v;
+}
+
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
     __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
     return *reinterpret_cast<uint32_t*>(&v);
@@ -187,6 +200,30 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 __device__ __forceinline__ float ex2(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// exp2 of two values on the FMA pipe (packed f32x2 ops), for the fraction of the
+// exponentials moved off MUFU.  Round-to-nearest split x = j + f, f in [-1/2, 1/2],
+// degree-5 polynomial for 2^f (max relative error 2.4e-7 in fp32 Horner, the same
+// order as ex2.approx), exponent added with one integer LEA.  Inputs are clamped to
+// >= -125 so the exponent never underflows (values < 2^-125 are irrelevant here).
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+    constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
+    x.x = fmaxf(x.x, -125.f);
+    x.y = fmaxf(x.y, -125.f);
+    const float2 t = __fadd2_rn(x, make_float2(kMagic, kMagic));
+    const float2 r = __fadd2_rn(t, make_float2(-kMagic, -kMagic));
+    const float2 f = __ffma2_rn(r, make_float2(-1.f, -1.f), x);
+    float2 p = make_float2(1.3276363e-3f, 1.3276363e-3f);
+    p = __ffma2_rn(p, f, make_float2(9.6755046e-3f, 9.6755046e-3f));
+    p = __ffma2_rn(p, f, make_float2(5.5507131e-2f, 5.5507131e-2f));
+    p = __ffma2_rn(p, f, make_float2(2.4022120e-1f, 2.4022120e-1f));
+    p = __ffma2_rn(p, f, make_float2(6.9314694e-1f, 6.9314694e-1f));
+    p = __ffma2_rn(p, f, make_float2(1.0000001f, 1.0000001f));
+    float2 y;
+    y.x = __uint_as_float(__float_as_uint(p.x) + (__float_as_uint(t.x) << 23));
+    y.y = __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(t.y) << 23));
     return y;
 }
 

@@ -1,0 +1,47 @@
+"""Microbenchmarks of the per-SM pipes the score kernels lean on (one CTA per SM):
+TMEM load bandwidth, MUFU.EX2, FFMA, FFMA2 and the polynomial exp2 throughput."""
+import ctypes as C
+import json
+import os
+import sys
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+L = C.CDLL(os.path.join(ROOT, "tests", "_build", "libems_selftest.so"))
+L.ems_micro.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p]
+
+
+def run(kind, threads, iters, blocks=148):
+    cyc = torch.zeros(blocks, dtype=torch.int64, device="cuda")
+    sink = torch.zeros(1024, device="cuda")
+    assert L.ems_micro(kind, threads, blocks, iters, cyc.data_ptr(), sink.data_ptr()) == 0
+    return cyc.double().median().item()
+
+
+res = {}
+for threads in (128, 256, 512):
+    w = threads // 32
+    it = 4096
+    c = run(0, threads, it)
+    res[f"tmem_ld_x32_wait_each_{w}w_B_per_clk"] = w * it * 32 * 32 * 4 / c
+    c = run(1, threads, it)
+    res[f"tmem_ld_4x32_then_wait_{w}w_B_per_clk"] = w * it * 32 * 32 * 4 / c
+    c = run(2, threads, it)
+    res[f"mufu_ex2_{w}w_per_clk"] = w * 32 * it * 8 / c
+    c = run(3, threads, it)
+    res[f"ffma_{w}w_per_clk"] = w * 32 * it * 8 / c
+    c = run(4, threads, it)
+    res[f"ffma2_{w}w_elem_per_clk"] = w * 32 * it * 8 / c
+    c = run(5, threads, 1024)
+    res[f"poly_exp2_{w}w_elem_per_clk"] = w * 32 * 1024 * 8 / c
+print(json.dumps(res, indent=1))
+
+shapes = {10: "32x32b.x32 x2", 11: "16x64b.x32 x2", 12: "16x128b.x16 x2", 13: "16x256b.x8 x2", 14: "32x32b.x64"}
+res2 = {}
+for threads in (128, 256, 512):
+    w = threads // 32
+    for kind, name in shapes.items():
+        c = run(kind, threads, 4096)
+        res2[f"{name} {w}w B/clk"] = w * 4096 * 32 * 32 * 4 / c
+print(json.dumps(res2, indent=1))
