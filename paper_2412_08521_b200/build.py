@@ -82,5 +82,30 @@ def build_selftest(force: bool = False) -> str:
     return SELFTEST_LIB
 
 
+CPP_TEST_SRC = os.path.join(ROOT, "tests", "cpp", "test_ems_hpp.cpp")
+CPP_TEST_BIN = os.path.join(ROOT, "tests", "_build", "test_ems_hpp")
+ORACLE_DIR = os.path.join(ROOT, "oracle")
+
+
+def build_cpp_tests(force: bool = False) -> str:
+    """Test-only binary: the C++ reference-shaped API (include/ems_b200/ems.hpp) checked
+    against the C oracle.  Needs oracle/_build/libems_oracle.so (oracle.build())."""
+    oracle_so = os.path.join(ORACLE_DIR, "_build", "libems_oracle.so")
+    if not (os.path.exists(CPP_TEST_SRC) and os.path.exists(oracle_so)):
+        return ""
+    deps = [CPP_TEST_SRC, os.path.join(INCLUDE, "ems_b200", "ems.hpp"), LIB, oracle_so]
+    if force or not os.path.exists(CPP_TEST_BIN) or os.path.getmtime(CPP_TEST_BIN) < max(map(os.path.getmtime, deps)):
+        os.makedirs(os.path.dirname(CPP_TEST_BIN), exist_ok=True)
+        cmd = [NVCC, *ARCH, "-O2", "-std=c++17", "-I", INCLUDE, "-I", ORACLE_DIR, CPP_TEST_SRC,
+               "-L", PKG, "-lems_b200", "-L", os.path.dirname(oracle_so), "-lems_oracle",
+               "-Xlinker", "-rpath," + PKG, "-Xlinker", "-rpath," + os.path.dirname(oracle_so),
+               "-Xlinker", "-rpath,$ORIGIN/../../paper_2412_08521_b200",
+               "-Xlinker", "-rpath,$ORIGIN/../../oracle/_build", "-o", CPP_TEST_BIN]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"cpp test build failed:\n{r.stdout}\n{r.stderr}")
+    return CPP_TEST_BIN
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

@@ -78,6 +78,7 @@ __device__ __forceinline__ void fwd_item(const FwdArgs& a, int bid, int& plane0,
     }
 }
 
+template <int kPoly>
 __global__ void __launch_bounds__(kFwdThreads, 1)
     fwd_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                   const __grid_constant__ CUtensorMap tv, const FwdArgs a) {
@@ -233,20 +234,25 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             const float corr = need ? ex2(m_ref - new_m) : 1.f;
             m_ref = new_m;
             l *= corr;
-            float rs = 0.f;
+            // p = exp2(s*c - m_ref): pairs with (x % 8) < kPoly on the FMA pipe, rest on MUFU
+            const float2 c2 = make_float2(a.c, a.c), nm2 = make_float2(-m_ref, -m_ref);
+            float2 rs2 = make_float2(0.f, 0.f);
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
                 uint32_t pk[16];
 #pragma unroll
                 for (int x = 0; x < 16; ++x) {
-                    const float p0 = ex2(fmaf(__uint_as_float(r[c][2 * x]), a.c, -m_ref));
-                    const float p1 = ex2(fmaf(__uint_as_float(r[c][2 * x + 1]), a.c, -m_ref));
-                    rs += p0 + p1;
-                    pk[x] = pack_bf16(p0, p1);
+                    const float2 arg = __ffma2_rn(
+                        make_float2(__uint_as_float(r[c][2 * x]), __uint_as_float(r[c][2 * x + 1])), c2, nm2);
+                    float2 p;
+                    if ((x & 7) < kPoly) p = ex2_poly2(arg);
+                    else p = make_float2(ex2(arg.x), ex2(arg.y));
+                    rs2 = __fadd2_rn(rs2, p);
+                    pk[x] = pack_bf16(p.x, p.y);
                 }
                 tmem_st16(sS + c * 16, pk);
             }
-            l += rs;
+            l += rs2.x + rs2.y;
             if (warp_need && j > 0) {  // rescale O_t once PV(j-1) has landed (rare)
                 mbar_wait(&bars.o_full[t], (j - 1) & 1);
                 tc_fence_after();
@@ -333,11 +339,24 @@ cudaError_t score_tc(const Dims& dm, const void* q, const void* k, const void* v
     fa.lse_nat = lse;
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFwdSmem);
+        cudaFuncSetAttribute(fwd_tc_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFwdSmem);
+        cudaFuncSetAttribute(fwd_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFwdSmem);
+        cudaFuncSetAttribute(fwd_tc_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFwdSmem);
+        cudaFuncSetAttribute(fwd_tc_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFwdSmem);
         attr_set = true;
     }
     const int n_fwd = dm.G >= 2 ? fa.nT * dm.units * (dm.G / 2) : (fa.nT / 2) * dm.units;
-    fwd_tc_kernel<<<n_fwd, kFwdThreads, kFwdSmem, s>>>(tq, tk, tv, fa);
+    // pairs (of every 8) whose exp2 runs on the FMA pipe; EMS_P1_POLY overrides (tuning)
+    static const int poly = [] {
+        const char* e = getenv("EMS_P1_POLY");
+        return e ? atoi(e) : 0;
+    }();
+    switch (poly) {
+        case 0: fwd_tc_kernel<0><<<n_fwd, kFwdThreads, kFwdSmem, s>>>(tq, tk, tv, fa); break;
+        case 2: fwd_tc_kernel<2><<<n_fwd, kFwdThreads, kFwdSmem, s>>>(tq, tk, tv, fa); break;
+        case 4: fwd_tc_kernel<4><<<n_fwd, kFwdThreads, kFwdSmem, s>>>(tq, tk, tv, fa); break;
+        default: fwd_tc_kernel<3><<<n_fwd, kFwdThreads, kFwdSmem, s>>>(tq, tk, tv, fa); break;
+    }
     ColArgs ca;
     ca.L = dm.L;
     ca.Hq = dm.Hq;
