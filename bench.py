@@ -201,6 +201,8 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="cfg3")
+    ap.add_argument("--seq-len", type=int, default=0, help="override L (debug / scaling sweeps)")
+    ap.add_argument("--batch", type=int, default=0, help="override B (config 4 uses 1/8/32)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--score-impl", default="auto", choices=["auto", "simt", "tcgen05"])
     ap.add_argument("--cpu-seconds", type=float, default=8.0,
@@ -212,6 +214,10 @@ def main():
     from paper_2412_08521_b200.inputs import CONFIGS
 
     w = CONFIGS[args.config]
+    if args.seq_len:
+        w = w.with_(seq_len=args.seq_len)
+    if args.batch:
+        w = w.with_(batch=args.batch)
     if args.impl == "reference":
         run_reference(args, w)
         return

@@ -323,6 +323,7 @@ int ems_score(const ems_desc* d, const void* q, const void* k, const void* v, vo
         set_error("ems_score: null tensor");
         return EMS_INVALID_ARGUMENT;
     }
+    EMS_CUDA_CHECK(cudaMemsetAsync(ws, 0, sizeof(DevStatus), s));  // start of a pipeline
     return run_score(d, q, k, v, out_o, lse, glo, loc, ws, s);
 }
 

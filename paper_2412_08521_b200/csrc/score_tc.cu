@@ -1,18 +1,20 @@
 // score_tc.cu -- the tcgen05/TMEM/TMA score pass for bf16, head_dim 128, L % 128 == 0.
 //
-// Two warp-specialised kernels:
-//
 // (P1) fwd_tc: causal FlashAttention forward, Q-stationary.  One CTA owns two
 //      128-row query tiles ("slots") that share one KV head (two heads of a GQA
 //      group, or two consecutive tiles when G == 1) and streams K/V tiles through
-//      a 2-stage TMA ring.  S_t = Q_t K^T (SS MMA, M=N=128, K=128) lands in TMEM;
-//      a softmax warpgroup per slot turns its row into P = exp2(S*c - m_ref) with
-//      a lazily-updated reference max (rescale only when the max grows by > 8 in
-//      log2 units), writes P as packed bf16 back into TMEM over S, and the MMA warp
-//      accumulates O_t += P_t V (TS MMA, A from TMEM, V MN-major).  MMA order
-//      S0 S1 | PV0 S0' | PV1 S1' | ... keeps the tensor core busy while the two
-//      softmax warpgroups alternate.  Outputs: O (bf16), row LSE in log2 units
-//      (workspace, feeds P2) and optionally natural-log LSE.
+//      a 2-stage TMA ring, so every K/V tile read from L2 feeds two QK^T MMAs.
+//      S_t = Q_t K^T (SS MMA, M=N=128, K=128) lands in TMEM; the softmax of each
+//      slot is split over two warpgroups, one per 64-column half of every row
+//      (thread = half a row), which halves the softmax latency that sits between
+//      a slot's S MMA and its PV MMA.  The halves agree on the row max through a
+//      shared-memory exchange + named barrier per tile; P = exp2(S*c - m_ref) uses a
+//      lazily-updated reference max (O is rescaled only when the max grows by > 8
+//      in log2 units), is written as packed bf16 over S, and the MMA warp
+//      accumulates O_t += P_t V (TS MMA: A from TMEM, V MN-major from smem).  MMA
+//      order S0 S1 | PV0 S0' | PV1 S1' | ... keeps the tensor core on one slot
+//      while the other slot's softmax runs.  Outputs: O (bf16), the negated row LSE
+//      in log2 units (workspace, feeds P2) and optionally the natural-log LSE.
 //
 // (P2) colsum_tc.cu: KV-stationary column sums (glo, loc) normalised with P1's LSE.
 //
@@ -32,19 +34,20 @@ using namespace sc;
 
 constexpr float kRescaleThresh = 8.0f;  // log2 units
 
-// ============================================================================ P1
 struct FwdArgs {
     int L, Hq, Hkv, G, nT;         // nT = L / 128
     int units;
     float c;                       // log2(e) / sqrt(d)
     __nv_bfloat16* out;            // [B*Hq][L][128] (may be null)
-    float* lse2;                   // [B*Hq][L] log2-domain LSE (always)
+    float* nlse2;                  // [B*Hq][L] negated log2-domain LSE (always)
     float* lse_nat;                // [B*Hq][L] natural LSE (may be null)
 };
 
 constexpr int kFwdStages = 2;
-constexpr int kFwdThreads = 384;   // w0 TMA, w1 MMA, w2-3 spare, w4-7 softmax slot 0, w8-11 slot 1
-constexpr size_t kFwdSmem = 1024 + (2 + 2 * kFwdStages) * kTileBytes;
+// w0 TMA, w1 MMA, w2-3 spare; softmax warps 4..19: slot t = (w-4)/8, column half
+// h = ((w-4)/4) % 2, TMEM sub-partition w % 4.
+constexpr int kFwdThreads = 640;
+constexpr size_t kFwdSmem = 1024 + (2 + 2 * kFwdStages) * kTileBytes + 2 * 2 * 2 * 128 * 4;
 
 struct FwdBars {
     uint64_t q_full;
@@ -78,6 +81,10 @@ __device__ __forceinline__ void fwd_item(const FwdArgs& a, int bid, int& plane0,
     }
 }
 
+__device__ __forceinline__ void named_sync(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
 template <int kPoly>
 __global__ void __launch_bounds__(kFwdThreads, 1)
     fwd_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
@@ -88,6 +95,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     uint8_t* sq = sm;                                  // 2 x 32 KB
     uint8_t* sk = sq + 2 * kTileBytes;                 // stages x 32 KB
     uint8_t* sv = sk + kFwdStages * kTileBytes;        // stages x 32 KB
+    float* xch = reinterpret_cast<float*>(sv + kFwdStages * kTileBytes);  // [slot][buf][half][128]
     __shared__ FwdBars bars;
 
     const int tid = threadIdx.x, warp = tid >> 5;
@@ -106,7 +114,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         }
         for (int t = 0; t < 2; ++t) {
             mbar_init(&bars.s_full[t], 1);
-            mbar_init(&bars.p_full[t], 128);
+            mbar_init(&bars.p_full[t], 256);
             mbar_init(&bars.o_full[t], 1);
         }
         fence_barrier_init();
@@ -200,33 +208,43 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             }
         }
     } else if (warp >= 4) {
-        // ---------------------------------------------------------------- softmax slots
-        const int t = (warp - 4) >> 2;          // slot
-        const int wi = warp & 3;                // warp within the warpgroup == TMEM subpartition
+        // ---------------------------------------------------------------- softmax (half rows)
+        const int t = (warp - 4) >> 3;          // slot
+        const int h = ((warp - 4) >> 2) & 1;    // column half: keys [64h, 64h + 64)
+        const int wi = warp & 3;                // TMEM sub-partition
         const int m = wi * 32 + (tid & 31);     // row within the tile
         const int I = tile[t];
-        const uint32_t sS = tmem_lane_addr(tS[t], wi);
-        const uint32_t sO = tmem_lane_addr(tO[t], wi);
+        const uint32_t sS = tmem_lane_addr(tS[t], wi) + 64 * h;   // this thread's S half
+        const uint32_t sP = tmem_lane_addr(tS[t], wi) + 32 * h;   // its packed-P half
+        const uint32_t sO = tmem_lane_addr(tO[t], wi) + 64 * h;   // its O half
+        float* xt = xch + t * 2 * 2 * 128;      // [buf][half][128]
+        const int bar_id = 1 + t;
         float m_ref = -INFINITY, l = 0.f;
         for (int j = 0; j <= I; ++j) {
             mbar_wait(&bars.s_full[t], j & 1);
             tc_fence_after();
-            uint32_t r[4][32];
-#pragma unroll
-            for (int c = 0; c < 4; ++c) tmem_ld32(sS + c * 32, r[c]);
+            uint32_t r[2][32];
+            tmem_ld32(sS, r[0]);
+            tmem_ld32(sS + 32, r[1]);
             tmem_ld_wait();
-            if (j == I) {  // diagonal tile: key n > query m is masked
+            if (j == I) {  // diagonal tile: key 64h + n > query m is masked
 #pragma unroll
-                for (int c = 0; c < 4; ++c)
+                for (int c = 0; c < 2; ++c)
 #pragma unroll
                     for (int x = 0; x < 32; ++x)
-                        if (c * 32 + x > m) r[c][x] = __float_as_uint(-INFINITY);
+                        if (64 * h + c * 32 + x > m) r[c][x] = __float_as_uint(-INFINITY);
             }
-            float mx = -INFINITY;
+            float hm = -INFINITY;
 #pragma unroll
-            for (int c = 0; c < 4; ++c)
+            for (int c = 0; c < 2; ++c)
 #pragma unroll
-                for (int x = 0; x < 32; ++x) mx = fmaxf(mx, __uint_as_float(r[c][x]));
+                for (int x = 0; x < 32; ++x) hm = fmaxf(hm, __uint_as_float(r[c][x]));
+            // exchange half-row maxima (also orders both halves' S loads before any P store,
+            // since P of half 1 overwrites S columns 32..63 of half 0)
+            float* xb = xt + (j & 1) * 256;
+            xb[h * 128 + m] = hm;
+            named_sync(bar_id, 256);
+            const float mx = fmaxf(hm, xb[(h ^ 1) * 128 + m]);
             const float mx2 = mx * a.c;
             const bool need = mx2 > m_ref + kRescaleThresh;
             const bool warp_need = __any_sync(0xffffffffu, need);
@@ -234,11 +252,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             const float corr = need ? ex2(m_ref - new_m) : 1.f;
             m_ref = new_m;
             l *= corr;
-            // p = exp2(s*c - m_ref): pairs with (x % 8) < kPoly on the FMA pipe, rest on MUFU
             const float2 c2 = make_float2(a.c, a.c), nm2 = make_float2(-m_ref, -m_ref);
             float2 rs2 = make_float2(0.f, 0.f);
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
+            for (int c = 0; c < 2; ++c) {
                 uint32_t pk[16];
 #pragma unroll
                 for (int x = 0; x < 16; ++x) {
@@ -250,14 +267,14 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
                     rs2 = __fadd2_rn(rs2, p);
                     pk[x] = pack_bf16(p.x, p.y);
                 }
-                tmem_st16(sS + c * 16, pk);
+                tmem_st16(sP + c * 16, pk);
             }
             l += rs2.x + rs2.y;
-            if (warp_need && j > 0) {  // rescale O_t once PV(j-1) has landed (rare)
+            if (warp_need && j > 0) {  // rescale this half of O_t once PV(j-1) has landed (rare)
                 mbar_wait(&bars.o_full[t], (j - 1) & 1);
                 tc_fence_after();
 #pragma unroll
-                for (int c = 0; c < 4; ++c) {
+                for (int c = 0; c < 2; ++c) {
                     uint32_t o[32];
                     tmem_ld32(sO + c * 32, o);
                     tmem_ld_wait();
@@ -270,15 +287,19 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             tc_fence_before();
             mbar_arrive(&bars.p_full[t]);
         }
-        // epilogue: O / l -> bf16, LSE
+        // epilogue: l = l_half0 + l_half1 (fixed order), O / l -> bf16, LSE
+        float* xb = xt + ((I + 1) & 1) * 256;
+        xb[h * 128 + m] = l;
+        named_sync(bar_id, 256);
+        const float lt = h == 0 ? l + xb[128 + m] : xb[m] + l;
         mbar_wait(&bars.o_full[t], I & 1);
         tc_fence_after();
         const size_t row = (size_t)plane[t] * a.L + (size_t)I * kTile + m;
-        const float inv = 1.f / l;
+        const float inv = 1.f / lt;
         if (a.out) {
-            uint4* dst = reinterpret_cast<uint4*>(a.out + row * kD);
+            uint4* dst = reinterpret_cast<uint4*>(a.out + row * kD + 64 * h);
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
+            for (int c = 0; c < 2; ++c) {
                 uint32_t o[32];
                 tmem_ld32(sO + c * 32, o);
                 tmem_ld_wait();
@@ -293,13 +314,27 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
                 }
             }
         }
-        const float lse2 = m_ref + __log2f(l);
-        a.lse2[row] = -lse2;  // stored negated: P2 computes s*c + nlse2 with one FFMA
-        if (a.lse_nat) a.lse_nat[row] = lse2 * kLn2;
+        if (h == 0) {
+            const float lse2 = m_ref + __log2f(lt);
+            a.nlse2[row] = -lse2;  // negated: P2 computes s*c + nlse2 with one FFMA
+            if (a.lse_nat) a.lse_nat[row] = lse2 * kLn2;
+        }
     }
     tc_fence_before();
     __syncthreads();
     if (warp == 0) tmem_dealloc<512>(tmem);
+}
+
+template <int kPoly>
+void fwd_launch(int grid, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+                const FwdArgs& fa, cudaStream_t s) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(fwd_tc_kernel<kPoly>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)kFwdSmem);
+        attr = true;
+    }
+    fwd_tc_kernel<kPoly><<<grid, kFwdThreads, kFwdSmem, s>>>(tq, tk, tv, fa);
 }
 
 }  // namespace
@@ -335,16 +370,8 @@ cudaError_t score_tc(const Dims& dm, const void* q, const void* k, const void* v
     fa.units = dm.units;
     fa.c = kLog2e / sqrtf((float)kD);
     fa.out = static_cast<__nv_bfloat16*>(o);
-    fa.lse2 = nlse2;
+    fa.nlse2 = nlse2;
     fa.lse_nat = lse;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(fwd_tc_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFwdSmem);
-        cudaFuncSetAttribute(fwd_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFwdSmem);
-        cudaFuncSetAttribute(fwd_tc_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFwdSmem);
-        cudaFuncSetAttribute(fwd_tc_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFwdSmem);
-        attr_set = true;
-    }
     const int n_fwd = dm.G >= 2 ? fa.nT * dm.units * (dm.G / 2) : (fa.nT / 2) * dm.units;
     // pairs (of every 8) whose exp2 runs on the FMA pipe; EMS_P1_POLY overrides (tuning)
     static const int poly = [] {
@@ -352,10 +379,10 @@ cudaError_t score_tc(const Dims& dm, const void* q, const void* k, const void* v
         return e ? atoi(e) : 0;
     }();
     switch (poly) {
-        case 0: fwd_tc_kernel<0><<<n_fwd, kFwdThreads, kFwdSmem, s>>>(tq, tk, tv, fa); break;
-        case 2: fwd_tc_kernel<2><<<n_fwd, kFwdThreads, kFwdSmem, s>>>(tq, tk, tv, fa); break;
-        case 4: fwd_tc_kernel<4><<<n_fwd, kFwdThreads, kFwdSmem, s>>>(tq, tk, tv, fa); break;
-        default: fwd_tc_kernel<3><<<n_fwd, kFwdThreads, kFwdSmem, s>>>(tq, tk, tv, fa); break;
+        case 1: fwd_launch<1>(n_fwd, tq, tk, tv, fa, s); break;
+        case 2: fwd_launch<2>(n_fwd, tq, tk, tv, fa, s); break;
+        case 3: fwd_launch<3>(n_fwd, tq, tk, tv, fa, s); break;
+        default: fwd_launch<0>(n_fwd, tq, tk, tv, fa, s); break;
     }
     ColArgs ca;
     ca.L = dm.L;

@@ -175,6 +175,7 @@ class Plan:
         dev = self.device
         nbytes = L_.ems_workspace_bytes(C.byref(self.desc))
         self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+        self.workspace[:256].zero_()  # device status word: no error recorded yet
         mk = lambda *s, dt=torch.float32: torch.zeros(s, dtype=dt, device=dev)  # noqa: E731
         self.glo = mk(B, Hkv, L)
         self.loc = mk(B, Hkv, L)

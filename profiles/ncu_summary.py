@@ -71,7 +71,9 @@ def launches(path):
                 k = d["Kernel Name"].split("(")[0][-70:]
                 unit = d["Metric Unit"]
                 v = float(d["Metric Value"].replace(",", ""))
-                v = v / 1e3 if unit == "nsecond" else (v * 1e3 if unit == "msecond" else v)
+                scale = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3,
+                         "msecond": 1e3, "s": 1e6, "second": 1e6}.get(unit, 1.0)
+                v = v * scale
                 agg.setdefault(k, []).append(v)
     tot = sum(sum(v) for v in agg.values())
     lines = ["| kernel | launches | mean us | share |", "|---|---|---|---|"]

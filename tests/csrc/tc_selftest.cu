@@ -194,7 +194,136 @@ __global__ void __launch_bounds__(512, 1) micro_kernel(int kind, int iters, long
     }
 }
 
+// MMA throughput: one elected thread issues `iters` MMAs (K=16 each) back to back on
+// operands already in smem/TMEM (garbage values; only timing matters).
+// kind 0: SS M128 N128   1: TS M128 N128 (A in TMEM)   2: SS M128 N256   3: SS M128 N128 B MN-major
+__global__ void __launch_bounds__(128, 1) mma_micro_kernel(int kind, int iters, long long* cyc) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tmem_base;
+    const int warp = threadIdx.x >> 5;
+    if (warp == 0) tmem_alloc<512>(&tmem_base);
+    if (threadIdx.x == 32) {
+        mbar_init(&bar, 1);
+        fence_barrier_init();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tm = tmem_base;
+    if (threadIdx.x == 0) {
+        const uint32_t a = smem_u32(sm), b = smem_u32(sm + 65536);
+        const int N = kind == 2 ? 256 : 128;
+        const uint32_t id = idesc_bf16(128, N, 0, kind == 3 ? 1 : 0);
+        const long long t0 = clock64();
+        if (kind >= 4) {  // descriptors precomputed outside the issue loop (kind-4 -> 0/1/2)
+            uint64_t ad[8], bd[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                ad[k] = sdesc(a + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024);
+                bd[k] = sdesc(b + (k >> 2) * 32768 + (k & 3) * 32, 16, 1024);
+            }
+            const uint32_t id2 = idesc_bf16(128, kind == 6 ? 256 : 128, 0, 0);
+            for (int i = 0; i < iters; i += 8) {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    if (kind == 5) mma_ts(tm, tm + 256 + k * 8, bd[k], id2, 1);
+                    else mma_ss(tm, ad[k], bd[k], id2, 1);
+                }
+            }
+        } else
+        for (int i = 0; i < iters; ++i) {
+            const int k = i & 7;
+            const uint64_t ad = sdesc(a + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024);
+            const uint64_t bd = kind == 3 ? sdesc(b + k * 2048, 16384, 1024)
+                                          : sdesc(b + (k >> 2) * 32768 + (k & 3) * 32, 16, 1024);
+            if (kind == 1)
+                mma_ts(tm, tm + 256 + k * 8, bd, id, 1);
+            else
+                mma_ss(tm, ad, bd, id, 1);
+        }
+        mma_commit(&bar);
+        mbar_wait(&bar, 0);
+        cyc[blockIdx.x] = clock64() - t0;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc<512>(tm);
+}
+
+// 2-SM (cta_group::2) MMA throughput on a CTA pair; the leader issues.
+// kind 0: SS M256 N128   1: TS M256 N128 (A in TMEM)   2: SS M256 N256
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
+    mma2_micro_kernel(int kind, int iters, long long* cyc) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tmem_base;
+    uint32_t rank;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    const int warp = threadIdx.x >> 5;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    if (threadIdx.x == 32) {
+        mbar_init(&bar, 1);
+        fence_barrier_init();
+    }
+    tc_fence_before();
+    asm volatile("barrier.cluster.arrive.release.aligned; barrier.cluster.wait.acquire.aligned;");
+    tc_fence_after();
+    const uint32_t tm = tmem_base;
+    if (rank == 0 && threadIdx.x == 0) {
+        const uint32_t a = smem_u32(sm), b = smem_u32(sm + 65536);
+        const int N = kind == 2 ? 256 : 128;
+        const uint32_t id = idesc_bf16(256, N, 0, 0);
+        const long long t0 = clock64();
+        for (int i = 0; i < iters; ++i) {
+            const int k = i & 7;
+            const uint64_t ad = sdesc(a + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024);
+            const uint64_t bd = sdesc(b + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024);
+            if (kind == 1)
+                asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, 1, 0;\n\t"
+                             "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tm),
+                             "r"(tm + 256 + k * 8), "l"(bd), "r"(id));
+            else
+                asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, 1, 0;\n\t"
+                             "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tm),
+                             "l"(ad), "l"(bd), "r"(id));
+        }
+        asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                     ::"r"(smem_u32(&bar)), "h"((uint16_t)1));
+        mbar_wait(&bar, 0);
+        cyc[blockIdx.x / 2] = clock64() - t0;
+    }
+    tc_fence_before();
+    asm volatile("barrier.cluster.arrive.release.aligned; barrier.cluster.wait.acquire.aligned;");
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tm));
+}
+
 }  // namespace
+
+extern "C" __attribute__((visibility("default"))) int ems_mma2_micro(int kind, int pairs, int iters,
+                                                                    long long* cyc) {
+    const int smem = 1024 + 65536 + 65536;
+    cudaFuncSetAttribute(mma2_micro_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    mma2_micro_kernel<<<2 * pairs, 128, smem>>>(kind, iters, cyc);
+    if (cudaGetLastError() != cudaSuccess) return 3;
+    if (cudaDeviceSynchronize() != cudaSuccess) return 4;
+    return 0;
+}
+
+extern "C" __attribute__((visibility("default"))) int ems_mma_micro(int kind, int blocks, int iters,
+                                                                   long long* cyc) {
+    const int smem = 1024 + 65536 + 65536;
+    cudaFuncSetAttribute(mma_micro_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    mma_micro_kernel<<<blocks, 128, smem>>>(kind, iters, cyc);
+    if (cudaGetLastError() != cudaSuccess) return 3;
+    if (cudaDeviceSynchronize() != cudaSuccess) return 4;
+    return 0;
+}
 
 extern "C" __attribute__((visibility("default"))) int ems_micro(int kind, int threads, int blocks,
                                                                int iters, long long* cyc, float* sink) {

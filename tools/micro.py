@@ -45,3 +45,36 @@ for threads in (128, 256, 512):
         c = run(kind, threads, 4096)
         res2[f"{name} {w}w B/clk"] = w * 4096 * 32 * 32 * 4 / c
 print(json.dumps(res2, indent=1))
+
+L.ems_mma_micro.argtypes = [C.c_int, C.c_int, C.c_int, C.c_void_p]
+res3 = {}
+for kind, (name, n) in {0: ("SS 128x128", 128), 1: ("TS 128x128", 128), 2: ("SS 128x256", 256),
+                        3: ("SS 128x128 B MN-major", 128)}.items():
+    cyc = torch.zeros(148, dtype=torch.int64, device="cuda")
+    it = 4096
+    assert L.ems_mma_micro(kind, 148, it, cyc.data_ptr()) == 0
+    c = cyc.double().median().item()
+    res3[name + " MAC/clk/SM"] = 128 * n * 16 * it / c
+print(json.dumps(res3, indent=1))
+
+L.ems_mma2_micro.argtypes = [C.c_int, C.c_int, C.c_int, C.c_void_p]
+res4 = {}
+for kind, (name, n) in {0: ("2SM SS 256x128", 128), 1: ("2SM TS 256x128", 128), 2: ("2SM SS 256x256", 256)}.items():
+    cyc = torch.zeros(74, dtype=torch.int64, device="cuda")
+    it = 4096
+    rc = L.ems_mma2_micro(kind, 74, it, cyc.data_ptr())
+    if rc:
+        res4[name] = f"rc={rc}"
+        continue
+    c = cyc.double().median().item()
+    res4[name + " MAC/clk/SM"] = 256 * n * 16 * it / c / 2
+print(json.dumps(res4, indent=1))
+
+res5 = {}
+for kind, (name, n) in {4: ("SS 128x128 pre-desc", 128), 5: ("TS 128x128 pre-desc", 128), 6: ("SS 128x256 pre-desc", 256)}.items():
+    cyc = torch.zeros(148, dtype=torch.int64, device="cuda")
+    it = 4096
+    assert L.ems_mma_micro(kind, 148, it, cyc.data_ptr()) == 0
+    c = cyc.double().median().item()
+    res5[name + " MAC/clk/SM"] = 128 * n * 16 * it / c
+print(json.dumps(res5, indent=1))
