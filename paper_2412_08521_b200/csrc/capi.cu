@@ -14,6 +14,10 @@ cudaError_t score_simt(const Dims& dm, int dtype, const void* q, const void* k, 
 cudaError_t score_tc(const Dims& dm, const void* q, const void* k, const void* v, void* o,
                      float* lse, float* glo, float* loc, void* ws, cudaStream_t s);
 size_t score_tc_workspace(const Dims& dm);
+size_t merge_tc_workspace(const Dims& dm);
+bool merge_tc_supported(const Dims& dm, int dtype);
+cudaError_t launch_merge_tc(const Dims& dm, const void* k, const void* v, const ems_stage& sg,
+                            double tau, int key_only, void* ws, cudaStream_t s);
 bool score_tc_supported(const Dims& dm, int dtype);
 cudaError_t launch_select(const Dims& dm, int l_win, int n_imp, int n_tbm, int kernel,
                           const float* glo, const float* loc, const ems_stage& sg,
@@ -71,7 +75,7 @@ size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
 // Workspace carve-up.  Offsets are deterministic functions of the descriptor.
 struct Layout {
-    size_t status, lse, glo, loc, pooled, cls, imp, tbm, pcount, dest, inv, cnt, mem, tc, total;
+    size_t status, lse, glo, loc, pooled, cls, imp, tbm, pcount, dest, inv, cnt, mem, tc, mtc, total;
 };
 
 Layout layout(const ems_desc& d) {
@@ -98,6 +102,7 @@ Layout layout(const ems_desc& d) {
     l.cnt = take(sizeof(int32_t) * U * (size_t)(m.cap_c + 1));
     l.mem = take(sizeof(int32_t) * U * (size_t)(m.cap_tbm > 0 ? m.cap_tbm : 1));
     l.tc = take(score_tc_workspace(m));
+    l.mtc = take(merge_tc_supported(m, d.dtype) ? merge_tc_workspace(m) : 0);
     l.total = off;
     return l;
 }
@@ -189,14 +194,20 @@ int run_merge(const ems_desc* desc, const void* k_raw, const void* v, const ems_
     const Dims m = make_dims(*desc);
     if (m.cap_tbm <= 0) return EMS_OK;
     const Layout l = layout(*desc);
-    float* inv = at<float>(ws, l.inv);
-    const size_t U = m.units;
-    float* inv_kc = inv;
-    float* inv_vc = inv_kc + U * m.cap_c;
-    float* inv_kt = inv_vc + U * m.cap_c;
-    float* inv_vt = inv_kt + U * m.cap_tbm;
-    cudaError_t e = launch_merge_assign(m, desc->dtype, k_raw, v, sg, desc->tau, desc->key_only,
-                                        inv_kc, inv_vc, inv_kt, inv_vt, s);
+    cudaError_t e;
+    // tensor-core similarity for bf16 / d = 128 unless the SIMT kernels are forced
+    if (desc->score_impl != EMS_SCORE_SIMT && merge_tc_supported(m, desc->dtype)) {
+        e = launch_merge_tc(m, k_raw, v, sg, desc->tau, desc->key_only, at<void>(ws, l.mtc), s);
+    } else {
+        float* inv = at<float>(ws, l.inv);
+        const size_t U = m.units;
+        float* inv_kc = inv;
+        float* inv_vc = inv_kc + U * m.cap_c;
+        float* inv_kt = inv_vc + U * m.cap_c;
+        float* inv_vt = inv_kt + U * m.cap_tbm;
+        e = launch_merge_assign(m, desc->dtype, k_raw, v, sg, desc->tau, desc->key_only, inv_kc,
+                                inv_vc, inv_kt, inv_vt, s);
+    }
     if (e != cudaSuccess) {
         set_error("merge launch: %s", cudaGetErrorString(e));
         return EMS_CUDA_ERROR;

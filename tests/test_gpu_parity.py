@@ -182,3 +182,20 @@ def test_gpu_redundancy_cross_matches_oracle(oracle):
     want = oracle.redundancy_cross(kr, vr, kc, vc)
     np.testing.assert_allclose(r, want, atol=2e-6)
     assert abs(r[5, 7] - 1.0) < 1e-5 and np.all(r[:, 3] == 0.0)
+
+
+@pytest.mark.parametrize("wname,L,key_only", [("cfgM", 2048, False), ("cfgM", 2048, True), ("cfg3b", 4096, False)])
+def test_gpu_tc_merge_matches_simt_and_oracle(wname, L, key_only, oracle):
+    """Tensor-core similarity/argmax (merge_tc.cu) vs the SIMT kernels and the oracle."""
+    w = CONFIGS[wname]
+    units = [make_unit_np(w, seed=5, seq_len=L, unit=u) for u in range(2)]
+    cfg = _cfg_of(w)
+    cfg.key_only = key_only
+    a = run_gpu(units, w.dtype, cfg, score_impl="auto")
+    b = run_gpu(units, w.dtype, cfg, score_impl="simt")
+    for i, un in enumerate(units):
+        ref = oracle.prefill_unit(un.q_rot, un.k_rot, un.k_raw, un.v, cfg)
+        rep = check_unit(a, i, un, ref, ref.extra["glo"], ref.extra["loc"], w.dtype, cfg, oracle)
+        check_unit(b, i, un, ref, ref.extra["glo"], ref.extra["loc"], w.dtype, cfg, oracle)
+        if wname == "cfgM":
+            assert rep["merged"] > 0
