@@ -396,6 +396,12 @@ cudaError_t score_tc(const Dims& dm, const void* q, const void* k, const void* v
     ca.nlse2 = nlse2;
     ca.glo = glo;
     ca.loc = loc;
+    // P2 variant: 2 = CTA-pair (cta_group::2, M = N = 256) kernel, 1 = single-CTA kernel
+    static const int p2 = [] {
+        const char* e = getenv("EMS_P2_IMPL");
+        return e ? atoi(e) : 2;
+    }();
+    if (p2 == 2) return launch_colsum2_tc(ca, tk, tq, s);
     return launch_colsum_tc(ca, tk, tq, s);
 }
 

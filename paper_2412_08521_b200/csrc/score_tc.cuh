@@ -39,5 +39,7 @@ struct ColArgs {
 
 cudaError_t launch_colsum_tc(const sc::ColArgs& a, const CUtensorMap& tk, const CUtensorMap& tq,
                              cudaStream_t s);
+cudaError_t launch_colsum2_tc(const sc::ColArgs& a, const CUtensorMap& tk, const CUtensorMap& tq,
+                              cudaStream_t s);
 
 }  // namespace ems

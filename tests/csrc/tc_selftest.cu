@@ -303,7 +303,98 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tm));
 }
 
+// 2-SM correctness: D[256 x N] = A[256 x 128] * B[N x 128]^T on a CTA pair.  CTA r holds
+// A rows [128r, 128r+128) and B rows [N/2 r, N/2 (r+1)); TMA completes on the leader's
+// barrier; the leader issues cta_group::2 MMAs and multicasts the commit to both CTAs.
+// mode bit 0: A staged in TMEM (TS) instead of smem.  N = 256 (mode bit 1 clear) or 128.
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
+    selftest2_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
+                     const __nv_bfloat16* A, float* D, int mode) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sa = sm;            // this CTA's 128 A rows (32 KB)
+    uint8_t* sb = sm + 32768;    // this CTA's N/2 B rows
+    __shared__ uint64_t bar_load, bar_mma;
+    __shared__ uint32_t tmem_base;
+    const uint32_t rank = cluster_ctarank();
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const bool a_tmem = mode & 1;
+    const int N = (mode & 2) ? 128 : 256, nb = N / 2;
+    if (warp == 0) tmem_alloc_2sm<512>(&tmem_base);
+    if (tid == 32) {
+        mbar_init(&bar_load, 1);
+        mbar_init(&bar_mma, 1);
+        fence_barrier_init();
+    }
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tm = tmem_base;
+    if (tid == 0) {
+        if (rank == 0) mbar_expect_tx(&bar_load, 2 * (32768 + nb * 256));
+        tma_load_3d_2sm(sa, &ta, &bar_load, 0, 128 * rank, 0);
+        tma_load_3d_2sm(sa + 16384, &ta, &bar_load, 64, 128 * rank, 0);
+        tma_load_3d_2sm(sb, &tb, &bar_load, 0, nb * rank, 0);
+        tma_load_3d_2sm(sb + nb * 128, &tb, &bar_load, 64, nb * rank, 0);
+    }
+    if (a_tmem) {
+        uint32_t r[32];
+        for (int c = 0; c < 2; ++c) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                const __nv_bfloat16* p = A + (128 * rank + tid) * 128 + c * 64 + 2 * j;
+                r[j] = pack_bf16(__bfloat162float(p[0]), __bfloat162float(p[1]));
+            }
+            tmem_st32(tm + ((uint32_t)(warp * 32) << 16) + 256 + c * 32, r);
+        }
+        tmem_st_wait();
+    }
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    if (rank == 0 && tid == 0) {
+        mbar_wait(&bar_load, 0);
+        tc_fence_after();
+        const uint32_t idesc = idesc_bf16(256, N, 0, 0);
+        for (int k = 0; k < 8; ++k) {
+            const uint64_t bd = sdesc(smem_u32(sb) + (k >> 2) * (nb * 128) + (k & 3) * 32, 16, 1024);
+            if (a_tmem)
+                mma_ts_2sm(tm, tm + 256 + k * 8, bd, idesc, k > 0);
+            else
+                mma_ss_2sm(tm, sdesc(smem_u32(sa) + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024), bd, idesc,
+                           k > 0);
+        }
+        mma_commit_2sm(&bar_mma, 0x3);
+    }
+    mbar_wait(&bar_mma, 0);
+    tc_fence_after();
+    for (int c = 0; c < N / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld32(tm + ((uint32_t)(warp * 32) << 16) + c * 32, r);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) D[(128 * rank + tid) * N + c * 32 + j] = __uint_as_float(r[j]);
+    }
+    tc_fence_before();
+    cluster_sync();
+    if (warp == 0) tmem_dealloc_2sm<512>(tm);
+}
+
 }  // namespace
+
+extern "C" __attribute__((visibility("default"))) int ems_tc_selftest2(int mode, const void* A,
+                                                                      const void* B, float* D) {
+    CUtensorMap ta, tb;
+    const int N = (mode & 2) ? 128 : 256;
+    if (!make_tmap_bf16_3d(&ta, A, 128, 256, 1, 128)) return 1;
+    if (!make_tmap_bf16_3d(&tb, B, 128, N, 1, N / 2)) return 2;
+    const int smem = 1024 + 32768 + 32768;
+    cudaFuncSetAttribute(selftest2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    selftest2_kernel<<<2, 128, smem>>>(ta, tb, (const __nv_bfloat16*)A, D, mode);
+    if (cudaGetLastError() != cudaSuccess) return 3;
+    if (cudaDeviceSynchronize() != cudaSuccess) return 4;
+    return 0;
+}
 
 extern "C" __attribute__((visibility("default"))) int ems_mma2_micro(int kind, int pairs, int iters,
                                                                     long long* cyc) {

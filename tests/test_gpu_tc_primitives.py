@@ -34,3 +34,18 @@ def test_mma_modes(st, mode):
     want = A.float() @ (B.float() if mode & 1 else B.float().t())
     err = (D - want).abs().max().item() / want.abs().max().item()
     assert err < 1e-5, f"mode {mode}: rel err {err}"
+
+
+@pytest.mark.parametrize("mode", [0, 1, 2, 3])
+def test_mma_2sm(st, mode):
+    """cta_group::2: M = 256 over a CTA pair, N = 256 (mode & 2 == 0) or 128; TS when mode & 1."""
+    st.ems_tc_selftest2.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]
+    N = 128 if mode & 2 else 256
+    g = torch.Generator(device="cuda").manual_seed(10 + mode)
+    A = torch.randn(256, 128, generator=g, device="cuda").bfloat16()
+    B = torch.randn(N, 128, generator=g, device="cuda").bfloat16()
+    D = torch.zeros(256, N, device="cuda")
+    assert st.ems_tc_selftest2(mode, A.data_ptr(), B.data_ptr(), D.data_ptr()) == 0
+    want = A.float() @ B.float().t()
+    err = (D - want).abs().max().item() / want.abs().max().item()
+    assert err < 1e-5, f"mode {mode}: rel err {err}"

@@ -48,7 +48,7 @@ def child(cfg: str, reps: int) -> dict:
     kern = {}
     for e in prof.key_averages():
         if e.device_time_total > 0 and ("tc_kernel" in e.key or "simt" in e.key):
-            name = "fwd_tc" if "fwd_tc" in e.key else ("colsum_tc" if "colsum_tc" in e.key else e.key[:40])
+            name = "fwd_tc" if "fwd_tc" in e.key else ("colsum_tc" if "colsum" in e.key else e.key[:40])
             kern[name] = round(e.device_time_total / e.count / 1e3, 3)
     return {"ms": sorted(ts)[len(ts) // 2], "min_ms": min(ts), "kernels_ms": kern,
             "glo_mass_err": float((glo.sum(-1) - L).abs().max().item() / L)}
