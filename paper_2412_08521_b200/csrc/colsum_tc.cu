@@ -9,12 +9,14 @@
 // One CTA owns TWO 128-key tiles (J0 = 2*jp, J1 = J0 + 1) of one unit, both resident
 // in smem, and streams every (query head h, query tile I >= J0) through a 4-stage
 // TMA ring.  Each streamed Q tile feeds two SS MMAs  S^T_w = K_Jw Q_I^T  (keys on
-// TMEM lanes), which halves the L2 traffic per MMA compared with one key tile per
-// CTA (v1 was L2-bandwidth bound).  Warpgroup w owns key tile Jw: thread m owns key
-// Jw*128 + m and the column sum over the 128 queries is an in-thread row sum.
-// Interior tiles take a mask-free path where kPoly of every 8 exp2 pairs run as a
-// degree-5 polynomial on the FMA pipe (ex2_poly2) and the rest on MUFU.  Per-item
-// fp32 sums are accumulated in fp64 in item order -> deterministic.
+// TMEM lanes), so the L2 traffic per MMA is half that of one key tile per CTA.
+// Four column warpgroups: warpgroup (w, hc) owns key tile Jw and query columns
+// [64 hc, 64 hc + 64) of every item; thread m owns key Jw*128 + m, so the column sum
+// over queries is an in-thread row sum (no atomics).  Interior tiles take a
+// mask-free path where kPoly of every 8 exp2 pairs run as a degree-5 polynomial on
+// the FMA pipe (ex2_poly2) and the rest on MUFU.  Per-item fp32 sums are accumulated
+// in fp64 in item order and the two column halves are combined in a fixed order ->
+// deterministic.
 #include <stdlib.h>
 
 #include "score_tc.cuh"
@@ -28,8 +30,8 @@ using namespace sc;
 
 constexpr int kQStages = 4;
 constexpr int kBufs = 2;                 // TMEM: 2 x (2 key tiles x 128 cols) = 512 cols
-constexpr int kThreads = 384;            // w0 TMA, w1 MMA, w4-7 key tile J0, w8-11 key tile J1
-constexpr size_t kSmem = 1024 + (2 + kQStages) * kTileBytes + kBufs * 512;
+constexpr int kThreads = 640;            // w0 TMA, w1 MMA, w2-3 spare, w4-19 column sums
+constexpr size_t kSmem = 1024 + (2 + kQStages) * kTileBytes + kBufs * 512 + 2 * 2 * 128 * 8;
 
 struct Bars {
     uint64_t k_full;
@@ -38,69 +40,62 @@ struct Bars {
     uint32_t tmem_base;
 };
 
-// Process one 128-query row of S^T for the thread's key (general path: masks).
-__device__ __forceinline__ void row_masked(uint32_t sa, uint32_t lb, float c, int I, int Jw,
-                                           int mrow, int loc_start, float& sg, float& sl) {
-    const bool diag = (I == Jw);
+// 64 query columns of the thread's key row, general path (causal mask + window).
+__device__ __forceinline__ void cols_masked(uint32_t sa, uint32_t lb, float c, int q0, int key,
+                                            int loc_start, float& sg, float& sl) {
     sg = 0.f;
     sl = 0.f;
-#pragma unroll 1
-    for (int h2 = 0; h2 < 2; ++h2) {
-        uint32_t r[2][32];
-        tmem_ld32(sa + h2 * 64, r[0]);
-        tmem_ld32(sa + h2 * 64 + 32, r[1]);
-        tmem_ld_wait();
+    uint32_t r[2][32];
+    tmem_ld32(sa, r[0]);
+    tmem_ld32(sa + 32, r[1]);
+    tmem_ld_wait();
 #pragma unroll
-        for (int cc = 0; cc < 2; ++cc) {
-            const int c0 = (2 * h2 + cc) * 32;
+    for (int cc = 0; cc < 2; ++cc)
 #pragma unroll
-            for (int x = 0; x < 32; ++x) {
-                const int n = c0 + x;
-                float p = ex2(fmaf(__uint_as_float(r[cc][x]), c, lds32(lb + 4 * n)));
-                if (diag && n < mrow) p = 0.f;  // query < key: masked
-                sg += p;
-                if (I * kTile + n >= loc_start) sl += p;
-            }
+        for (int x = 0; x < 32; ++x) {
+            const int n = cc * 32 + x, qi = q0 + n;
+            float p = ex2(fmaf(__uint_as_float(r[cc][x]), c, lds32(lb + 4 * n)));
+            if (qi < key) p = 0.f;  // query before key: masked
+            sg += p;
+            if (qi >= loc_start) sl += p;
         }
-    }
 }
 
+// 64 query columns, interior tile: no masks.  c = log2(e)/sqrt(128) is a literal (the
+// tensor-core path is d = 128 only); groups of 4 pairs are tree-summed before entering
+// one of 4 independent accumulators, keeping the FADD dependency chains short.
+constexpr float kC128 = 0.12751743f;
 template <int kPoly>
-__device__ __forceinline__ float row_fast(uint32_t sa, uint32_t lb, float c) {
-    const float2 c2 = make_float2(c, c);
-    float2 acc = make_float2(0.f, 0.f);
+__device__ __forceinline__ float cols_fast(uint32_t sa, uint32_t lb) {
+    const float2 c2 = make_float2(kC128, kC128);
+    uint32_t r[2][32];
+    tmem_ld32(sa, r[0]);
+    tmem_ld32(sa + 32, r[1]);
+    tmem_ld_wait();
+    float2 acc[4];
 #pragma unroll
-    for (int h2 = 0; h2 < 2; ++h2) {
-        uint32_t r[2][32];
-        tmem_ld32(sa + h2 * 64, r[0]);
-        tmem_ld32(sa + h2 * 64 + 32, r[1]);
-        tmem_ld_wait();
+    for (int g = 0; g < 4; ++g) acc[g] = make_float2(0.f, 0.f);
 #pragma unroll
-        for (int cc = 0; cc < 2; ++cc) {
-            const uint32_t lc = lb + (2 * h2 + cc) * 128;
-            float2 s0 = make_float2(0.f, 0.f), s1 = make_float2(0.f, 0.f);
+    for (int cc = 0; cc < 2; ++cc) {
 #pragma unroll
-            for (int x = 0; x < 32; x += 4) {
-                const float4 lv = lds128(lc + 4 * x);
-                const float2 a0 = __ffma2_rn(
-                    make_float2(__uint_as_float(r[cc][x]), __uint_as_float(r[cc][x + 1])), c2,
-                    make_float2(lv.x, lv.y));
-                const float2 a1 = __ffma2_rn(
-                    make_float2(__uint_as_float(r[cc][x + 2]), __uint_as_float(r[cc][x + 3])), c2,
-                    make_float2(lv.z, lv.w));
-                const int e0 = x / 2, e1 = x / 2 + 1;
-                float2 p0, p1;
-                if ((e0 & 7) < kPoly) p0 = ex2_poly2(a0);
-                else p0 = make_float2(ex2(a0.x), ex2(a0.y));
-                if ((e1 & 7) < kPoly) p1 = ex2_poly2(a1);
-                else p1 = make_float2(ex2(a1.x), ex2(a1.y));
-                s0 = __fadd2_rn(s0, p0);
-                s1 = __fadd2_rn(s1, p1);
+        for (int x = 0; x < 32; x += 8) {
+            const float4 l0 = lds128(lb + 4 * (cc * 32 + x));
+            const float4 l1 = lds128(lb + 4 * (cc * 32 + x + 4));
+            const float2 lv[4] = {make_float2(l0.x, l0.y), make_float2(l0.z, l0.w), make_float2(l1.x, l1.y),
+                                  make_float2(l1.z, l1.w)};
+            float2 p[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const float2 arg = __ffma2_rn(
+                    make_float2(__uint_as_float(r[cc][x + 2 * e]), __uint_as_float(r[cc][x + 2 * e + 1])), c2, lv[e]);
+                p[e] = ((x / 2 + e) & 7) < kPoly ? ex2_poly2(arg) : make_float2(ex2(arg.x), ex2(arg.y));
             }
-            acc = __fadd2_rn(acc, __fadd2_rn(s0, s1));
+            const int g = (x / 8) & 3;
+            acc[g] = __fadd2_rn(acc[g], __fadd2_rn(__fadd2_rn(p[0], p[1]), __fadd2_rn(p[2], p[3])));
         }
     }
-    return acc.x + acc.y;
+    const float2 s = __fadd2_rn(__fadd2_rn(acc[0], acc[1]), __fadd2_rn(acc[2], acc[3]));
+    return s.x + s.y;
 }
 
 template <int kPoly>
@@ -113,6 +108,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* sk = sm;                                  // K_J0 | K_J1 (2 x 32 KB)
     uint8_t* sq = sk + 2 * kTileBytes;                 // Q ring
     float* slse = reinterpret_cast<float*>(sq + kQStages * kTileBytes);  // [kBufs][128]
+    double* spart = reinterpret_cast<double*>(slse + kBufs * 128);       // [2 key tiles][2][128]
     __shared__ Bars bars;
 
     const int tid = threadIdx.x, warp = tid >> 5;
@@ -134,7 +130,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int s = 0; s < kBufs; ++s) {
             mbar_init(&bars.s_full[s], 1);
-            mbar_init(&bars.s_empty[s], 256);
+            mbar_init(&bars.s_empty[s], 16);   // one arrival per column warp
             mbar_init(&bars.l_full[s], 1);
         }
         fence_barrier_init();
@@ -187,9 +183,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t d0 = tmem + bb * 256;
 #pragma unroll
                 for (int k = 0; k < 8; ++k)
-                    mma_ss(d0, sdesc(kmajor_addr(ka0, k), 16, 1024), sdesc(kmajor_addr(qa, k), 16, 1024),
-                           id_s, k > 0);
-                if (has1 && I >= J0 + 1) {  // key tile J1 is fully masked against query tile J0
+                    if (a.debug != 2)
+                        mma_ss(d0, sdesc(kmajor_addr(ka0, k), 16, 1024),
+                               sdesc(kmajor_addr(qa, k), 16, 1024), id_s, k > 0);
+                if (has1 && I >= J0 + 1 && a.debug != 2) {  // key tile J1 is fully masked vs query tile J0
 #pragma unroll
                     for (int k = 0; k < 8; ++k)
                         mma_ss(d0 + 128, sdesc(kmajor_addr(ka1, k), 16, 1024),
@@ -201,10 +198,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp >= 4) {
         // ------------------------------------------------------------- column sums
-        const int w = (warp - 4) >> 2;          // key tile J0 + w
+        const int w = (warp - 4) >> 3;          // key tile J0 + w
+        const int hc = ((warp - 4) >> 2) & 1;   // query columns [64 hc, 64 hc + 64)
         const int wi = warp & 3;
         const int mrow = wi * 32 + (tid & 31);  // key within the tile
         const int Jw = J0 + w;
+        const int key = Jw * kTile + mrow;
         const bool active = (w == 0) || has1;
         const int loc_start = a.L - a.lwin;
         const int last_interior = (loc_start / kTile) - 1;  // tiles <= this hold no window query
@@ -216,25 +215,33 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(&bars.l_full[bb], ph);
             mbar_wait(&bars.s_full[bb], ph);
             tc_fence_after();
-            if (active && I >= Jw) {
-                const uint32_t sa = tmem_lane_addr(tmem + bb * 256 + w * 128, wi);
-                const uint32_t lb = smem_u32(slse + bb * 128);
+            if (active && I >= Jw && a.debug != 1) {
+                const uint32_t sa = tmem + bb * 256 + w * 128 + 64 * hc + ((uint32_t)(wi * 32) << 16);
+                const uint32_t lb = smem_u32(slse + bb * 128 + 64 * hc);
                 if (I > Jw && I <= last_interior) {
-                    acc_g += (double)row_fast<kPoly>(sa, lb, a.c);
+                    acc_g += (double)cols_fast<kPoly>(sa, lb);
                 } else {
                     float sg, sl;
-                    row_masked(sa, lb, a.c, I, Jw, mrow, loc_start, sg, sl);
+                    cols_masked(sa, lb, a.c, I * kTile + 64 * hc, key, loc_start, sg, sl);
                     acc_g += (double)sg;
                     acc_l += (double)sl;
                 }
             }
             tc_fence_before();
-            mbar_arrive(&bars.s_empty[bb]);
+            __syncwarp();
+            if ((tid & 31) == 0) mbar_arrive(&bars.s_empty[bb]);
         }
-        if (active) {
+        // combine the two column halves in a fixed order: (half 0 + half 1) / G
+        double* sp = spart + w * 256;
+        if (hc == 1) {
+            sp[mrow] = acc_g;
+            sp[128 + mrow] = acc_l;
+        }
+        asm volatile("bar.sync %0, 256;" ::"r"(1 + w) : "memory");
+        if (hc == 0 && active) {
             const size_t o = (size_t)unit * a.L + (size_t)Jw * kTile + mrow;
-            a.glo[o] = (float)(acc_g / a.G);
-            a.loc[o] = (float)(acc_l / a.G);
+            a.glo[o] = (float)((acc_g + sp[mrow]) / a.G);
+            a.loc[o] = (float)((acc_l + sp[128 + mrow]) / a.G);
         }
     }
     tc_fence_before();
@@ -262,7 +269,7 @@ cudaError_t launch_colsum_tc(const ColArgs& a, const CUtensorMap& tk, const CUte
     // pairs (of every 8) whose exp2 runs on the FMA pipe; EMS_P2_POLY overrides (tuning)
     static const int poly = [] {
         const char* e = getenv("EMS_P2_POLY");
-        return e ? atoi(e) : 3;
+        return e ? atoi(e) : 2;
     }();
     switch (poly) {
         case 0: return launch_t<0>(a, tk, tq, s);

@@ -242,9 +242,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             // exchange half-row maxima (also orders both halves' S loads before any P store,
             // since P of half 1 overwrites S columns 32..63 of half 0)
             float* xb = xt + (j & 1) * 256;
-            xb[h * 128 + m] = hm;
+            const uint32_t xs = smem_u32(xb);  // explicit shared ops (generic LD/ST stall here)
+            sts32(xs + 4 * (h * 128 + m), hm);
             named_sync(bar_id, 256);
-            const float mx = fmaxf(hm, xb[(h ^ 1) * 128 + m]);
+            const float mx = fmaxf(hm, lds32(xs + 4 * ((h ^ 1) * 128 + m)));
             const float mx2 = mx * a.c;
             const bool need = mx2 > m_ref + kRescaleThresh;
             const bool warp_need = __any_sync(0xffffffffu, need);
@@ -289,9 +290,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         }
         // epilogue: l = l_half0 + l_half1 (fixed order), O / l -> bf16, LSE
         float* xb = xt + ((I + 1) & 1) * 256;
-        xb[h * 128 + m] = l;
+        const uint32_t xs = smem_u32(xb);
+        sts32(xs + 4 * (h * 128 + m), l);
         named_sync(bar_id, 256);
-        const float lt = h == 0 ? l + xb[128 + m] : xb[m] + l;
+        const float lt = h == 0 ? l + lds32(xs + 4 * (128 + m)) : lds32(xs + 4 * m) + l;
         mbar_wait(&bars.o_full[t], I & 1);
         tc_fence_after();
         const size_t row = (size_t)plane[t] * a.L + (size_t)I * kTile + m;
@@ -396,10 +398,15 @@ cudaError_t score_tc(const Dims& dm, const void* q, const void* k, const void* v
     ca.nlse2 = nlse2;
     ca.glo = glo;
     ca.loc = loc;
+    static const int p2_debug = [] {
+        const char* e = getenv("EMS_P2_DEBUG");  // profiling experiments only
+        return e ? atoi(e) : 0;
+    }();
+    ca.debug = p2_debug;
     // P2 variant: 2 = CTA-pair (cta_group::2, M = N = 256) kernel, 1 = single-CTA kernel
     static const int p2 = [] {
         const char* e = getenv("EMS_P2_IMPL");
-        return e ? atoi(e) : 2;
+        return e ? atoi(e) : 1;
     }();
     if (p2 == 2) return launch_colsum2_tc(ca, tk, tq, s);
     return launch_colsum_tc(ca, tk, tq, s);

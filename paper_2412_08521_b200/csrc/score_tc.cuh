@@ -33,6 +33,7 @@ struct ColArgs {
     const float* nlse2;    // [B*Hq][L] negated log2-domain LSE from P1
     float* glo;            // [units][L]
     float* loc;
+    int debug = 0;         // profiling only: 1 = skip the exp epilogue, 2 = skip the MMAs
 };
 
 }  // namespace sc

@@ -266,6 +266,9 @@ __device__ __forceinline__ float4 lds128(uint32_t saddr) {
                  : "r"(saddr));
     return v;
 }
+__device__ __forceinline__ void sts32(uint32_t saddr, float v) {
+    asm volatile("st.shared.f32 [%0], %1;" ::"r"(saddr), "f"(v) : "memory");
+}
 __device__ __forceinline__ float lds32(uint32_t saddr) {
     float v;
     asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(saddr));
