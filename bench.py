@@ -70,7 +70,7 @@ class ClockSampler:
 
     def __init__(self, index: int, period_s: float = 0.005):
         self.index, self.period = index, period_s
-        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self.samples, self.reasons, self.max_mhz, self.power = [], set(), None, []
 
     def _run(self):
         import pynvml
@@ -78,6 +78,10 @@ class ClockSampler:
         self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
         while not self._stop.is_set():
             self.samples.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+            try:
+                self.power.append(pynvml.nvmlDeviceGetPowerUsage(h) / 1000.0)
+            except pynvml.NVMLError:
+                pass
             r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
             for n, bit in self.REASONS.items():
                 if r & bit:
@@ -111,7 +115,8 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
         return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
                 "reasons": sorted(self.reasons), "samples": len(self.samples),
-                "sm_mhz_min": min(self.samples)}
+                "sm_mhz_min": min(self.samples),
+                "power_w_max": max(self.power) if self.power else None}
 
 
 def dist_env():
@@ -335,6 +340,7 @@ def main():
             "stage_ms": {"score": score_ms, "select+merge+compact": tail_ms},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
                          "frac": achieved / peak_tf, "traffic": None,
+                         "frac_of_sustained_peak": achieved / pk.get("bf16_tflops_sustained", peak_tf),
                          "kernel": "score pass (O+LSE and glo/loc column sums)",
                          "peak_source": f"{pk['source']} bf16_tflops (burst)",
                          "algorithmic_flops_per_launch": flops},
