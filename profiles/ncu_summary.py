@@ -83,6 +83,9 @@ def launches(path):
 
 
 if __name__ == "__main__":
+    out_arg = sys.argv[2] if sys.argv[1] == "--launches" else sys.argv[1]
+    if not out_arg.endswith(".md"):
+        sys.exit(f"output must be a .md summary, got {out_arg!r} (would clobber a report)")
     if sys.argv[1] == "--launches":
         text = launches(sys.argv[3])
         out = sys.argv[2]
