@@ -44,9 +44,9 @@ struct FwdArgs {
 };
 
 constexpr int kFwdStages = 2;
-// w0 TMA, w1 MMA, w2-3 spare; softmax warps 4..19: slot t = (w-4)/8, column half
-// h = ((w-4)/4) % 2, TMEM sub-partition w % 4.
-constexpr int kFwdThreads = 640;
+// w0 TMA, w1 MMA; softmax warps 2..17: slot t = (w-2)/8, column half
+// h = ((w-2)/4) % 2, TMEM sub-partition w % 4.
+constexpr int kFwdThreads = 576;
 constexpr size_t kFwdSmem = 1024 + (2 + 2 * kFwdStages) * kTileBytes + 2 * 2 * 2 * 128 * 4;
 
 struct FwdBars {
@@ -207,10 +207,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
                 mma_commit(&bars.kv_empty[s]);
             }
         }
-    } else if (warp >= 4) {
+    } else {
         // ---------------------------------------------------------------- softmax (half rows)
-        const int t = (warp - 4) >> 3;          // slot
-        const int h = ((warp - 4) >> 2) & 1;    // column half: keys [64h, 64h + 64)
+        const int t = (warp - 2) >> 3;          // slot
+        const int h = ((warp - 2) >> 2) & 1;    // column half: keys [64h, 64h + 64)
         const int wi = warp & 3;                // TMEM sub-partition
         const int m = wi * 32 + (tid & 31);     // row within the tile
         const int I = tile[t];
@@ -234,11 +234,19 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
                     for (int x = 0; x < 32; ++x)
                         if (64 * h + c * 32 + x > m) r[c][x] = __float_as_uint(-INFINITY);
             }
-            float hm = -INFINITY;
+            // half-row max: 3-input FMNMX3, four independent chains
+            float hmv[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
             for (int c = 0; c < 2; ++c)
 #pragma unroll
-                for (int x = 0; x < 32; ++x) hm = fmaxf(hm, __uint_as_float(r[c][x]));
+                for (int x = 0; x < 32; x += 8)
+#pragma unroll
+                    for (int g = 0; g < 4; g += 2) {
+                        hmv[g] = fmax3(hmv[g], __uint_as_float(r[c][x + 2 * g]), __uint_as_float(r[c][x + 2 * g + 1]));
+                        hmv[g + 1] = fmax3(hmv[g + 1], __uint_as_float(r[c][x + 2 * g + 2]),
+                                           __uint_as_float(r[c][x + 2 * g + 3]));
+                    }
+            const float hm = fmax3(hmv[0], hmv[1], fmaxf(hmv[2], hmv[3]));
             // exchange half-row maxima (also orders both halves' S loads before any P store,
             // since P of half 1 overwrites S columns 32..63 of half 0)
             float* xb = xt + (j & 1) * 256;

@@ -19,7 +19,7 @@ from dataclasses import dataclass
 import torch
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libems_b200.so")
+LIB_PATH = os.environ.get("EMS_LIB_PATH") or os.path.join(PKG, "libems_b200.so")  # override: A/B tuning only
 
 EMS_F32, EMS_BF16 = 0, 1
 SCORE_IMPL = {"auto": 0, "simt": 1, "tcgen05": 2}

@@ -194,6 +194,76 @@ __global__ void __launch_bounds__(512, 1) micro_kernel(int kind, int iters, long
     }
 }
 
+// Exp-epilogue throughput in isolation (no TMEM, no barriers): the P2 column-sum inner
+// loop of colsum_tc.cu on register-resident logits.  kPoly pairs of every 8 run on the
+// FMA pipe.  Reports cycles for `iters` passes of 64 columns per thread.
+template <int kPoly>
+__device__ __forceinline__ float epi_cols64(const uint32_t (&r)[2][32], uint32_t lb, float cs) {
+    const float2 c2 = make_float2(cs, cs);
+    float2 acc[4];
+#pragma unroll
+    for (int g = 0; g < 4; ++g) acc[g] = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int cc = 0; cc < 2; ++cc) {
+#pragma unroll
+        for (int x = 0; x < 32; x += 8) {
+            const float4 l0 = lds128(lb + 4 * (cc * 32 + x));
+            const float4 l1 = lds128(lb + 4 * (cc * 32 + x + 4));
+            const float2 lv[4] = {make_float2(l0.x, l0.y), make_float2(l0.z, l0.w), make_float2(l1.x, l1.y),
+                                  make_float2(l1.z, l1.w)};
+            float2 p[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const float2 arg = __ffma2_rn(
+                    make_float2(__uint_as_float(r[cc][x + 2 * e]), __uint_as_float(r[cc][x + 2 * e + 1])), c2, lv[e]);
+                p[e] = ((x / 2 + e) & 7) < kPoly ? ex2_poly2(arg) : make_float2(ex2(arg.x), ex2(arg.y));
+            }
+            const int g = (x / 8) & 3;
+            acc[g] = __fadd2_rn(acc[g], __fadd2_rn(__fadd2_rn(p[0], p[1]), __fadd2_rn(p[2], p[3])));
+        }
+    }
+    const float2 s = __fadd2_rn(__fadd2_rn(acc[0], acc[1]), __fadd2_rn(acc[2], acc[3]));
+    return s.x + s.y;
+}
+
+template <int kPoly, int kDouble>
+__global__ void __launch_bounds__(512, 1) epi_micro_kernel(int iters, int zmask, long long* cyc, float* sink) {
+    __shared__ __align__(16) float lse[128];
+    if (threadIdx.x < 128) lse[threadIdx.x] = -14.f - 0.01f * threadIdx.x;
+    __syncthreads();
+    uint32_t r[2][32];
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int x = 0; x < 32; ++x) r[c][x] = __float_as_uint(0.37f * ((threadIdx.x * 7 + c * 32 + x) % 61) - 11.f);
+    const uint32_t lb = smem_u32(lse);
+    double accd = 0.0;
+    float accf = 0.f;
+    const long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+        // the scale depends on the (runtime-zero) iteration mask, so nothing can be hoisted
+        const float v = epi_cols64<kPoly>(r, lb, 0.12751743f + (float)(it & zmask));
+        if (kDouble) accd += (double)v;
+        else accf += v;
+    }
+    asm volatile("" ::"f"(accf), "d"(accd));  // results complete before the clock read
+    const long long t1 = clock64();
+    if (accd + accf == 12345.0) sink[threadIdx.x] = (float)accd;
+    if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
+extern "C" __attribute__((visibility("default"))) int ems_epi_micro(int poly, int dbl, int blocks, int iters,
+                                                                   long long* cyc, float* sink) {
+    auto k = poly == 0 ? (dbl ? epi_micro_kernel<0, 1> : epi_micro_kernel<0, 0>)
+           : poly == 2 ? (dbl ? epi_micro_kernel<2, 1> : epi_micro_kernel<2, 0>)
+           : poly == 3 ? (dbl ? epi_micro_kernel<3, 1> : epi_micro_kernel<3, 0>)
+                       : (dbl ? epi_micro_kernel<4, 1> : epi_micro_kernel<4, 0>);
+    k<<<blocks, 512>>>(iters, 0, cyc, sink);
+    if (cudaGetLastError() != cudaSuccess) return 3;
+    if (cudaDeviceSynchronize() != cudaSuccess) return 4;
+    return 0;
+}
+
 // MMA throughput: one elected thread issues `iters` MMAs (K=16 each) back to back on
 // operands already in smem/TMEM (garbage values; only timing matters).
 // kind 0: SS M128 N128   1: TS M128 N128 (A in TMEM)   2: SS M128 N256   3: SS M128 N128 B MN-major
@@ -225,6 +295,18 @@ __global__ void __launch_bounds__(128, 1) mma_micro_kernel(int kind, int iters, 
                 bd[k] = sdesc(b + (k >> 2) * 32768 + (k & 3) * 32, 16, 1024);
             }
             const uint32_t id2 = idesc_bf16(128, kind == 6 ? 256 : 128, 0, 0);
+            if (kind >= 7) {
+                // 7: SS N128 alternating 2 accumulators per instruction, 8: TS N128 alternating 2,
+                // 9: SS N128 rotating over 4 accumulators (dependent accumulations spaced apart)
+                for (int i = 0; i < iters; i += 8) {
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        if (kind == 7) mma_ss(tm + (k & 1) * 128, ad[k], bd[k], id2, 1);
+                        else if (kind == 8) mma_ts(tm + (k & 1) * 128, tm + 256 + k * 8, bd[k], id2, 1);
+                        else mma_ss(tm + (k & 3) * 128, ad[k], bd[k], id2, 1);
+                    }
+                }
+            } else
             for (int i = 0; i < iters; i += 8) {
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
@@ -401,6 +483,74 @@ extern "C" __attribute__((visibility("default"))) int ems_mma2_micro(int kind, i
     const int smem = 1024 + 65536 + 65536;
     cudaFuncSetAttribute(mma2_micro_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     mma2_micro_kernel<<<2 * pairs, 128, smem>>>(kind, iters, cyc);
+    if (cudaGetLastError() != cudaSuccess) return 3;
+    if (cudaDeviceSynchronize() != cudaSuccess) return 4;
+    return 0;
+}
+
+// MMA issue patterns: 8 consecutive K=16 MMAs (N = n) with per-instruction accumulator
+// column offsets d[k] and (TS) A-operand TMEM column offsets a[k]; ts = 0 for SS.
+struct MmaPat {
+    int ts, n, d[8], a[8], same_b;
+};
+__global__ void __launch_bounds__(128, 1) mma_pat_kernel(MmaPat pt, int iters, long long* cyc) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tmem_base;
+    const int warp = threadIdx.x >> 5;
+    if (warp == 0) tmem_alloc<512>(&tmem_base);
+    if (threadIdx.x == 32) {
+        mbar_init(&bar, 1);
+        fence_barrier_init();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tm = tmem_base;
+    if (threadIdx.x == 0) {
+        const uint32_t a = smem_u32(sm), b = smem_u32(sm + 65536);
+        uint64_t ad[8], bd[8];
+        uint32_t dd[8], at[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            ad[k] = sdesc(a + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024);
+            const int kb = pt.same_b ? (k >> 1) : k;
+            bd[k] = sdesc(b + (kb >> 2) * 32768 + (kb & 3) * 32, 16, 1024);
+            dd[k] = tm + pt.d[k];
+            at[k] = tm + pt.a[k];
+        }
+        const uint32_t id = idesc_bf16(128, pt.n, 0, 0);
+        const long long t0 = clock64();
+        for (int i = 0; i < iters; i += 8) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                if (pt.ts) mma_ts(dd[k], at[k], bd[k], id, 1);
+                else mma_ss(dd[k], ad[k], bd[k], id, 1);
+            }
+        }
+        mma_commit(&bar);
+        mbar_wait(&bar, 0);
+        cyc[blockIdx.x] = clock64() - t0;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc<512>(tm);
+}
+
+extern "C" __attribute__((visibility("default"))) int ems_mma_pat(const int* pat, int blocks, int iters,
+                                                                 long long* cyc) {
+    MmaPat pt;
+    pt.ts = pat[0];
+    pt.n = pat[1];
+    for (int k = 0; k < 8; ++k) {
+        pt.d[k] = pat[2 + k];
+        pt.a[k] = pat[10 + k];
+    }
+    pt.same_b = pat[18];
+    const int smem = 1024 + 65536 + 65536;
+    cudaFuncSetAttribute(mma_pat_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    mma_pat_kernel<<<blocks, 128, smem>>>(pt, iters, cyc);
     if (cudaGetLastError() != cudaSuccess) return 3;
     if (cudaDeviceSynchronize() != cudaSuccess) return 4;
     return 0;

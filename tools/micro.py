@@ -71,10 +71,23 @@ for kind, (name, n) in {0: ("2SM SS 256x128", 128), 1: ("2SM TS 256x128", 128), 
 print(json.dumps(res4, indent=1))
 
 res5 = {}
-for kind, (name, n) in {4: ("SS 128x128 pre-desc", 128), 5: ("TS 128x128 pre-desc", 128), 6: ("SS 128x256 pre-desc", 256)}.items():
+for kind, (name, n) in {4: ("SS 128x128 pre-desc", 128), 5: ("TS 128x128 pre-desc", 128), 6: ("SS 128x256 pre-desc", 256),
+                        7: ("SS 128x128 2 accumulators alternating", 128), 8: ("TS 128x128 2 accumulators alternating", 128),
+                        9: ("SS 128x128 4 accumulators rotating", 128)}.items():
     cyc = torch.zeros(148, dtype=torch.int64, device="cuda")
     it = 4096
     assert L.ems_mma_micro(kind, 148, it, cyc.data_ptr()) == 0
     c = cyc.double().median().item()
     res5[name + " MAC/clk/SM"] = 128 * n * 16 * it / c
 print(json.dumps(res5, indent=1))
+
+L.ems_epi_micro.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p]
+res6 = {}
+for poly in (0, 2, 3, 4):
+    for dbl in (0, 1):
+        cyc = torch.zeros(148, dtype=torch.int64, device="cuda")
+        sink = torch.zeros(1024, device="cuda")
+        it = 2048
+        assert L.ems_epi_micro(poly, dbl, 148, it, cyc.data_ptr(), sink.data_ptr()) == 0
+        res6[f"P2 epilogue poly={poly} double={dbl} elem/clk/SM"] = 512 * 64 * it / cyc.double().median().item()
+print(json.dumps(res6, indent=1))

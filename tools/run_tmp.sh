@@ -1,3 +1,1 @@
-python tools/tune_score.py --reps 5
-python tools/tune_score.py --reps 40
-nvidia-smi --query-gpu=clocks.sm,clocks.max.sm,power.draw,power.limit,temperature.gpu,clocks_event_reasons.active --format=csv
+python tools/tune_score.py --reps 10 --var EMS_LIB_PATH=_variants/dbg2.so --var EMS_P2_DEBUG=0,2,5,6 --var EMS_P2_POLY=0,2
