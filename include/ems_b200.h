@@ -22,6 +22,8 @@
  *   weighted_merge      compressor.hpp:32-51                    ems_compact (merge epilogue)
  *   compress_prefill    compressor.hpp:58-60                    ems_select+ems_merge+ems_compact
  *   engine prefill (score -> compress)  proj/src/engine.cpp:42-82  ems_prefill_compress
+ *   engine prefill incl. RoPE           proj/src/engine.cpp:42-82  ems_prefill (raw Q/K)
+ *   apply_rope / detail::rotate         proj/src/rope.cpp:10-37    ems_rope
  *
  * Conventions
  *  - A "unit" is one (b, h_kv) with its G = heads_q / heads_kv query heads;
@@ -169,6 +171,22 @@ EMS_API int ems_prefill_compress(const ems_desc* desc, const void* q_rot, const 
                          const void* k_raw, const void* v, void* out_o, float* lse, float* glo,
                          float* loc, const ems_stage* stage, const ems_cache* cache,
                          void* workspace, size_t workspace_bytes, cudaStream_t stream);
+
+/* Rotary position embedding, detail::rotate (proj/src/rope.cpp:10-28) applied per token as
+ * rotate_block does (proj/src/engine.cpp:14-22): x, y [planes][seq_len][head_dim] (dtype),
+ * token l at position first_position + l, pair (2i, 2i+1) rotated by pos * base^(-2i/d) in
+ * fp64 and rounded once to dtype.  x == y (in place) is allowed. */
+EMS_API int ems_rope(int32_t dtype, int32_t planes, int32_t seq_len, int32_t head_dim, double base,
+             int64_t first_position, const void* x, void* y, cudaStream_t stream);
+
+/* engine::prefill (proj/src/engine.cpp:42-82) on RAW inputs: RoPE of q [B][Hq][L][d] and
+ * k [B][Hkv][L][d] (base rope_base, positions first_position + i; rope_base == 0 means no
+ * RoPE) into the caller's q_rot / k_rot scratch (same shapes, may be NULL when rope_base == 0),
+ * then the whole path of ems_prefill_compress with k as the raw (pre-RoPE) keys. */
+EMS_API int ems_prefill(const ems_desc* desc, double rope_base, const void* q, const void* k,
+                const void* v, void* q_rot, void* k_rot, void* out_o, float* lse, float* glo,
+                float* loc, const ems_stage* stage, const ems_cache* cache, void* workspace,
+                size_t workspace_bytes, cudaStream_t stream);
 
 /* Standalone redundancy_cross (analysis.hpp:19-20) for one pair of token groups:
  * k_rows/v_rows [n_rows][d], k_cols/v_cols [n_cols][d] (dtype) -> r [n_rows][n_cols] fp32. */

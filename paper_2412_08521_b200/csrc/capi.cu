@@ -35,6 +35,8 @@ cudaError_t launch_compact(const Dims& dm, int dtype, const void* k, const void*
 cudaError_t launch_keep_all(const Dims& dm, int dtype, const void* k, const void* v,
                             const float* glo, const float* loc, const ems_stage& sg,
                             const ems_cache& c, int64_t first_pos, cudaStream_t s);
+cudaError_t launch_rope(int dtype, int planes, int L, int d, double base, long long first_pos,
+                        const void* x, void* y, cudaStream_t s);
 cudaError_t launch_redundancy_cross(int dtype, int d, const void* kr, const void* vr, int nr,
                                     const void* kc, const void* vc, int nc, int key_only,
                                     float* r, cudaStream_t s);
@@ -393,6 +395,53 @@ int ems_prefill_compress(const ems_desc* d, const void* q_rot, const void* k_rot
         if (int rc = run_merge(d, k_raw, v, sg, ws, s)) return rc;
     }
     return run_compact(d, k_raw, v, g, lc, sg, *c, ws, s);
+}
+
+int ems_rope(int32_t dtype, int32_t planes, int32_t L, int32_t d, double base, int64_t first_pos,
+             const void* x, void* y, cudaStream_t s) {
+    if ((dtype != EMS_F32 && dtype != EMS_BF16) || planes < 0 || L < 0 || d <= 0 || d % 2 != 0 ||
+        d > 512 || !(base > 0.0) || (planes > 0 && L > 0 && (!x || !y))) {
+        set_error("ems_rope: bad arguments (need even head_dim <= 512, base > 0)");  // rope.cpp:11-13
+        return EMS_INVALID_ARGUMENT;
+    }
+    if (first_pos < 0) {
+        set_error("apply_rope: position must be nonnegative");  // rope.cpp:33-35
+        return EMS_INVALID_ARGUMENT;
+    }
+    cudaError_t e = launch_rope(dtype, planes, L, d, base, first_pos, x, y, s);
+    if (e != cudaSuccess) {
+        set_error("rope launch: %s", cudaGetErrorString(e));
+        return EMS_CUDA_ERROR;
+    }
+    return EMS_OK;
+}
+
+int ems_prefill(const ems_desc* d, double rope_base, const void* q, const void* k, const void* v,
+                void* q_rot, void* k_rot, void* out_o, float* lse, float* glo, float* loc,
+                const ems_stage* st, const ems_cache* c, void* ws, size_t ws_bytes, cudaStream_t s) {
+    if (int rc = ems_validate(d)) return rc;
+    if (!(rope_base >= 0.0)) {
+        set_error("ems_prefill: rope_base must be >= 0 (0 = no RoPE)");
+        return EMS_INVALID_ARGUMENT;
+    }
+    const void* qr = q;
+    const void* kr = k;
+    if (rope_base > 0.0) {
+        if (!q_rot || !k_rot || !q || !k) {
+            set_error("ems_prefill: RoPE needs q_rot / k_rot scratch");
+            return EMS_INVALID_ARGUMENT;
+        }
+        const int32_t pq = d->batch * d->heads_q, pk = d->batch * d->heads_kv;
+        if (int rc = ems_rope(d->dtype, pq, d->seq_len, d->head_dim, rope_base, d->first_position, q,
+                              q_rot, s))
+            return rc;
+        if (int rc = ems_rope(d->dtype, pk, d->seq_len, d->head_dim, rope_base, d->first_position, k,
+                              k_rot, s))
+            return rc;
+        qr = q_rot;
+        kr = k_rot;
+    }
+    return ems_prefill_compress(d, qr, kr, k, v, out_o, lse, glo, loc, st, c, ws, ws_bytes, s);
 }
 
 int ems_redundancy_cross(int32_t dtype, int32_t d, const void* k_rows, const void* v_rows,

@@ -103,6 +103,10 @@ def lib() -> C.CDLL:
         L.ems_redundancy_cross.argtypes = [C.c_int32, C.c_int32, vp, vp, C.c_int32, vp, vp,
                                            C.c_int32, C.c_int32, fp, vp]
         L.ems_sync_status.argtypes = [C.POINTER(Desc), vp, vp]
+        L.ems_rope.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_double, C.c_int64, vp, vp,
+                               vp]
+        L.ems_prefill.argtypes = [C.POINTER(Desc), C.c_double, vp, vp, vp, vp, vp, vp, fp, fp, fp,
+                                  C.POINTER(CStage), C.POINTER(CCache), vp, C.c_size_t, vp]
         _lib = L
     return _lib
 
@@ -223,6 +227,23 @@ class Plan:
                                           _p(self.workspace), self.workspace.numel(),
                                           _stream(stream)))
 
+    def run_raw(self, q, k, v, rope_base: float, stream=None) -> None:
+        """engine::prefill on RAW Q/K (ems_prefill): RoPE on the device into the plan's
+        q_rot/k_rot scratch, then the whole path with k as the pre-RoPE keys."""
+        self._check_inputs(q, k, k, v)
+        if rope_base > 0 and getattr(self, "q_rot", None) is None:
+            D = self.desc
+            self.q_rot = torch.empty((D.batch, D.heads_q, D.seq_len, D.head_dim), dtype=self.dtype,
+                                     device=self.device)
+            self.k_rot = torch.empty((D.batch, D.heads_kv, D.seq_len, D.head_dim), dtype=self.dtype,
+                                     device=self.device)
+        qr = self.q_rot if rope_base > 0 else None
+        kr = self.k_rot if rope_base > 0 else None
+        _check(lib().ems_prefill(C.byref(self.desc), float(rope_base), _p(q), _p(k), _p(v), _p(qr), _p(kr),
+                                 _p(self.out), _p(self.lse), _p(self.glo), _p(self.loc),
+                                 C.byref(self._cstage), C.byref(self._ccache), _p(self.workspace),
+                                 self.workspace.numel(), _stream(stream)))
+
     def score(self, q_rot, k_rot, v=None, stream=None) -> None:
         self._check_inputs(q_rot, k_rot, None, v)
         _check(lib().ems_score(C.byref(self.desc), _p(q_rot), _p(k_rot), _p(v),
@@ -276,6 +297,31 @@ def prefill_compress(q_rot, k_rot, k_raw, v, cfg: EmsConfig, want_out=True, scor
     plan = Plan(B, Hq, Hkv, L, d, q_rot.dtype, cfg, q_rot.device, score_impl, want_out,
                 first_position=first_position)
     plan.run(q_rot, k_rot, k_raw, v)
+    plan.sync_status()
+    return plan
+
+
+def rope(x: torch.Tensor, base: float, first_position: int = 0, out: torch.Tensor | None = None) -> torch.Tensor:
+    """apply_rope (proj/src/rope.cpp:10-37) over the token axis of [..., L, d] on the device:
+    fp64 rotation, rounded once to the tensor's dtype."""
+    if not x.is_contiguous():
+        raise InvalidArgument("rope: x must be contiguous")
+    L, d = x.shape[-2], x.shape[-1]
+    planes = x.numel() // max(L * d, 1)
+    y = torch.empty_like(x) if out is None else out
+    _check(lib().ems_rope(_dtype_code(x.dtype), planes, L, d, float(base), int(first_position), _p(x), _p(y),
+                          _stream()))
+    return y
+
+
+def prefill(q, k, v, cfg: EmsConfig, rope_base: float, want_out=True, score_impl="auto",
+            first_position=0) -> Plan:
+    """engine::prefill (proj/src/engine.cpp:42-82) on RAW [B][H][L][d] tensors: RoPE
+    (rope_base, 0 = none), score, compress.  Returns the Plan (O, glo/loc, cache)."""
+    B, Hq, L, d = q.shape
+    plan = Plan(B, Hq, k.shape[1], L, d, q.dtype, cfg, q.device, score_impl, want_out,
+                first_position=first_position)
+    plan.run_raw(q, k, v, rope_base)
     plan.sync_status()
     return plan
 
