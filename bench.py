@@ -119,6 +119,23 @@ class ClockSampler:
                 "power_w_max": max(self.power) if self.power else None}
 
 
+def unrope(x, base: float):
+    """Inverse interleaved-pair RoPE (detail::rotate at -position, proj/src/rope.cpp:10-28), so
+    the e2e arm can feed raw Q the way engine::prefill receives it."""
+    import torch
+    L, d = x.shape[-2], x.shape[-1]
+    pos = -torch.arange(L, device=x.device, dtype=torch.float64)[:, None]
+    freq = torch.pow(torch.tensor(base, dtype=torch.float64, device=x.device),
+                     -torch.arange(0, d, 2, device=x.device, dtype=torch.float64) / d)[None, :]
+    c, s = torch.cos(pos * freq), torch.sin(pos * freq)
+    out = torch.empty_like(x)
+    for p in range(x.shape[1]):  # plane by plane (fp64 temporaries stay small)
+        a0, a1 = x[:, p, :, 0::2].double(), x[:, p, :, 1::2].double()
+        out[:, p, :, 0::2] = (a0 * c - a1 * s).to(x.dtype)
+        out[:, p, :, 1::2] = (a0 * s + a1 * c).to(x.dtype)
+    return out
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -214,6 +231,7 @@ def main():
                     help="CPU work budget per reference sample (ours arm uses 2.5x for cpu_baseline)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-chunks", type=int, default=4, help="unit groups of the host copy/compute pipeline")
     args = ap.parse_args()
 
     from paper_2412_08521_b200.inputs import CONFIGS
@@ -289,21 +307,21 @@ def main():
     tokens_step = B * L * ws
     value = tokens_step / (ms_step / 1e3)
 
-    # e2e through the public API from pinned host memory
+    # e2e through the public API the reference's callers use: engine::prefill on RAW host
+    # matrices (ems_prefill_host): pinned host Q/K/V in, RoPE on the device, compressed cache
+    # back to pinned host memory; copies pipelined with compute in --e2e-chunks unit groups.
     e2e = None
     if not args.no_e2e:
-        hq, hkr, hkw, hv = (x.cpu().pin_memory() for x in (q, kr, kw, v))
-        dq, dkr, dkw, dv = (torch.empty_like(x) for x in (q, kr, kw, v))
-        host_cache = {k: torch.empty(t_.shape, dtype=t_.dtype, pin_memory=True) for k, t_ in plan.cache.items()}
-        h2d = sum(x.numel() * x.element_size() for x in (hq, hkr, hkw, hv))
+        base = w.rope_base or 0.0
+        q_raw = unrope(q, base) if base else q
+        hq, hk, hv = (x.cpu().pin_memory() for x in (q_raw, kw, v))
+        del q_raw
+        host_cache = plan.host_cache()
+        h2d = sum(x.numel() * x.element_size() for x in (hq, hk, hv))
         d2h = sum(x.numel() * x.element_size() for x in host_cache.values())
 
         def e2e_step():
-            for dst, src in ((dq, hq), (dkr, hkr), (dkw, hkw), (dv, hv)):
-                dst.copy_(src, non_blocking=True)
-            plan.run(dq, dkr, dkw, dv)
-            for k_, dst in host_cache.items():
-                dst.copy_(plan.cache[k_], non_blocking=True)
+            plan.run_host(hq, hk, hv, base, h_k_raw=None if base else hk, chunks=args.e2e_chunks)
 
         for _ in range(2):
             e2e_step()
@@ -319,7 +337,8 @@ def main():
         if ws > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": tokens_step / (te.item() / 1e3), "unit": "tokens/s",
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": te.item()}
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": te.item(),
+               "api": f"ems.Plan.run_host (ems_prefill_host, raw Q/K + device RoPE, {args.e2e_chunks} chunks)"}
 
     pk = peaks()
     flops = f_alg(w)

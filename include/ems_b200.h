@@ -23,6 +23,7 @@
  *   compress_prefill    compressor.hpp:58-60                    ems_select+ems_merge+ems_compact
  *   engine prefill (score -> compress)  proj/src/engine.cpp:42-82  ems_prefill_compress
  *   engine prefill incl. RoPE           proj/src/engine.cpp:42-82  ems_prefill (raw Q/K)
+ *   engine prefill from host matrices   proj/src/engine.cpp:42-82  ems_prefill_host
  *   apply_rope / detail::rotate         proj/src/rope.cpp:10-37    ems_rope
  *
  * Conventions
@@ -187,6 +188,23 @@ EMS_API int ems_prefill(const ems_desc* desc, double rope_base, const void* q, c
                 const void* v, void* q_rot, void* k_rot, void* out_o, float* lse, float* glo,
                 float* loc, const ems_stage* stage, const ems_cache* cache, void* workspace,
                 size_t workspace_bytes, cudaStream_t stream);
+
+/* engine::prefill from HOST memory -- the reference's own calling convention (per-head host
+ * matrices, proj/src/engine.cpp:42-82), batched.  h_* are pinned host [B][H][L][d] tensors;
+ * d_* are the caller's device staging buffers of the same shapes.  The units are split into
+ * `chunks` contiguous groups: the host-to-device copy of group c+1 (on copy_stream, or a
+ * library-owned per-thread stream when NULL) overlaps the compute of group c (on stream), and
+ * each group's compressed cache is copied to h_cache (pinned host SoA with the device
+ * cache's shapes; may be NULL) as soon as it is done.  rope_base > 0: h_q/h_k are raw and
+ * RoPE runs on the device into d_q_rot/d_k_rot (h_k_raw/d_k_raw unused); rope_base == 0:
+ * h_q/h_k are pre-rotated and h_k_raw/d_k_raw carry the raw keys.  Asynchronous: on return
+ * `stream` is ordered after every copy, so synchronising it completes the call. */
+EMS_API int ems_prefill_host(const ems_desc* desc, double rope_base, const void* h_q, const void* h_k,
+                     const void* h_k_raw, const void* h_v, void* d_q, void* d_k, void* d_k_raw,
+                     void* d_v, void* d_q_rot, void* d_k_rot, void* out_o, float* lse, float* glo,
+                     float* loc, const ems_cache* d_cache, const ems_cache* h_cache, int32_t chunks,
+                     void* workspace, size_t workspace_bytes, cudaStream_t stream,
+                     cudaStream_t copy_stream);
 
 /* Standalone redundancy_cross (analysis.hpp:19-20) for one pair of token groups:
  * k_rows/v_rows [n_rows][d], k_cols/v_cols [n_cols][d] (dtype) -> r [n_rows][n_cols] fp32. */

@@ -4,6 +4,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <vector>
 
 #include "common.cuh"
 
@@ -126,8 +127,25 @@ ems_stage default_stage(const ems_desc& d, void* ws) {
     return s;
 }
 
+// The whole problem, and any contiguous group of its units as the chunked host pipeline runs
+// them (ems_prefill_host): a group's score workspace can exceed its share of the whole one
+// (colsum head-split partials), so the requirement is the maximum over group sizes.
+size_t workspace_need(const ems_desc& d) {
+    size_t need = layout(d).total;
+    const int G = d.heads_q / d.heads_kv, U = d.batch * d.heads_kv;
+    for (int n = 1; n < U; ++n) {
+        ems_desc sub = d;
+        sub.batch = 1;
+        sub.heads_kv = n;
+        sub.heads_q = n * G;
+        const size_t t = layout(sub).total;
+        if (t > need) need = t;
+    }
+    return need;
+}
+
 int check_ws(const ems_desc* d, void* ws, size_t bytes) {
-    const size_t need = layout(*d).total;
+    const size_t need = workspace_need(*d);
     if (ws == nullptr || bytes < need) {
         set_error("workspace too small: need %zu bytes, got %zu", need, bytes);
         return EMS_INVALID_ARGUMENT;
@@ -177,8 +195,9 @@ int run_score(const ems_desc* desc, const void* q, const void* k, const void* v,
 }
 
 int run_select(const ems_desc* desc, const float* glo, const float* loc, const ems_stage& sg,
-               void* ws, cudaStream_t s) {
-    const Dims m = make_dims(*desc);
+               void* ws, cudaStream_t s, int unit_base = 0) {
+    Dims m = make_dims(*desc);
+    m.unit_base = unit_base;
     const int n_cand = m.L - desc->l_win;
     const int n_imp = m.cap_c < n_cand ? m.cap_c : n_cand;                     // :64
     const int n_tbm = m.cap_tbm < n_cand - n_imp ? m.cap_tbm : n_cand - n_imp;  // :65
@@ -325,7 +344,7 @@ int ems_cache_dims_for(const ems_desc* d, ems_cache_dims* out) {
 
 size_t ems_workspace_bytes(const ems_desc* d) {
     if (ems_validate(d) != EMS_OK) return 0;
-    return layout(*d).total;
+    return workspace_need(*d);
 }
 
 int ems_score(const ems_desc* d, const void* q, const void* k, const void* v, void* out_o,
@@ -374,6 +393,31 @@ int ems_compact(const ems_desc* d, const void* k_raw, const void* v, const float
     return run_compact(d, k_raw, v, glo, loc, sg, *c, ws, s);
 }
 
+}  // extern "C"
+
+namespace ems {
+namespace {
+// The whole path on one descriptor, without resetting the status word (shared by the
+// public entry points and the chunked host pipeline).
+int run_path(const ems_desc* d, const void* q_rot, const void* k_rot, const void* k_raw,
+             const void* v, void* out_o, float* lse, float* glo, float* loc, const ems_stage* st,
+             const ems_cache& c, void* ws, cudaStream_t s, int unit_base = 0) {
+    const Layout l = layout(*d);
+    float* g = glo ? glo : at<float>(ws, l.glo);
+    float* lc = loc ? loc : at<float>(ws, l.loc);
+    const ems_stage sg = st ? *st : default_stage(*d, ws);
+    if (int rc = run_score(d, q_rot, k_rot, v, out_o, lse, g, lc, ws, s)) return rc;
+    if (d->seq_len > d->n_budget) {  // policies.cpp:136-138: keep-all when n <= n_budget
+        if (int rc = run_select(d, g, lc, sg, ws, s, unit_base)) return rc;
+        if (int rc = run_merge(d, k_raw, v, sg, ws, s)) return rc;
+    }
+    return run_compact(d, k_raw, v, g, lc, sg, c, ws, s);
+}
+}  // namespace
+}  // namespace ems
+
+extern "C" {
+
 int ems_prefill_compress(const ems_desc* d, const void* q_rot, const void* k_rot,
                          const void* k_raw, const void* v, void* out_o, float* lse, float* glo,
                          float* loc, const ems_stage* st, const ems_cache* c, void* ws,
@@ -384,17 +428,8 @@ int ems_prefill_compress(const ems_desc* d, const void* q_rot, const void* k_rot
         set_error("ems_prefill_compress: null tensor");
         return EMS_INVALID_ARGUMENT;
     }
-    const Layout l = layout(*d);
     EMS_CUDA_CHECK(cudaMemsetAsync(ws, 0, sizeof(DevStatus), s));
-    float* g = glo ? glo : at<float>(ws, l.glo);
-    float* lc = loc ? loc : at<float>(ws, l.loc);
-    const ems_stage sg = st ? *st : default_stage(*d, ws);
-    if (int rc = run_score(d, q_rot, k_rot, v, out_o, lse, g, lc, ws, s)) return rc;
-    if (d->seq_len > d->n_budget) {  // policies.cpp:136-138: keep-all when n <= n_budget
-        if (int rc = run_select(d, g, lc, sg, ws, s)) return rc;
-        if (int rc = run_merge(d, k_raw, v, sg, ws, s)) return rc;
-    }
-    return run_compact(d, k_raw, v, g, lc, sg, *c, ws, s);
+    return run_path(d, q_rot, k_rot, k_raw, v, out_o, lse, glo, loc, st, *c, ws, s);
 }
 
 int ems_rope(int32_t dtype, int32_t planes, int32_t L, int32_t d, double base, int64_t first_pos,
@@ -474,3 +509,154 @@ int ems_sync_status(const ems_desc* d, void* ws, cudaStream_t s) {
 }
 
 }  // extern "C"
+
+// ----------------------------------------------------------------------------------------
+// Host-resident inputs: the chunked copy/compute pipeline (ems_prefill_host).
+namespace ems {
+namespace {
+
+// Per-(host thread, device) pool of timing-free events and a non-blocking copy stream.
+struct HostPipeRes {
+    int device = -1;
+    cudaStream_t copy = nullptr;
+    std::vector<cudaEvent_t> ev;
+};
+thread_local HostPipeRes g_pipe[8];
+
+HostPipeRes* pipe_res(int nev) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 8) return nullptr;
+    HostPipeRes& r = g_pipe[dev];
+    if (r.copy == nullptr && cudaStreamCreateWithFlags(&r.copy, cudaStreamNonBlocking) != cudaSuccess)
+        return nullptr;
+    while ((int)r.ev.size() < nev) {
+        cudaEvent_t e;
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+        r.ev.push_back(e);
+    }
+    r.device = dev;
+    return &r;
+}
+
+template <class T>
+T* off(T* p, size_t bytes) {
+    return p ? reinterpret_cast<T*>(reinterpret_cast<char*>(p) + bytes) : nullptr;
+}
+template <class T>
+const T* off(const T* p, size_t bytes) {
+    return p ? reinterpret_cast<const T*>(reinterpret_cast<const char*>(p) + bytes) : nullptr;
+}
+
+// Cache arrays of units [u0, u0 + n): byte offset and size per unit of each SoA field.
+struct CacheField {
+    void* ems_cache::*ptr;
+    size_t per_unit;
+};
+
+}  // namespace
+}  // namespace ems
+
+extern "C" int ems_prefill_host(const ems_desc* d, double rope_base, const void* h_q, const void* h_k,
+                                const void* h_k_raw, const void* h_v, void* d_q, void* d_k, void* d_k_raw,
+                                void* d_v, void* d_q_rot, void* d_k_rot, void* out_o, float* lse,
+                                float* glo, float* loc, const ems_cache* d_cache, const ems_cache* h_cache,
+                                int32_t chunks, void* ws, size_t ws_bytes, cudaStream_t s,
+                                cudaStream_t copy_stream) {
+    using namespace ems;
+    if (int rc = ems_validate(d)) return rc;
+    if (int rc = check_ws(d, ws, ws_bytes)) return rc;
+    const bool rope = rope_base > 0.0;
+    if (!(rope_base >= 0.0) || !h_q || !h_k || !h_v || !d_q || !d_k || !d_v || !d_cache ||
+        (rope && (!d_q_rot || !d_k_rot)) || (!rope && (!h_k_raw || !d_k_raw))) {
+        set_error("ems_prefill_host: missing buffer (RoPE needs q_rot/k_rot scratch; pre-rotated "
+                  "inputs need k_raw)");
+        return EMS_INVALID_ARGUMENT;
+    }
+    const Dims m = make_dims(*d);
+    const int U = m.units, G = m.G;
+    int nc = chunks < 1 ? 1 : (chunks > U ? U : chunks);
+    HostPipeRes* res = pipe_res(2 * nc + 2);
+    if (!res) {
+        set_error("ems_prefill_host: could not create copy stream / events");
+        return EMS_CUDA_ERROR;
+    }
+    cudaStream_t cs = copy_stream ? copy_stream : res->copy;
+    cudaEvent_t* ev = res->ev.data();  // [0, nc): inputs of chunk c staged; [nc, 2nc): chunk c done
+    const size_t row = (size_t)m.L * m.d * m.esize;  // one [L][d] plane
+    const size_t cache_d = (size_t)m.d * m.esize;
+    const CacheField fields[] = {
+        {(void* ems_cache::*)&ems_cache::center_key, (size_t)m.cap_c * cache_d},
+        {(void* ems_cache::*)&ems_cache::center_norm, (size_t)m.cap_c * 4},
+        {(void* ems_cache::*)&ems_cache::center_value, (size_t)m.cap_c * cache_d},
+        {(void* ems_cache::*)&ems_cache::center_pos, (size_t)m.cap_c * 4},
+        {(void* ems_cache::*)&ems_cache::center_score, (size_t)m.cap_c * 12},
+        {(void* ems_cache::*)&ems_cache::local_key, (size_t)m.cap_l * cache_d},
+        {(void* ems_cache::*)&ems_cache::local_value, (size_t)m.cap_l * cache_d},
+        {(void* ems_cache::*)&ems_cache::local_pos, (size_t)m.cap_l * 4},
+        {(void* ems_cache::*)&ems_cache::local_score, (size_t)m.cap_l * 12},
+        {(void* ems_cache::*)&ems_cache::lut_pos, (size_t)(m.cap_lut > 0 ? m.cap_lut : 1) * 4},
+        {(void* ems_cache::*)&ems_cache::lut_slot, (size_t)(m.cap_lut > 0 ? m.cap_lut : 1) * 4},
+        {(void* ems_cache::*)&ems_cache::counts, 16},
+    };
+    EMS_CUDA_CHECK(cudaMemsetAsync(ws, 0, sizeof(DevStatus), s));
+    // the copy stream must not overwrite device inputs that earlier work on `s` still reads
+    EMS_CUDA_CHECK(cudaEventRecord(ev[2 * nc], s));
+    EMS_CUDA_CHECK(cudaStreamWaitEvent(cs, ev[2 * nc], 0));
+    auto unit_range = [&](int c, int& u0, int& n) {
+        u0 = (int)((long long)U * c / nc);
+        n = (int)((long long)U * (c + 1) / nc) - u0;
+    };
+    // (1) H2D of every chunk, in chunk order (score inputs first, the raw K of a pre-rotated
+    //     problem last since only the merge/compact stages read it)
+    for (int c = 0; c < nc; ++c) {
+        int u0, n;
+        unit_range(c, u0, n);
+        const size_t oq = (size_t)u0 * G * row, nq = (size_t)n * G * row;
+        const size_t ok = (size_t)u0 * row, nk = (size_t)n * row;
+        EMS_CUDA_CHECK(cudaMemcpyAsync(off(d_q, oq), off(h_q, oq), nq, cudaMemcpyHostToDevice, cs));
+        EMS_CUDA_CHECK(cudaMemcpyAsync(off(d_k, ok), off(h_k, ok), nk, cudaMemcpyHostToDevice, cs));
+        EMS_CUDA_CHECK(cudaMemcpyAsync(off(d_v, ok), off(h_v, ok), nk, cudaMemcpyHostToDevice, cs));
+        if (!rope)
+            EMS_CUDA_CHECK(cudaMemcpyAsync(off(d_k_raw, ok), off(h_k_raw, ok), nk, cudaMemcpyHostToDevice, cs));
+        EMS_CUDA_CHECK(cudaEventRecord(ev[c], cs));
+    }
+    // (2) compute chunk c once its inputs landed; (3) copy its cache back as soon as it is done
+    for (int c = 0; c < nc; ++c) {
+        int u0, n;
+        unit_range(c, u0, n);
+        ems_desc sub = *d;
+        sub.batch = 1;
+        sub.heads_kv = n;
+        sub.heads_q = n * G;
+        const size_t oq = (size_t)u0 * G * row, ok = (size_t)u0 * row;
+        EMS_CUDA_CHECK(cudaStreamWaitEvent(s, ev[c], 0));
+        const void* qr = off(d_q, oq);
+        const void* kr = off(d_k, ok);
+        const void* kraw = rope ? kr : off(d_k_raw, ok);
+        if (rope) {
+            EMS_CUDA_CHECK(launch_rope(d->dtype, n * G, m.L, m.d, rope_base, d->first_position, qr,
+                                       off(d_q_rot, oq), s));
+            EMS_CUDA_CHECK(launch_rope(d->dtype, n, m.L, m.d, rope_base, d->first_position, kr,
+                                       off(d_k_rot, ok), s));
+            qr = off(d_q_rot, oq);
+            kr = off(d_k_rot, ok);
+        }
+        ems_cache sc = *d_cache;
+        for (const CacheField& f : fields) sc.*f.ptr = off(d_cache->*f.ptr, (size_t)u0 * f.per_unit);
+        const size_t ol = (size_t)u0 * m.L;
+        if (int rc = run_path(&sub, qr, kr, kraw, off(d_v, ok), off(out_o, oq), off(lse, (size_t)u0 * G * m.L * 4),
+                              off(glo, ol * 4), off(loc, ol * 4), nullptr, sc, ws, s, u0))
+            return rc;
+        EMS_CUDA_CHECK(cudaEventRecord(ev[nc + c], s));
+        if (h_cache) {
+            EMS_CUDA_CHECK(cudaStreamWaitEvent(cs, ev[nc + c], 0));
+            for (const CacheField& f : fields)
+                EMS_CUDA_CHECK(cudaMemcpyAsync(off(h_cache->*f.ptr, (size_t)u0 * f.per_unit), sc.*f.ptr,
+                                               (size_t)n * f.per_unit, cudaMemcpyDeviceToHost, cs));
+        }
+    }
+    // the caller synchronises `s`: make it cover the last cache copy
+    EMS_CUDA_CHECK(cudaEventRecord(ev[2 * nc + 1], cs));
+    EMS_CUDA_CHECK(cudaStreamWaitEvent(s, ev[2 * nc + 1], 0));
+    return EMS_OK;
+}

@@ -112,13 +112,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     __shared__ Bars bars;
 
     const int tid = threadIdx.x, warp = tid >> 5;
-    const int jp = blockIdx.x / a.units;               // key-tile pair, heaviest first
+    const int per_jp = a.units * a.hsplit;
+    const int jp = blockIdx.x / per_jp;                // key-tile pair, heaviest first
     const int unit = blockIdx.x % a.units;
+    const int hg = (blockIdx.x % per_jp) / a.units;    // head group (hsplit > 1)
+    const int gh = a.G / a.hsplit;                     // query heads of this CTA
     const int b = unit / a.Hkv, hk = unit % a.Hkv;
     const int J0 = 2 * jp;
     const bool has1 = J0 + 1 < a.nT;
     const int span = a.nT - J0;
-    const int n_items = a.G * span;                    // item i -> head i / span, tile J0 + i % span
+    const int n_items = gh * span;                     // item i -> head hg*gh + i / span, tile J0 + i % span
 
     if (warp == 0) {
         tmem_alloc<512>(&bars.tmem_base);
@@ -153,7 +156,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tma_load_3d(sk + kTileBytes + 16384, &tk, &bars.k_full, 64, (J0 + 1) * kTile, unit);
             }
             for (int i = 0; i < n_items; ++i) {
-                const int h = i / span, I = J0 + i % span;
+                const int h = hg * gh + i / span, I = J0 + i % span;
                 const int plane = b * a.Hq + hk * a.G + h;
                 const int s = i % kQStages, bb = i % kBufs;
                 if (i >= kQStages) mbar_wait(&bars.q_empty[s], ((i / kQStages) - 1) & 1);
@@ -239,9 +242,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         asm volatile("bar.sync %0, 256;" ::"r"(1 + w) : "memory");
         if (hc == 0 && active) {
-            const size_t o = (size_t)unit * a.L + (size_t)Jw * kTile + mrow;
-            a.glo[o] = (float)((acc_g + sp[mrow]) / a.G);
-            a.loc[o] = (float)((acc_l + sp[128 + mrow]) / a.G);
+            if (a.hsplit == 1) {
+                const size_t o = (size_t)unit * a.L + (size_t)Jw * kTile + mrow;
+                a.glo[o] = (float)((acc_g + sp[mrow]) / a.G);
+                a.loc[o] = (float)((acc_l + sp[128 + mrow]) / a.G);
+            } else {
+                const size_t o = ((size_t)unit * a.hsplit + hg) * a.L + (size_t)Jw * kTile + mrow;
+                a.part_g[o] = acc_g + sp[mrow];
+                a.part_l[o] = acc_l + sp[128 + mrow];
+            }
         }
     }
     tc_fence_before();
@@ -257,9 +266,26 @@ cudaError_t launch_t(const ColArgs& a, const CUtensorMap& tk, const CUtensorMap&
                              (int)kSmem);
         attr = true;
     }
-    const dim3 grid(((a.nT + 1) / 2) * a.units);
+    const dim3 grid(((a.nT + 1) / 2) * a.units * a.hsplit);
     colsum_tc_kernel<kPoly><<<grid, kThreads, kSmem, s>>>(tk, tq, a);
     return cudaGetLastError();
+}
+
+// glo/loc = (sum over head groups, in order) / G  -- deterministic
+__global__ void colsum_reduce_kernel(const double* __restrict__ pg, const double* __restrict__ pl,
+                                     float* __restrict__ glo, float* __restrict__ loc, int units, int L,
+                                     int hsplit, int G) {
+    const size_t n = (size_t)units * L;
+    for (size_t x = blockIdx.x * (size_t)blockDim.x + threadIdx.x; x < n; x += (size_t)gridDim.x * blockDim.x) {
+        const size_t u = x / L, l = x % L;
+        double g = 0.0, c = 0.0;
+        for (int h = 0; h < hsplit; ++h) {
+            g += pg[(u * hsplit + h) * L + l];
+            c += pl[(u * hsplit + h) * L + l];
+        }
+        glo[x] = (float)(g / G);
+        loc[x] = (float)(c / G);
+    }
 }
 
 }  // namespace
@@ -271,12 +297,25 @@ cudaError_t launch_colsum_tc(const ColArgs& a, const CUtensorMap& tk, const CUte
         const char* e = getenv("EMS_P2_POLY");
         return e ? atoi(e) : 2;
     }();
+    cudaError_t e;
     switch (poly) {
-        case 0: return launch_t<0>(a, tk, tq, s);
-        case 2: return launch_t<2>(a, tk, tq, s);
-        case 4: return launch_t<4>(a, tk, tq, s);
-        default: return launch_t<3>(a, tk, tq, s);
+        case 0: e = launch_t<0>(a, tk, tq, s); break;
+        case 2: e = launch_t<2>(a, tk, tq, s); break;
+        case 4: e = launch_t<4>(a, tk, tq, s); break;
+        default: e = launch_t<3>(a, tk, tq, s); break;
     }
+    if (e != cudaSuccess || a.hsplit == 1) return e;
+    colsum_reduce_kernel<<<4 * 148, 256, 0, s>>>(a.part_g, a.part_l, a.glo, a.loc, a.units, a.L, a.hsplit, a.G);
+    return cudaGetLastError();
+}
+
+// Head split for load balance: the smallest power-of-two divisor of G that gives at least
+// ~4 CTAs per SM (the heaviest key-tile pair otherwise dominates small unit counts).
+int colsum_hsplit(int G, int nT, int units) {
+    const int pairs = (nT + 1) / 2;
+    int hs = 1;
+    while (hs < G && G % (2 * hs) == 0 && (long long)pairs * units * hs < 4LL * 148) hs *= 2;
+    return hs;
 }
 
 }  // namespace ems

@@ -72,6 +72,7 @@ struct Dims {
     int lwin_scores;   // min(l_win, L)
     int cap_c, cap_l, cap_lut, cap_tbm;
     size_t esize;      // bytes per element of the dtype
+    int unit_base = 0; // absolute index of unit 0 (chunked host pipeline), for status reports
 };
 
 Dims make_dims(const ems_desc& d);

@@ -360,7 +360,14 @@ bool score_tc_supported(const Dims& dm, int dtype) {
     return major == 10 && minor == 0 && encode_fn() != nullptr;
 }
 
-size_t score_tc_workspace(const Dims& dm) { return sizeof(float) * (size_t)dm.B * dm.Hq * dm.L; }
+// workspace: nlse2 [B*Hq][L] fp32, then (head split only) fp64 partials [2][units][hsplit][L]
+static size_t nlse2_bytes(const Dims& dm) {
+    return (sizeof(float) * (size_t)dm.B * dm.Hq * dm.L + 255) / 256 * 256;
+}
+size_t score_tc_workspace(const Dims& dm) {
+    const int hs = colsum_hsplit(dm.G, dm.L / kTile, dm.units);
+    return nlse2_bytes(dm) + (hs > 1 ? 2 * sizeof(double) * (size_t)dm.units * hs * dm.L : 0);
+}
 
 cudaError_t score_tc(const Dims& dm, const void* q, const void* k, const void* v, void* o,
                      float* lse, float* glo, float* loc, void* ws, cudaStream_t s) {
@@ -411,12 +418,17 @@ cudaError_t score_tc(const Dims& dm, const void* q, const void* k, const void* v
         return e ? atoi(e) : 0;
     }();
     ca.debug = p2_debug;
+    ca.hsplit = colsum_hsplit(dm.G, fa.nT, dm.units);
     // P2 variant: 2 = CTA-pair (cta_group::2, M = N = 256) kernel, 1 = single-CTA kernel
     static const int p2 = [] {
         const char* e = getenv("EMS_P2_IMPL");
         return e ? atoi(e) : 1;
     }();
-    if (p2 == 2) return launch_colsum2_tc(ca, tk, tq, s);
+    if (ca.hsplit > 1) {
+        ca.part_g = reinterpret_cast<double*>(static_cast<char*>(ws) + nlse2_bytes(dm));
+        ca.part_l = ca.part_g + (size_t)dm.units * ca.hsplit * dm.L;
+    }
+    if (p2 == 2 && ca.hsplit == 1) return launch_colsum2_tc(ca, tk, tq, s);
     return launch_colsum_tc(ca, tk, tq, s);
 }
 

@@ -34,12 +34,19 @@ struct ColArgs {
     float* glo;            // [units][L]
     float* loc;
     int debug = 0;         // profiling only: 1 = skip the exp epilogue, 2 = skip the MMAs
+    // Head split (load balance when few units): each CTA takes G / hsplit query heads of its
+    // key-tile pair and writes fp64 partial sums part_{g,l}[unit][hsplit][L]; a reduce kernel
+    // sums them in head-group order.  hsplit == 1 writes glo/loc directly.
+    int hsplit = 1;
+    double* part_g = nullptr;
+    double* part_l = nullptr;
 };
 
 }  // namespace sc
 
 cudaError_t launch_colsum_tc(const sc::ColArgs& a, const CUtensorMap& tk, const CUtensorMap& tq,
                              cudaStream_t s);
+int colsum_hsplit(int G, int nT, int units);
 cudaError_t launch_colsum2_tc(const sc::ColArgs& a, const CUtensorMap& tk, const CUtensorMap& tq,
                               cudaStream_t s);
 

@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(
     const float* __restrict__ glo, const float* __restrict__ loc, int L, int l_win, int n_imp,
     int n_tbm, int kernel, float* __restrict__ pooled_all, int8_t* __restrict__ cls_all,
     int32_t* __restrict__ imp_idx_all, int32_t* __restrict__ tbm_idx_all,
-    int32_t* __restrict__ counts_all, int cap_c, int cap_tbm, DevStatus* status) {
+    int32_t* __restrict__ counts_all, int cap_c, int cap_tbm, DevStatus* status, int unit_base) {
     __shared__ double sh[32];
     __shared__ int hist[2][256];
     __shared__ int sel_bin[2], sel_above[2];
@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(
     if (tid == 0) degenerate = !(sg > 0.0);
     __syncthreads();
     if (degenerate) {
-        if (tid == 0) record_status(status, EMS_DEGENERATE_INPUT, u);
+        if (tid == 0) record_status(status, EMS_DEGENERATE_INPUT, unit_base + u);
         return;
     }
     const double align = sl / sg;
@@ -212,7 +212,7 @@ cudaError_t launch_select(const Dims& dm, int l_win, int n_imp, int n_tbm, int k
                           DevStatus* status, cudaStream_t s) {
     select_kernel<<<dm.units, kSelThreads, 0, s>>>(glo, loc, dm.L, l_win, n_imp, n_tbm, kernel,
                                                    sg.pooled, sg.cls, sg.imp_idx, sg.tbm_idx,
-                                                   sg.part_counts, dm.cap_c, dm.cap_tbm, status);
+                                                   sg.part_counts, dm.cap_c, dm.cap_tbm, status, dm.unit_base);
     return cudaGetLastError();
 }
 

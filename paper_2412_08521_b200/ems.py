@@ -103,6 +103,9 @@ def lib() -> C.CDLL:
         L.ems_redundancy_cross.argtypes = [C.c_int32, C.c_int32, vp, vp, C.c_int32, vp, vp,
                                            C.c_int32, C.c_int32, fp, vp]
         L.ems_sync_status.argtypes = [C.POINTER(Desc), vp, vp]
+        L.ems_prefill_host.argtypes = [C.POINTER(Desc), C.c_double, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,
+                                       fp, fp, fp, C.POINTER(CCache), C.POINTER(CCache), C.c_int32, vp,
+                                       C.c_size_t, vp, vp]
         L.ems_rope.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_double, C.c_int64, vp, vp,
                                vp]
         L.ems_prefill.argtypes = [C.POINTER(Desc), C.c_double, vp, vp, vp, vp, vp, vp, fp, fp, fp,
@@ -244,6 +247,50 @@ class Plan:
                                  C.byref(self._cstage), C.byref(self._ccache), _p(self.workspace),
                                  self.workspace.numel(), _stream(stream)))
 
+    def host_cache(self) -> dict:
+        """Pinned host buffers shaped like the device cache (targets of run_host)."""
+        if getattr(self, "_host_cache", None) is None:
+            self._host_cache = {k: torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for k, t in self.cache.items()}
+            self._hcache = CCache(*[_p(self._host_cache[f]) for f, _ in CCache._fields_])
+        return self._host_cache
+
+    def run_host(self, h_q, h_k, h_v, rope_base: float, h_k_raw=None, chunks: int = 4, stream=None) -> dict:
+        """engine::prefill from HOST (pinned) tensors (ems_prefill_host): the library stages the
+        inputs in `chunks` groups of units and overlaps each group's host-to-device copy with
+        the previous group's compute; every group's compressed cache is copied back to the
+        pinned host cache as soon as it is done.  rope_base > 0: raw Q/K, RoPE on the device;
+        rope_base == 0: pre-rotated Q/K plus h_k_raw.  Asynchronous; returns the host cache."""
+        D = self.desc
+        qs = (D.batch, D.heads_q, D.seq_len, D.head_dim)
+        ks = (D.batch, D.heads_kv, D.seq_len, D.head_dim)
+        for name, t, shp in (("q", h_q, qs), ("k", h_k, ks), ("v", h_v, ks), ("k_raw", h_k_raw, ks)):
+            if t is None:
+                continue
+            if tuple(t.shape) != shp or t.dtype != self.dtype or not t.is_contiguous() or t.is_cuda \
+                    or not t.is_pinned():
+                raise InvalidArgument(f"{name}: want contiguous pinned host {shp} {self.dtype}")
+        if getattr(self, "_stage_in", None) is None:
+            mk = lambda shp: torch.empty(shp, dtype=self.dtype, device=self.device)  # noqa: E731
+            self._stage_in = dict(q=mk(qs), k=mk(ks), v=mk(ks))
+        st = self._stage_in
+        if rope_base > 0:
+            if getattr(self, "q_rot", None) is None:
+                self.q_rot = torch.empty(qs, dtype=self.dtype, device=self.device)
+                self.k_rot = torch.empty(ks, dtype=self.dtype, device=self.device)
+            kraw_d = None
+        else:
+            if h_k_raw is None:
+                raise InvalidArgument("pre-rotated inputs (rope_base == 0) need h_k_raw")
+            kraw_d = st.setdefault("k_raw", torch.empty(ks, dtype=self.dtype, device=self.device))
+        hc = self.host_cache()
+        _check(lib().ems_prefill_host(
+            C.byref(self.desc), float(rope_base), _p(h_q), _p(h_k), _p(h_k_raw), _p(h_v), _p(st["q"]), _p(st["k"]),
+            _p(kraw_d), _p(st["v"]), _p(self.q_rot) if rope_base > 0 else None,
+            _p(self.k_rot) if rope_base > 0 else None, _p(self.out), _p(self.lse), _p(self.glo), _p(self.loc),
+            C.byref(self._ccache), C.byref(self._hcache), int(chunks), _p(self.workspace), self.workspace.numel(),
+            _stream(stream), None))
+        return hc
+
     def score(self, q_rot, k_rot, v=None, stream=None) -> None:
         self._check_inputs(q_rot, k_rot, None, v)
         _check(lib().ems_score(C.byref(self.desc), _p(q_rot), _p(k_rot), _p(v),
@@ -322,6 +369,19 @@ def prefill(q, k, v, cfg: EmsConfig, rope_base: float, want_out=True, score_impl
     plan = Plan(B, Hq, k.shape[1], L, d, q.dtype, cfg, q.device, score_impl, want_out,
                 first_position=first_position)
     plan.run_raw(q, k, v, rope_base)
+    plan.sync_status()
+    return plan
+
+
+def prefill_host(q, k, v, cfg: EmsConfig, rope_base: float, chunks: int = 4, want_out=True, score_impl="auto",
+                 first_position=0) -> Plan:
+    """engine::prefill (proj/src/engine.cpp:42-82) on pinned HOST [B][H][L][d] tensors, the
+    reference's own calling convention: copies pipelined with compute (ems_prefill_host).
+    Returns the Plan; plan.host_cache() holds the compressed cache on the host."""
+    B, Hq, L, d = q.shape
+    plan = Plan(B, Hq, k.shape[1], L, d, q.dtype, cfg, "cuda", score_impl, want_out,
+                first_position=first_position)
+    plan.run_host(q, k, v, rope_base, chunks=chunks)
     plan.sync_status()
     return plan
 

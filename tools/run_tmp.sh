@@ -1,1 +1,2 @@
-python tools/tune_score.py --reps 10 --var EMS_LIB_PATH=_variants/dbg2.so --var EMS_P2_DEBUG=0,2,5,6 --var EMS_P2_POLY=0,2
+python -m pytest tests/test_gpu_host_pipeline.py tests/test_gpu_rope.py tests/test_gpu_parity.py tests/test_gpu_score_tc.py -x -q 2>&1 | tail -15
+for c in 1 2 4 8; do python bench.py --steps 5 --warmup 3 --no-cpu-baseline --e2e-chunks $c 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print($c, d['ms_per_step'], d['e2e'])"; done
