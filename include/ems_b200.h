@@ -55,7 +55,7 @@
 extern "C" {
 #endif
 
-#define EMS_B200_ABI_VERSION 1
+#define EMS_B200_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define EMS_API __attribute__((visibility("default")))
@@ -79,7 +79,21 @@ typedef enum { EMS_F32 = 0, EMS_BF16 = 1 } ems_dtype;
  * that keeps the 1e-4 contract; SURVEY.md section 7 "fp32 config 1"). */
 typedef enum { EMS_SCORE_AUTO = 0, EMS_SCORE_SIMT = 1, EMS_SCORE_TCGEN05 = 2 } ems_score_impl;
 
-/* Problem descriptor: shapes + CompressionConfig (proj/include/ems/cache.hpp:20-39). */
+/* Prefill policy (PolicyHandle, proj/include/ems/policies.hpp:12-20; policy_prefill_compress,
+ * proj/src/policies.cpp:131-180).  The baselines reuse the select and compact kernels:
+ * FULL keeps every token (locals capacity becomes seq_len), STREAMING keeps sink_count
+ * sinks plus the most recent tokens, H2O the top-(n_budget - l_win) candidates by glo,
+ * SNAPKV the top ones by mean-pooled loc; none of them merges (no TBM set, LUT = kept
+ * centers self-mapped).  Numbered so that a zero-initialised descriptor means EMS. */
+typedef enum {
+    EMS_POLICY_EMS = 0,
+    EMS_POLICY_FULL = 1,
+    EMS_POLICY_STREAMING = 2,
+    EMS_POLICY_H2O = 3,
+    EMS_POLICY_SNAPKV = 4,
+} ems_policy;
+
+/* Problem descriptor: shapes + CompressionConfig (proj/include/ems/cache.hpp:20-39) + policy. */
 typedef struct {
     int32_t batch;
     int32_t heads_q;
@@ -96,15 +110,17 @@ typedef struct {
     int32_t key_only;        /* 0: R = cos_k*cos_v (reference); 1: key cosine only (D1) */
     int32_t score_impl;      /* ems_score_impl */
     int64_t first_position;  /* logical position of token 0 */
+    int32_t policy;          /* ems_policy (0 = EMS) */
+    int32_t sink_count;      /* PolicyHandle::sink_count (streaming_llm; reference default 4) */
 } ems_desc;
 
 /* Per-unit capacities of the compressed cache (fixed-size SoA). */
 typedef struct {
     int32_t units;
     int32_t centers;   /* n_budget - l_win */
-    int32_t locals;    /* n_budget (keep-all path stores up to n_budget tokens) */
-    int32_t lut;       /* (n_budget - l_win) + floor((gamma - 1) * n_budget) */
-    int32_t tbm;       /* floor((gamma - 1) * n_budget) */
+    int32_t locals;    /* n_budget (keep-all path stores up to n_budget tokens); seq_len for FULL */
+    int32_t lut;       /* centers + tbm */
+    int32_t tbm;       /* floor((gamma - 1) * n_budget) for EMS, 0 for the baselines */
 } ems_cache_dims;
 
 /* The compressed per-unit cache, device SoA (flattened HeadCacheState,

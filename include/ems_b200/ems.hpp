@@ -325,11 +325,14 @@ struct CompressResult {
 
 // compress_prefill on device for one KV head with externally supplied scores.
 inline CompressResult compress_device(const Matrix& k_raw, const Matrix& v_raw, const Vector& glo,
-                                      const Vector& loc, const CompressionConfig& c, int dtype) {
+                                      const Vector& loc, const CompressionConfig& c, int dtype,
+                                      int policy = EMS_POLICY_EMS, std::size_t sink_count = 4) {
     const std::size_t n = k_raw.rows, d = k_raw.cols;
     if (n == 0 || v_raw.rows != n || glo.size() != n || loc.size() != n)
         throw std::invalid_argument("compress_prefill: inconsistent token counts");
     ems_desc desc = make_desc(1, 1, n, d, dtype, c);
+    desc.policy = policy;
+    desc.sink_count = static_cast<int32_t>(sink_count);
     check(ems_validate(&desc));
     ems_cache_dims dims{};
     check(ems_cache_dims_for(&desc, &dims));
@@ -348,7 +351,7 @@ inline CompressResult compress_device(const Matrix& k_raw, const Matrix& v_raw, 
     ems_stage stage{pooled.as<float>(), cls.as<int8_t>(), imp.as<int32_t>(), tbm.as<int32_t>(),
                     pc.as<int32_t>(), dest.as<int32_t>()};
     DevBuf ws(ems_workspace_bytes(&desc));
-    if (n > c.n_budget) {
+    if (n > c.n_budget && policy != EMS_POLICY_FULL) {
         check(ems_select(&desc, dg.as<float>(), dl.as<float>(), &stage, ws.p, ws.n, nullptr));
         check(ems_merge(&desc, dk.p, dv.p, &stage, ws.p, ws.n, nullptr));
     }
@@ -384,7 +387,7 @@ inline CompressResult compress_device(const Matrix& k_raw, const Matrix& v_raw, 
     }
     const auto uph = download_raw<int32_t>(up.p, U), ush = download_raw<int32_t>(us.p, U);
     for (int i = 0; i < counts[2]; ++i) hc.lut.push_back({uph[i], ush[i]});
-    if (n > c.n_budget) {
+    if (n > c.n_budget && policy != EMS_POLICY_FULL) {
         r.pooled = download_raw<float>(pooled.p, n);
         r.cls = download_raw<int8_t>(cls.p, n);
     }
@@ -401,6 +404,39 @@ inline HeadCacheState compress_prefill(const Matrix& k_raw, const Matrix& v_raw,
     for (std::size_t i = 0; i < loc.size(); ++i)
         loc[i] = scores.loc_past[i] + (scores.loc_cur.empty() ? 0.0 : scores.loc_cur[i]);
     return detail::compress_device(k_raw, v_raw, scores.glo, loc, config, dtype).cache;
+}
+
+// policies.hpp: PolicyKind / PolicyHandle (proj/include/ems/policies.hpp:12-20) and
+// policy_prefill_compress (proj/src/policies.cpp:131-180) on the device select/compact kernels.
+enum class PolicyKind { full, streaming_llm, h2o, snapkv, ems };
+struct PolicyHandle {
+    PolicyKind kind = PolicyKind::full;
+    std::size_t sink_count = 4;  // streaming_llm
+    void validate(const CompressionConfig& config) const {  // policies.cpp:111-116
+        if (kind == PolicyKind::streaming_llm && config.n_budget < sink_count + config.l_win)
+            throw std::invalid_argument("streaming_llm: n_budget must cover sinks plus the local window");
+    }
+};
+inline int policy_code(PolicyKind k) {
+    switch (k) {
+        case PolicyKind::full: return EMS_POLICY_FULL;
+        case PolicyKind::streaming_llm: return EMS_POLICY_STREAMING;
+        case PolicyKind::h2o: return EMS_POLICY_H2O;
+        case PolicyKind::snapkv: return EMS_POLICY_SNAPKV;
+        case PolicyKind::ems: return EMS_POLICY_EMS;
+    }
+    return EMS_POLICY_EMS;
+}
+inline HeadCacheState policy_prefill_compress(const PolicyHandle& policy, const Matrix& k_raw,
+                                              const Matrix& v_raw, const ScoreState& scores,
+                                              const CompressionConfig& config, int dtype = EMS_F32) {
+    policy.validate(config);
+    Vector loc(scores.size());
+    for (std::size_t i = 0; i < loc.size(); ++i)
+        loc[i] = scores.loc_past[i] + (scores.loc_cur.empty() ? 0.0 : scores.loc_cur[i]);
+    return detail::compress_device(k_raw, v_raw, scores.glo, loc, config, dtype, policy_code(policy.kind),
+                                   policy.sink_count)
+        .cache;
 }
 
 // partition_tokens on the effective score of a ScoreState (the device select kernel

@@ -434,6 +434,110 @@ done:
     return rc;
 }
 
+/* top_k_by, policies.cpp:77-85: stable sort of [0, n_cand) by score desc, first k, ascending. */
+static int64_t top_k_by(const double* score, int64_t n_cand, int64_t k, int64_t* kept) {
+    int64_t* order = (int64_t*)malloc(sizeof(int64_t) * (size_t)n_cand);
+    for (int64_t i = 0; i < n_cand; ++i) order[i] = i;
+    g_sort_scores = score;
+    qsort(order, (size_t)n_cand, sizeof(int64_t), cmp_desc_stable);
+    const int64_t m = k < n_cand ? k : n_cand;
+    qsort(order, (size_t)m, sizeof(int64_t), cmp_i64);
+    memcpy(kept, order, sizeof(int64_t) * (size_t)m);
+    free(order);
+    return m;
+}
+
+/* policy_prefill_compress, policies.cpp:131-180 */
+int ems_oracle_policy_prefill(int32_t policy, int64_t sink, const double* k_raw, const double* v_raw,
+                              const double* glo, const double* loc_past, const double* loc_cur,
+                              int64_t n, int64_t d, const ems_oracle_config* c, ems_oracle_cache* out,
+                              int8_t* cls) {
+    int rc = ems_oracle_validate(c);
+    if (rc) return rc;
+    if (policy == EMS_ORACLE_POLICY_STREAMING && (sink < 0 || c->n_budget < sink + c->l_win))
+        return EMS_ORACLE_INVALID_ARGUMENT; /* PolicyHandle::validate, policies.cpp:111-116 */
+    if (policy < EMS_ORACLE_POLICY_EMS || policy > EMS_ORACLE_POLICY_SNAPKV || n <= 0)
+        return EMS_ORACLE_INVALID_ARGUMENT;
+    if (policy == EMS_ORACLE_POLICY_EMS)
+        return ems_oracle_compress_prefill(k_raw, v_raw, glo, loc_past, loc_cur, n, d, c, 0, out, NULL,
+                                           cls, NULL);
+    out->head_dim = d;
+    out->n_centers = out->n_locals = out->n_lut = 0;
+#define TRIPLE(dst, idx)                                        \
+    do {                                                        \
+        (dst)[0] = glo[idx];                                    \
+        (dst)[1] = loc_past[idx];                               \
+        (dst)[2] = loc_cur ? loc_cur[idx] : 0.0;                \
+    } while (0)
+    if (policy == EMS_ORACLE_POLICY_FULL || n <= c->n_budget) { /* keep_all, policies.cpp:31-45 */
+        for (int64_t i = 0; i < n; ++i) {
+            memcpy(out->local_key + i * d, k_raw + i * d, sizeof(double) * (size_t)d);
+            memcpy(out->local_value + i * d, v_raw + i * d, sizeof(double) * (size_t)d);
+            out->local_position[i] = i;
+            TRIPLE(out->local_score + 3 * i, i);
+            if (cls) cls[i] = 3;
+        }
+        out->n_locals = n;
+        out->compressed = 0;
+        return EMS_ORACLE_OK;
+    }
+    const int64_t n_cand = n - c->l_win, cap = ems_oracle_center_capacity(c);
+    int64_t* kept = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n_cand + 1));
+    int64_t n_kept = 0;
+    if (policy == EMS_ORACLE_POLICY_STREAMING) { /* policies.cpp:145-159 */
+        for (int64_t i = 0; i < sink && i < n; ++i) kept[n_kept++] = i;
+        const int64_t recent = c->n_budget - sink;
+        for (int64_t i = n - recent; i < n - c->l_win; ++i)
+            if (i >= sink) kept[n_kept++] = i;
+    } else if (policy == EMS_ORACLE_POLICY_H2O) { /* policies.cpp:160-164 */
+        n_kept = top_k_by(glo, n_cand, cap, kept);
+    } else { /* SnapKV, policies.cpp:165-176 */
+        double* lsum = (double*)malloc(sizeof(double) * (size_t)n);
+        double* pooled = (double*)malloc(sizeof(double) * (size_t)n);
+        for (int64_t i = 0; i < n; ++i) lsum[i] = loc_past[i] + (loc_cur ? loc_cur[i] : 0.0);
+        int64_t kernel = c->kernel_size;
+        if (kernel > n) kernel = (n % 2 == 1) ? n : n - 1;
+        rc = ems_oracle_mean_pool(lsum, n, kernel, pooled);
+        if (rc == EMS_ORACLE_OK) n_kept = top_k_by(pooled, n_cand, cap, kept);
+        free(lsum);
+        free(pooled);
+        if (rc) {
+            free(kept);
+            return rc;
+        }
+    }
+    /* keep_selection, policies.cpp:49-75 */
+    if (cls) {
+        memset(cls, 0, (size_t)n_cand);
+        memset(cls + n_cand, 3, (size_t)(n - n_cand));
+    }
+    for (int64_t s = 0; s < n_kept; ++s) {
+        const int64_t idx = kept[s];
+        out->key_norm[s] = normalize_into(k_raw + idx * d, out->unit_key + s * d, d);
+        memcpy(out->value + s * d, v_raw + idx * d, sizeof(double) * (size_t)d);
+        out->position[s] = idx;
+        TRIPLE(out->score + 3 * s, idx);
+        out->lut_position[s] = idx;
+        out->lut_slot[s] = (int32_t)s;
+        if (cls) cls[idx] = 2;
+    }
+    out->n_centers = out->n_lut = n_kept;
+    for (int64_t i = 0; i < c->l_win; ++i) {
+        const int64_t idx = n_cand + i;
+        memcpy(out->local_key + i * d, k_raw + idx * d, sizeof(double) * (size_t)d);
+        memcpy(out->local_value + i * d, v_raw + idx * d, sizeof(double) * (size_t)d);
+        out->local_position[i] = idx;
+        TRIPLE(out->local_score + 3 * i, idx);
+    }
+    out->n_locals = c->l_win;
+    out->compressed = 1;
+    for (int64_t e = 1; e < n_kept; ++e) /* check_integrity, cache.cpp:66-80 */
+        if (out->lut_position[e] <= out->lut_position[e - 1]) rc = EMS_ORACLE_CORRUPTION;
+#undef TRIPLE
+    free(kept);
+    return rc;
+}
+
 /* engine::prefill (engine.cpp:42-82) for one KV unit with GQA contract D2. */
 int ems_oracle_prefill_unit(const double* q_rot, const double* k_rot, const double* k_raw,
                             const double* v, int64_t G, int64_t n, int64_t d,

@@ -120,6 +120,25 @@ int ems_oracle_compress_prefill(const double* k_raw, const double* v_raw, const 
                                 ems_oracle_cache* out, double* pooled, int8_t* cls,
                                 int32_t* dest);
 
+/* Prefill policies (proj/include/ems/policies.hpp:12, numbered like the C ABI's ems_policy). */
+enum {
+    EMS_ORACLE_POLICY_EMS = 0,
+    EMS_ORACLE_POLICY_FULL = 1,
+    EMS_ORACLE_POLICY_STREAMING = 2,
+    EMS_ORACLE_POLICY_H2O = 3,
+    EMS_ORACLE_POLICY_SNAPKV = 4,
+};
+
+/* policy_prefill_compress, proj/src/policies.cpp:131-180 (keep_all :31-45, keep_selection
+ * :49-75, top_k_by :77-85; PolicyHandle::validate :111-116).  The EMS branch is
+ * ems_oracle_compress_prefill.  Baseline caches keep centers self-mapped in the LUT, no
+ * merge.  cls[n] may be NULL (2 kept, 0 dropped candidate, 3 local).  Positions are token
+ * indices (the policies take no first_position). */
+int ems_oracle_policy_prefill(int32_t policy, int64_t sink_count, const double* k_raw,
+                              const double* v_raw, const double* glo, const double* loc_past,
+                              const double* loc_cur, int64_t n, int64_t d, const ems_oracle_config* c,
+                              ems_oracle_cache* out, int8_t* cls);
+
 /* The prefill path of engine::prefill (proj/src/engine.cpp:42-82) for one KV unit
  * of G query heads, with the GQA contract D2 (per-KV-head glo/loc = mean over the
  * G heads).  q_rot [G][n][d], k_rot [n][d] (scoring), k_raw/v [n][d] (merge).

@@ -160,6 +160,10 @@ class Cache:
             extra={"slots": [c["slot"] for c in cs]})
 
 
+# prefill policies, numbered as the C ABI's ems_policy (proj/include/ems/policies.hpp:12)
+POLICY = {"ems": 0, "full": 1, "streaming": 2, "h2o": 3, "snapkv": 4}
+
+
 class Oracle:
     """The C restatement (oracle/ems_oracle.c)."""
 
@@ -186,6 +190,8 @@ class Oracle:
         L.ems_oracle_prefill_unit.argtypes = [_dp, _dp, _dp, _dp, C.c_int64, C.c_int64, C.c_int64,
                                               C.POINTER(_CConfig), _dp, _dp, _dp,
                                               C.POINTER(_CCache), _dp, _i8p, _i32p]
+        L.ems_oracle_policy_prefill.argtypes = [C.c_int32, C.c_int64, _dp, _dp, _dp, _dp, _dp, C.c_int64,
+                                                C.c_int64, C.POINTER(_CConfig), C.POINTER(_CCache), _i8p]
 
     # -- scoring -----------------------------------------------------------------
     def prefill_attention(self, q, k, v=None, l_win=32, want_out=True):
@@ -269,7 +275,7 @@ class Oracle:
     @staticmethod
     def _alloc_cache(n: int, d: int, c: Config):
         cap_c = max(c.center_capacity(), 1)
-        cap_l = max(c.n_budget, c.l_win, 1)
+        cap_l = max(c.n_budget, c.l_win, n, 1)  # the full policy keeps all n tokens as locals
         cap_lut = max(c.lut_capacity(), c.center_capacity() + c.tbm_target(), 1)
         a = dict(unit_key=np.zeros((cap_c, d)), key_norm=np.zeros(cap_c), value=np.zeros((cap_c, d)),
                  position=np.zeros(cap_c, dtype=np.int64), score=np.zeros((cap_c, 3)),
@@ -312,6 +318,21 @@ class Oracle:
                "compress_prefill")
         out = self._finish_cache(cc, a)
         out.extra.update(pooled=pooled, cls=cls, dest=dest)
+        return out
+
+    def policy_prefill(self, policy: int, sink: int, k_raw, v_raw, glo, loc_past, c: Config, loc_cur=None):
+        """policy_prefill_compress (policies.cpp:131-180); policy numbered as POLICY below."""
+        k, v, glo, lp = map(_f64, (k_raw, v_raw, glo, loc_past))
+        lc = np.zeros_like(glo) if loc_cur is None else _f64(loc_cur)
+        n, d = k.shape
+        cc, a = self._alloc_cache(n, d, c)
+        cls = np.zeros(n, dtype=np.int8)
+        cfg = self._cfg(c)
+        _check(self.lib.ems_oracle_policy_prefill(int(policy), int(sink), _ptr(k), _ptr(v), _ptr(glo), _ptr(lp),
+                                                  _ptr(lc), n, d, C.byref(cfg), C.byref(cc), _ptr(cls, _i8p)),
+               "policy_prefill")
+        out = self._finish_cache(cc, a)
+        out.extra.update(cls=cls)
         return out
 
     def prefill_unit(self, q_rot, k_rot, k_raw, v, c: Config, want_out=False):
@@ -359,6 +380,9 @@ class RefLib:
         L.ems_ref_engine_prefill.argtypes = [_dp, _dp, _dp, C.c_int64, C.c_int64, C.c_int64,
                                              C.c_int64, C.c_int64, C.c_double, C.c_double,
                                              C.c_int64, C.c_int32, C.c_double, C.c_int64]
+        L.ems_ref_policy_prefill.argtypes = [C.c_int32, C.c_int64, _dp, _dp, _dp, _dp, C.c_int64, C.c_int64,
+                                             C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_int64,
+                                             C.c_int32]
         L.ems_ref_gen_synthetic.argtypes = [C.c_int32, C.c_uint64, C.c_int64, C.c_int64, C.c_int64,
                                             C.c_int64, C.c_double, C.c_double, _dp, _dp, _dp]
 
@@ -401,6 +425,15 @@ class RefLib:
                                                     c.n_budget, c.l_win, c.tau, c.gamma,
                                                     c.kernel_size, int(c.zero_class)),
                   "compress_prefill")
+        return Cache.from_dump_json(self.lib.ems_ref_last_json().decode())
+
+    def policy_prefill(self, policy: int, sink: int, k_raw, v_raw, glo, loc, c: Config) -> Cache:
+        """policy_prefill_compress (proj/src/policies.cpp:131-180) through the reference."""
+        k, v, glo, loc = map(_f64, (k_raw, v_raw, glo, loc))
+        n, d = k.shape
+        self._chk(self.lib.ems_ref_policy_prefill(int(policy), int(sink), _ptr(k), _ptr(v), _ptr(glo), _ptr(loc), n,
+                                                  d, c.n_budget, c.l_win, c.tau, c.gamma, c.kernel_size,
+                                                  int(c.zero_class)), "policy_prefill")
         return Cache.from_dump_json(self.lib.ems_ref_last_json().decode())
 
     def prefill_unit(self, q_rot, k_rot, k_raw, v, c: Config, dump=True):

@@ -136,6 +136,28 @@ int ems_ref_compress_prefill(const double* k_raw, const double* v_raw, const dou
     });
 }
 
+// policy_prefill_compress (proj/src/policies.cpp:131-180) on one head: the reference's
+// baseline policies.  policy: 0 ems, 1 full, 2 streaming_llm, 3 h2o, 4 snapkv (the C ABI's
+// numbering, not PolicyKind's).
+int ems_ref_policy_prefill(int32_t policy, int64_t sink, const double* k_raw, const double* v_raw,
+                           const double* glo, const double* loc, int64_t n, int64_t d, int64_t n_budget,
+                           int64_t l_win, double tau, double gamma, int64_t kernel, int32_t zero_class) {
+    return guarded([&] {
+        static const ems::PolicyKind kinds[] = {ems::PolicyKind::ems, ems::PolicyKind::full,
+                                                ems::PolicyKind::streaming_llm, ems::PolicyKind::h2o,
+                                                ems::PolicyKind::snapkv};
+        if (policy < 0 || policy > 4) throw std::invalid_argument("policy code");
+        ems::PolicyHandle ph{kinds[policy]};
+        ph.sink_count = (std::size_t)sink;
+        const auto cfg = make_config(n_budget, l_win, tau, gamma, kernel, zero_class);
+        const ems::ScoreState s = ems::init_score_state(ems::Vector(glo, glo + n),
+                                                        ems::Vector(loc, loc + n), l_win);
+        const ems::HeadCacheState cache =
+            ems::policy_prefill_compress(ph, to_matrix(k_raw, n, d), to_matrix(v_raw, n, d), s, cfg);
+        g_json = ems::cache_dump_json(cache);
+    });
+}
+
 // The timed composition of the reference arm for one KV
 // unit: per query head prefill_attention in parallel over heads (engine.cpp:65),
 // GQA mean (contract D2), init_score_state, compress_prefill.  q_rot [G][n][d].

@@ -22,7 +22,7 @@ cudaError_t launch_merge_tc(const Dims& dm, const void* k, const void* v, const 
 bool score_tc_supported(const Dims& dm, int dtype);
 cudaError_t launch_select(const Dims& dm, int l_win, int n_imp, int n_tbm, int kernel,
                           const float* glo, const float* loc, const ems_stage& sg,
-                          DevStatus* status, cudaStream_t s);
+                          DevStatus* status, cudaStream_t s, int policy, int sink, int n_budget);
 cudaError_t launch_merge_assign(const Dims& dm, int dtype, const void* k, const void* v,
                                 const ems_stage& sg, double tau, int key_only, float* inv_kc,
                                 float* inv_vc, float* inv_kt, float* inv_vt, cudaStream_t s);
@@ -64,8 +64,9 @@ Dims make_dims(const ems_desc& d) {
     m.units = d.batch * d.heads_kv;
     m.lwin_scores = d.l_win < d.seq_len ? d.l_win : d.seq_len;  // engine.cpp:63
     m.cap_c = d.n_budget - d.l_win;                                // cache.hpp:32
-    m.cap_l = d.n_budget;
-    m.cap_tbm = (int)((d.gamma - 1.0) * (double)d.n_budget);     // cache.hpp:33-35
+    m.cap_l = d.policy == EMS_POLICY_FULL && d.seq_len > d.n_budget ? d.seq_len : d.n_budget;
+    // cache.hpp:33-35; the baseline policies never merge (policies.cpp:49-75)
+    m.cap_tbm = d.policy == EMS_POLICY_EMS ? (int)((d.gamma - 1.0) * (double)d.n_budget) : 0;
     m.cap_lut = m.cap_c + m.cap_tbm;
     m.esize = d.dtype == EMS_F32 ? 4 : 2;
     return m;
@@ -199,10 +200,18 @@ int run_select(const ems_desc* desc, const float* glo, const float* loc, const e
     Dims m = make_dims(*desc);
     m.unit_base = unit_base;
     const int n_cand = m.L - desc->l_win;
-    const int n_imp = m.cap_c < n_cand ? m.cap_c : n_cand;                     // :64
+    int n_imp = m.cap_c < n_cand ? m.cap_c : n_cand;                     // :64
     const int n_tbm = m.cap_tbm < n_cand - n_imp ? m.cap_tbm : n_cand - n_imp;  // :65
+    if (desc->policy == EMS_POLICY_STREAMING) {  // policies.cpp:145-159: sinks + recent window
+        const long long sink = desc->sink_count < m.L ? desc->sink_count : m.L;
+        const long long recent = desc->n_budget - desc->sink_count;
+        long long lo = m.L - recent;
+        if (lo < desc->sink_count) lo = desc->sink_count;
+        n_imp = (int)(sink + (n_cand > lo ? n_cand - lo : 0));
+    }
     cudaError_t e = launch_select(m, desc->l_win, n_imp, n_tbm, kernel_eff(*desc), glo, loc, sg,
-                                  at<DevStatus>(ws, layout(*desc).status), s);
+                                  at<DevStatus>(ws, layout(*desc).status), s, desc->policy,
+                                  desc->sink_count, desc->n_budget);
     if (e != cudaSuccess) {
         set_error("select launch: %s", cudaGetErrorString(e));
         return EMS_CUDA_ERROR;
@@ -242,7 +251,7 @@ int run_compact(const ems_desc* desc, const void* k_raw, const void* v, const fl
     const Dims m = make_dims(*desc);
     const Layout l = layout(*desc);
     cudaError_t e;
-    if (m.L <= desc->n_budget) {
+    if (m.L <= desc->n_budget || desc->policy == EMS_POLICY_FULL) {  // policies.cpp:136-138
         e = launch_keep_all(m, desc->dtype, k_raw, v, glo, loc, sg, c, desc->first_position, s);
     } else {
         ems_stage sg2 = sg;
@@ -324,6 +333,14 @@ int ems_validate(const ems_desc* d) {
         set_error("bad score_impl");
         return EMS_INVALID_ARGUMENT;
     }
+    if (d->policy < EMS_POLICY_EMS || d->policy > EMS_POLICY_SNAPKV) {
+        set_error("bad policy %d", d->policy);
+        return EMS_INVALID_ARGUMENT;
+    }
+    if (d->policy == EMS_POLICY_STREAMING && (d->sink_count < 0 || d->n_budget < d->sink_count + d->l_win)) {
+        set_error("streaming_llm: n_budget must cover sinks plus the local window");  // policies.cpp:113-115
+        return EMS_INVALID_ARGUMENT;
+    }
     if ((long long)d->seq_len + d->first_position > 0x7fffffffLL || d->first_position < 0) {
         set_error("positions must fit int32");
         return EMS_INVALID_ARGUMENT;
@@ -363,8 +380,8 @@ int ems_select(const ems_desc* d, const float* glo, const float* loc, const ems_
                void* ws, size_t ws_bytes, cudaStream_t s) {
     if (int rc = ems_validate(d)) return rc;
     if (int rc = check_ws(d, ws, ws_bytes)) return rc;
-    if (d->seq_len <= d->n_budget) {
-        set_error("ems_select: prompt fits the budget (keep-all path has no partition)");
+    if (d->seq_len <= d->n_budget || d->policy == EMS_POLICY_FULL) {
+        set_error("ems_select: keep-all (prompt fits the budget, or the full policy) has no partition");
         return EMS_INVALID_ARGUMENT;
     }
     EMS_CUDA_CHECK(cudaMemsetAsync(ws, 0, sizeof(DevStatus), s));
@@ -407,7 +424,7 @@ int run_path(const ems_desc* d, const void* q_rot, const void* k_rot, const void
     float* lc = loc ? loc : at<float>(ws, l.loc);
     const ems_stage sg = st ? *st : default_stage(*d, ws);
     if (int rc = run_score(d, q_rot, k_rot, v, out_o, lse, g, lc, ws, s)) return rc;
-    if (d->seq_len > d->n_budget) {  // policies.cpp:136-138: keep-all when n <= n_budget
+    if (d->seq_len > d->n_budget && d->policy != EMS_POLICY_FULL) {  // policies.cpp:136-138
         if (int rc = run_select(d, g, lc, sg, ws, s, unit_base)) return rc;
         if (int rc = run_merge(d, k_raw, v, sg, ws, s)) return rc;
     }

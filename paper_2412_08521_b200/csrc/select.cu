@@ -1,5 +1,7 @@
 // select.cu -- kernel (2): scale alignment + combine + mean-pool + exact top-k
-// partition of the candidate tokens, one CTA per unit.
+// partition of the candidate tokens, one CTA per unit.  The baseline policies
+// (policies.cpp:141-176) replace the ranked score: glo (H2O), mean-pooled loc (SnapKV),
+// or a sinks + recent-window indicator (StreamingLLM); they have no TBM set.
 //
 // Reference semantics (all per head/unit):
 //   effective_score  proj/src/scoring.cpp:146-152 ->
@@ -85,7 +87,8 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(
     const float* __restrict__ glo, const float* __restrict__ loc, int L, int l_win, int n_imp,
     int n_tbm, int kernel, float* __restrict__ pooled_all, int8_t* __restrict__ cls_all,
     int32_t* __restrict__ imp_idx_all, int32_t* __restrict__ tbm_idx_all,
-    int32_t* __restrict__ counts_all, int cap_c, int cap_tbm, DevStatus* status, int unit_base) {
+    int32_t* __restrict__ counts_all, int cap_c, int cap_tbm, DevStatus* status, int unit_base,
+    int policy, int sink, int n_budget) {
     __shared__ double sh[32];
     __shared__ int hist[2][256];
     __shared__ int sel_bin[2], sel_above[2];
@@ -97,6 +100,27 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(
     const float* lo = loc + (size_t)u * L;
     float* pooled = pooled_all + (size_t)u * L;
 
+    const int half = kernel / 2;
+    if (policy != EMS_POLICY_EMS) {
+        // baseline policies (policies.cpp:141-176): the ranked score, no combine / alignment
+        const int n_cand_b = L - l_win;
+        const int lo_recent = max(L - (n_budget - sink), sink);
+        for (int i = tid; i < L; i += kSelThreads) {
+            float v;
+            if (policy == EMS_POLICY_H2O) {
+                v = g[i];  // top_k_by(scores.glo, ...)
+            } else if (policy == EMS_POLICY_SNAPKV) {  // mean_pool_1d(loc_past + loc_cur)
+                const int a = max(0, i - half), bnd = min(L - 1, i + half);
+                double acc = 0.0;
+                for (int jj = a; jj <= bnd; ++jj) acc += (double)lo[jj];
+                v = (float)(acc / (double)(bnd - a + 1));
+            } else {  // streaming_llm: sinks + the recent window, as an indicator score
+                v = (i < sink || (i >= lo_recent && i < n_cand_b)) ? 1.f : 0.f;
+            }
+            pooled[i] = v;
+        }
+        __syncthreads();
+    } else {
     // 1. alignment sums over all L tokens (fp64)
     double sg = 0.0, sl = 0.0;
     for (int i = tid; i < L; i += kSelThreads) sg += (double)g[i], sl += (double)lo[i];
@@ -111,7 +135,6 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(
     const double align = sl / sg;
 
     // 2. combine + centred mean pool with truncated edges (fp64), stored as f32
-    const int half = kernel / 2;
     for (int i = tid; i < L; i += kSelThreads) {
         const int a = max(0, i - half), bnd = min(L - 1, i + half);
         double acc = 0.0;
@@ -122,6 +145,7 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(
         pooled[i] = (float)(acc / (double)(bnd - a + 1));
     }
     __syncthreads();
+    }
 
     // 3. radix select of the k1-th and k2-th largest candidate keys
     const int n_cand = L - l_win;
@@ -209,10 +233,11 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(
 
 cudaError_t launch_select(const Dims& dm, int l_win, int n_imp, int n_tbm, int kernel,
                           const float* glo, const float* loc, const ems_stage& sg,
-                          DevStatus* status, cudaStream_t s) {
+                          DevStatus* status, cudaStream_t s, int policy, int sink, int n_budget) {
     select_kernel<<<dm.units, kSelThreads, 0, s>>>(glo, loc, dm.L, l_win, n_imp, n_tbm, kernel,
                                                    sg.pooled, sg.cls, sg.imp_idx, sg.tbm_idx,
-                                                   sg.part_counts, dm.cap_c, dm.cap_tbm, status, dm.unit_base);
+                                                   sg.part_counts, dm.cap_c, dm.cap_tbm, status, dm.unit_base,
+                                                   policy, sink, n_budget);
     return cudaGetLastError();
 }
 

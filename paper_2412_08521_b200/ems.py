@@ -57,7 +57,11 @@ class Desc(C.Structure):
                 ("seq_len", C.c_int32), ("head_dim", C.c_int32), ("dtype", C.c_int32),
                 ("l_win", C.c_int32), ("n_budget", C.c_int32), ("tau", C.c_double),
                 ("gamma", C.c_double), ("kernel_size", C.c_int32), ("zero_class", C.c_int32),
-                ("key_only", C.c_int32), ("score_impl", C.c_int32), ("first_position", C.c_int64)]
+                ("key_only", C.c_int32), ("score_impl", C.c_int32), ("first_position", C.c_int64),
+                ("policy", C.c_int32), ("sink_count", C.c_int32)]
+
+# ems_policy (include/ems_b200.h; PolicyKind, proj/include/ems/policies.hpp:12)
+POLICY = {"ems": 0, "full": 1, "streaming": 2, "h2o": 3, "snapkv": 4}
 
 
 class CacheDims(C.Structure):
@@ -139,12 +143,14 @@ class EmsConfig:
     kernel_size: int = 7
     zero_class: bool = True
     key_only: bool = False
+    policy: str = "ems"      # PolicyHandle::kind: ems | full | streaming | h2o | snapkv
+    sink_count: int = 4      # PolicyHandle::sink_count (streaming)
 
     def center_capacity(self) -> int:
         return self.n_budget - self.l_win
 
     def tbm_target(self) -> int:
-        return int((self.gamma - 1.0) * float(self.n_budget))
+        return int((self.gamma - 1.0) * float(self.n_budget)) if self.policy == "ems" else 0
 
 
 def _dtype_code(t: torch.dtype) -> int:
@@ -157,9 +163,11 @@ def _dtype_code(t: torch.dtype) -> int:
 
 def make_desc(B: int, Hq: int, Hkv: int, L: int, d: int, dtype: torch.dtype, cfg: EmsConfig,
               score_impl: str = "auto", first_position: int = 0) -> Desc:
+    if cfg.policy not in POLICY:
+        raise InvalidArgument(f"unknown policy: {cfg.policy}")  # policy_kind_from_name, policies.cpp:118-125
     return Desc(B, Hq, Hkv, L, d, _dtype_code(dtype), cfg.l_win, cfg.n_budget, float(cfg.tau),
                 float(cfg.gamma), cfg.kernel_size, int(cfg.zero_class), int(cfg.key_only),
-                SCORE_IMPL[score_impl], first_position)
+                SCORE_IMPL[score_impl], first_position, POLICY[cfg.policy], int(cfg.sink_count))
 
 
 class Plan:

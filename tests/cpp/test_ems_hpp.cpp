@@ -120,6 +120,43 @@ int main() {
     for (std::size_t i = 0; i < rr.size(); ++i) re = std::max(re, std::abs(r.data[i] - rr[i]));
     CHECK(re < 1e-5, "redundancy abs err %g", re);
 
+    // --- baseline policies (policies.cpp:131-180) vs the oracle restatement
+    {
+        const PolicyKind kinds[] = {PolicyKind::full, PolicyKind::streaming_llm, PolicyKind::h2o,
+                                    PolicyKind::snapkv};
+        const int codes[] = {EMS_ORACLE_POLICY_FULL, EMS_ORACLE_POLICY_STREAMING, EMS_ORACLE_POLICY_H2O,
+                             EMS_ORACLE_POLICY_SNAPKV};
+        std::vector<double> lk2(n * d), lv2(n * d), ls2(n * 3);
+        std::vector<int64_t> lpos2(n);
+        for (int pi = 0; pi < 4; ++pi) {
+            PolicyHandle ph{kinds[pi], 4};
+            const HeadCacheState got = policy_prefill_compress(ph, k, v, init_score_state(og, ol, cfg.l_win), cfg);
+            ems_oracle_cache want{(int64_t)d, 0, 0, uk.data(), kn.data(), val.data(), pos.data(), sc.data(), 0,
+                                  lk2.data(), lv2.data(), lpos2.data(), ls2.data(), 0, lutp.data(), luts.data()};
+            ems_oracle_policy_prefill(codes[pi], 4, k.data.data(), v.data.data(), og.data(), ol.data(),
+                                      zeros.data(), n, d, &oc, &want, nullptr);
+            CHECK(got.slots.size() == (std::size_t)want.n_centers && got.locals.size() == (std::size_t)want.n_locals &&
+                      got.lut.size() == (std::size_t)want.n_lut,
+                  "policy %d sizes", pi);
+            int mism = 0;
+            for (std::size_t s = 0; s < std::min(got.slots.size(), (std::size_t)want.n_centers); ++s)
+                mism += got.slots[s]->position != pos[s];
+            for (std::size_t e = 0; e < std::min(got.lut.size(), (std::size_t)want.n_lut); ++e)
+                mism += got.lut[e].position != lutp[e] || got.lut[e].slot != luts[e];
+            CHECK(mism == 0, "policy %d: %d kept/LUT entries differ", pi, mism);
+        }
+        bool threw_p = false;
+        try {
+            CompressionConfig tight = cfg;
+            tight.n_budget = 10;
+            policy_prefill_compress(PolicyHandle{PolicyKind::streaming_llm, 4}, k, v,
+                                    init_score_state(og, ol, tight.l_win), tight);
+        } catch (const std::invalid_argument&) {
+            threw_p = true;
+        }
+        CHECK(threw_p, "streaming_llm with n_budget < sinks + l_win must throw invalid_argument");
+    }
+
     // --- engine-level prefill with GQA (G = 2), bf16 on device
     std::vector<Matrix> qs{q, random_matrix(gen, n, d)}, ks{k}, vs{v};
     const PrefillResult pr = prefill(qs, ks, ks, vs, cfg, EMS_BF16);
