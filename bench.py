@@ -62,33 +62,37 @@ def score_bytes(w) -> float:
 
 
 class ClockSampler:
-    """SM clock + throttle reasons sampled every 5 ms through NVML during the timed region
-    (the recipe's nvidia-smi clocks line, without its 100 ms granularity)."""
+    """SM clock, throttle reasons and power sampled every 5 ms through NVML (the recipe's
+    nvidia-smi clocks line without its 100 ms granularity).  The thread starts before the
+    warm-up so NVML is initialised and sampling when the timed region begins; summary()
+    keeps only the samples taken inside the window marked by begin()/end()."""
 
     REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
                "sw_power_cap": 0x4}
 
     def __init__(self, index: int, period_s: float = 0.005):
         self.index, self.period = index, period_s
-        self.samples, self.reasons, self.max_mhz, self.power = [], set(), None, []
+        self.samples, self.max_mhz = [], None  # (t, mhz, reasons_bits, watts)
+        self.t0 = self.t1 = None
+        self._thread = None
 
     def _run(self):
         import pynvml
         h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
         self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        self._ready.set()
         while not self._stop.is_set():
-            self.samples.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+            t = time.perf_counter()
+            mhz = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
             try:
-                self.power.append(pynvml.nvmlDeviceGetPowerUsage(h) / 1000.0)
+                w = pynvml.nvmlDeviceGetPowerUsage(h) / 1000.0
             except pynvml.NVMLError:
-                pass
+                w = None
             r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
-            for n, bit in self.REASONS.items():
-                if r & bit:
-                    self.reasons.add(n)
+            self.samples.append((t, mhz, r, w))
             time.sleep(self.period)
 
-    def __enter__(self):
+    def start(self):
         import threading
         try:
             import pynvml
@@ -97,26 +101,48 @@ class ClockSampler:
             if idx and idx[0].strip().isdigit():
                 self.index = int(idx[self.index].strip()) if self.index < len(idx) else self.index
         except Exception:  # noqa: BLE001
-            self._thread = None
             return self
-        self._stop = threading.Event()
+        self._stop, self._ready = threading.Event(), threading.Event()
         self._thread = threading.Thread(target=self._run, daemon=True)
         self._thread.start()
+        self._ready.wait(timeout=5.0)
         return self
 
-    def __exit__(self, *a):
-        if getattr(self, "_thread", None) is not None:
+    def _energy_mj(self):
+        try:
+            import pynvml
+            return pynvml.nvmlDeviceGetTotalEnergyConsumption(pynvml.nvmlDeviceGetHandleByIndex(self.index))
+        except Exception:  # noqa: BLE001
+            return None
+
+    def begin(self):
+        self.e0 = self._energy_mj()
+        self.t0 = time.perf_counter()
+
+    def end(self):
+        self.t1 = time.perf_counter()
+        self.e1 = self._energy_mj()
+
+    def energy_j(self):
+        """Board energy over the timed window (NVML counter, J), or None."""
+        e0, e1 = getattr(self, "e0", None), getattr(self, "e1", None)
+        return None if e0 is None or e1 is None else (e1 - e0) / 1e3
+
+    def stop(self):
+        if self._thread is not None:
             self._stop.set()
             self._thread.join(timeout=2)
 
     def summary(self):
         import statistics
-        if not self.samples:
+        win = [s for s in self.samples if self.t0 is not None and self.t0 <= s[0] <= (self.t1 or s[0])]
+        if not win:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
-        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons), "samples": len(self.samples),
-                "sm_mhz_min": min(self.samples),
-                "power_w_max": max(self.power) if self.power else None}
+        reasons = sorted(n for n, bit in self.REASONS.items() if any(s[2] & bit for s in win))
+        watts = [s[3] for s in win if s[3] is not None]
+        return {"sm_mhz": statistics.median(s[1] for s in win), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(win), "sm_mhz_min": min(s[1] for s in win),
+                "power_w_max": max(watts) if watts else None}
 
 
 def unrope(x, base: float):
@@ -277,6 +303,7 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    clk = ClockSampler(local).start()
     for _ in range(args.warmup):
         step()
     plan.sync_status()
@@ -287,15 +314,16 @@ def main():
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        barrier()
-        t_start.record(stream)
-        for i in range(args.steps):
-            starts[i].record(stream)
-            step(mids[i])
-            ends[i].record(stream)
-        t_end.record(stream)
-        barrier()
+    barrier()
+    clk.begin()
+    t_start.record(stream)
+    for i in range(args.steps):
+        starts[i].record(stream)
+        step(mids[i])
+        ends[i].record(stream)
+    t_end.record(stream)
+    barrier()
+    clk.end()
     plan.sync_status()
     total_ms = t_start.elapsed_time(t_end)
     score_ms = sum(starts[i].elapsed_time(mids[i]) for i in range(args.steps)) / args.steps
@@ -365,6 +393,8 @@ def main():
                          "algorithmic_flops_per_launch": flops},
             "gpu_launches": kernels_per_step * args.steps,
             "clocks": clk.summary(),
+            "step_ms": [round(starts[i].elapsed_time(ends[i]), 3) for i in range(args.steps)],
+            "energy_j_per_step": (clk.energy_j() / args.steps) if clk.energy_j() is not None else None,
             "e2e": e2e,
         }
         if not args.no_cpu_baseline and ws == 1:
@@ -375,6 +405,7 @@ def main():
             except Exception as ex:  # noqa: BLE001
                 line["cpu_baseline"] = {"value": None, "error": str(ex)[:200]}
         print(json.dumps(line), flush=True)
+    clk.stop()
     if ws > 1:
         dist.destroy_process_group()
 

@@ -25,6 +25,7 @@
  *   engine prefill incl. RoPE           proj/src/engine.cpp:42-82  ems_prefill (raw Q/K)
  *   engine prefill from host matrices   proj/src/engine.cpp:42-82  ems_prefill_host
  *   apply_rope / detail::rotate         proj/src/rope.cpp:10-37    ems_rope
+ *   decode_step + decode_update         engine.cpp:150-210, compressor.cpp:244-398  ems_decode_step
  *
  * Conventions
  *  - A "unit" is one (b, h_kv) with its G = heads_q / heads_kv query heads;
@@ -112,6 +113,8 @@ typedef struct {
     int64_t first_position;  /* logical position of token 0 */
     int32_t policy;          /* ems_policy (0 = EMS) */
     int32_t sink_count;      /* PolicyHandle::sink_count (streaming_llm; reference default 4) */
+    int32_t position_mode;   /* decode expansion RoPE: 0 with_pos (entry position), 1 without_pos
+                                (center position); CompressionConfig::position_mode, cache.hpp:11 */
 } ems_desc;
 
 /* Per-unit capacities of the compressed cache (fixed-size SoA). */
@@ -221,6 +224,60 @@ EMS_API int ems_prefill_host(const ems_desc* desc, double rope_base, const void*
                      float* loc, const ems_cache* d_cache, const ems_cache* h_cache, int32_t chunks,
                      void* workspace, size_t workspace_bytes, cudaStream_t stream,
                      cudaStream_t copy_stream);
+
+/* ---------------------------------------------------------------- decode
+ * The EMS decode loop, decode_step (proj/src/engine.cpp:150-210) with decode_update
+ * (proj/src/compressor.cpp:376-398), one CTA per unit per step.  The per-unit state is a
+ * fixed-capacity device SoA (HeadCacheState, proj/include/ems/cache.hpp:81-111): center
+ * slots (slot_alive marks live std::optional slots; a freed slot is reused lowest-first), a
+ * ring buffer of exact locals, the position-sorted LUT, and meta[8] = {ring head, locals,
+ * LUT entries, window_fill, compressed, live centers, 0, 0}.  Keys/values fp32, scores fp64.
+ * EMS policy only (the baselines' decode rules are not ported). */
+typedef struct {
+    float* slot_key;      /* [u][slots][d] unit-norm raw key */
+    float* slot_norm;     /* [u][slots] */
+    float* slot_value;    /* [u][slots][d] */
+    int32_t* slot_pos;    /* [u][slots] */
+    double* slot_score;   /* [u][slots][3] glo, loc_past, loc_cur */
+    int32_t* slot_alive;  /* [u][slots] */
+    float* local_key;     /* [u][locals][d] raw key (ring) */
+    float* local_value;   /* [u][locals][d] */
+    int32_t* local_pos;   /* [u][locals] */
+    double* local_score;  /* [u][locals][3] */
+    int32_t* lut_pos;     /* [u][lut] */
+    int32_t* lut_slot;    /* [u][lut], -1 = zero class */
+    int32_t* meta;        /* [u][8] */
+} ems_decode_state;
+
+typedef struct {
+    int32_t units;
+    int32_t slots;   /* center_capacity + 1 */
+    int32_t locals;  /* max(l_win, n_budget) + 1 (a keep-all prefill leaves up to n_budget locals) */
+    int32_t lut;     /* lut_capacity = floor(gamma * n_budget) (cache.hpp:36-38) */
+    int32_t rows;    /* lut + locals: the most expanded rows one step can attend */
+} ems_decode_dims;
+
+EMS_API int ems_decode_dims_for(const ems_desc* desc, ems_decode_dims* out);
+EMS_API size_t ems_decode_workspace_bytes(const ems_desc* desc);
+
+/* (cos, sin) of position * base^(-2i/d) for positions [0, max_positions), fp64 rounded to
+ * fp32: table = float2 [max_positions][head_dim / 2] (device).  Shared by all decode steps. */
+EMS_API int ems_rope_table(int32_t head_dim, double base, int32_t max_positions, void* table,
+                   cudaStream_t stream);
+
+/* Decode state from a prefill cache (ems_prefill / ems_prefill_compress output); window_fill
+ * starts at 0 as engine::prefill leaves it (engine.cpp:74). */
+EMS_API int ems_decode_init(const ems_desc* desc, const ems_cache* cache, const ems_decode_state* state,
+                    cudaStream_t stream);
+
+/* One decode step for every unit at logical `position` (engine::next_position):
+ *   q [B][Hq][d], k / v [B][Hkv][d] raw (pre-RoPE), dtype -> out [B][Hq][d] (dtype),
+ *   argmax_position [B][Hq] int32 (logical position of each query head's largest weight).
+ * position < max_positions of the RoPE table. */
+EMS_API int ems_decode_step(const ems_desc* desc, int64_t position, const void* rope_table,
+                    int32_t max_positions, const void* q, const void* k, const void* v, void* out,
+                    int32_t* argmax_position, const ems_decode_state* state, void* workspace,
+                    size_t workspace_bytes, cudaStream_t stream);
 
 /* Standalone redundancy_cross (analysis.hpp:19-20) for one pair of token groups:
  * k_rows/v_rows [n_rows][d], k_cols/v_cols [n_cols][d] (dtype) -> r [n_rows][n_cols] fp32. */

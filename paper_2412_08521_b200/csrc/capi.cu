@@ -38,6 +38,14 @@ cudaError_t launch_keep_all(const Dims& dm, int dtype, const void* k, const void
                             const ems_cache& c, int64_t first_pos, cudaStream_t s);
 cudaError_t launch_rope(int dtype, int planes, int L, int d, double base, long long first_pos,
                         const void* x, void* y, cudaStream_t s);
+cudaError_t launch_rope_table(float2* table, int max_pos, int d, double base, cudaStream_t s);
+cudaError_t launch_decode_init(const Dims& m, int dtype, const ems_cache& c, const ems_decode_state& st,
+                               int S, int W, int T, cudaStream_t s);
+cudaError_t launch_decode_step(const Dims& m, int dtype, int S, int W, int T, int R, int l_win, int lut_cap,
+                               double tau, int zero_class, int with_pos, long long position, int max_pos,
+                               const float2* table, const void* q, const void* k, const void* v, void* out,
+                               int32_t* argmax_pos, const ems_decode_state& st, void* ws, cudaStream_t s);
+size_t decode_workspace_bytes(const Dims& m, int R);
 cudaError_t launch_redundancy_cross(int dtype, int d, const void* kr, const void* vr, int nr,
                                     const void* kc, const void* vc, int nc, int key_only,
                                     float* r, cudaStream_t s);
@@ -677,3 +685,120 @@ extern "C" int ems_prefill_host(const ems_desc* d, double rope_base, const void*
     EMS_CUDA_CHECK(cudaStreamWaitEvent(s, ev[2 * nc + 1], 0));
     return EMS_OK;
 }
+
+// ----------------------------------------------------------------------------------------
+// Decode (decode_step / decode_update).
+namespace ems {
+namespace {
+void decode_caps(const ems_desc& d, int& S, int& W, int& T, int& R) {
+    const Dims m = make_dims(d);
+    S = m.cap_c + 1;
+    W = (d.l_win > d.n_budget ? d.l_win : d.n_budget) + 1;
+    T = (int)(d.gamma * (double)d.n_budget);  // lut_capacity, cache.hpp:36-38
+    if (T < m.cap_lut) T = m.cap_lut;
+    R = T + W;
+}
+int decode_check(const ems_desc* d) {
+    if (int rc = ems_validate(d)) return rc;
+    if (d->policy != EMS_POLICY_EMS) {
+        set_error("decode: only the EMS policy's decode_update is implemented on the device");
+        return EMS_UNSUPPORTED;
+    }
+    if (d->heads_q / d->heads_kv > 8) {
+        set_error("decode: at most 8 query heads per KV head");
+        return EMS_UNSUPPORTED;
+    }
+    if (d->position_mode != 0 && d->position_mode != 1) {
+        set_error("bad position_mode");
+        return EMS_INVALID_ARGUMENT;
+    }
+    return EMS_OK;
+}
+}  // namespace
+}  // namespace ems
+
+extern "C" {
+
+int ems_decode_dims_for(const ems_desc* d, ems_decode_dims* out) {
+    using namespace ems;
+    if (int rc = decode_check(d)) return rc;
+    int S, W, T, R;
+    decode_caps(*d, S, W, T, R);
+    out->units = d->batch * d->heads_kv;
+    out->slots = S;
+    out->locals = W;
+    out->lut = T;
+    out->rows = R;
+    return EMS_OK;
+}
+
+size_t ems_decode_workspace_bytes(const ems_desc* d) {
+    using namespace ems;
+    if (decode_check(d) != EMS_OK) return 0;
+    int S, W, T, R;
+    decode_caps(*d, S, W, T, R);
+    return decode_workspace_bytes(make_dims(*d), R);
+}
+
+int ems_rope_table(int32_t d, double base, int32_t max_pos, void* table, cudaStream_t s) {
+    using namespace ems;
+    if (d <= 0 || d % 2 || !(base > 0.0) || max_pos <= 0 || !table) {
+        set_error("ems_rope_table: bad arguments");
+        return EMS_INVALID_ARGUMENT;
+    }
+    cudaError_t e = launch_rope_table(static_cast<float2*>(table), max_pos, d, base, s);
+    if (e != cudaSuccess) {
+        set_error("rope table launch: %s", cudaGetErrorString(e));
+        return EMS_CUDA_ERROR;
+    }
+    return EMS_OK;
+}
+
+int ems_decode_init(const ems_desc* d, const ems_cache* c, const ems_decode_state* st, cudaStream_t s) {
+    using namespace ems;
+    if (int rc = decode_check(d)) return rc;
+    if (!c || !st) {
+        set_error("ems_decode_init: null cache/state");
+        return EMS_INVALID_ARGUMENT;
+    }
+    int S, W, T, R;
+    decode_caps(*d, S, W, T, R);
+    cudaError_t e = launch_decode_init(make_dims(*d), d->dtype, *c, *st, S, W, T, s);
+    if (e != cudaSuccess) {
+        set_error("decode init launch: %s", cudaGetErrorString(e));
+        return EMS_CUDA_ERROR;
+    }
+    return EMS_OK;
+}
+
+int ems_decode_step(const ems_desc* d, int64_t position, const void* table, int32_t max_pos, const void* q,
+                    const void* k, const void* v, void* out, int32_t* argmax_pos, const ems_decode_state* st,
+                    void* ws, size_t ws_bytes, cudaStream_t s) {
+    using namespace ems;
+    if (int rc = decode_check(d)) return rc;
+    if (!table || !q || !k || !v || !out || !argmax_pos || !st) {
+        set_error("ems_decode_step: null argument");
+        return EMS_INVALID_ARGUMENT;
+    }
+    if (position < 0 || position >= max_pos) {
+        set_error("ems_decode_step: position %lld outside the RoPE table [0, %d)", (long long)position, max_pos);
+        return EMS_INVALID_ARGUMENT;
+    }
+    int S, W, T, R;
+    decode_caps(*d, S, W, T, R);
+    const Dims m = make_dims(*d);
+    if (!ws || ws_bytes < decode_workspace_bytes(m, R)) {
+        set_error("ems_decode_step: workspace too small (need %zu)", decode_workspace_bytes(m, R));
+        return EMS_INVALID_ARGUMENT;
+    }
+    cudaError_t e = launch_decode_step(m, d->dtype, S, W, T, R, d->l_win, T, d->tau, d->zero_class,
+                                       d->position_mode == 0, position, max_pos, static_cast<const float2*>(table),
+                                       q, k, v, out, argmax_pos, *st, ws, s);
+    if (e != cudaSuccess) {
+        set_error("decode step launch: %s", cudaGetErrorString(e));
+        return EMS_CUDA_ERROR;
+    }
+    return EMS_OK;
+}
+
+}  // extern "C"

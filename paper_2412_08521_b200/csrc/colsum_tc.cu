@@ -112,10 +112,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     __shared__ Bars bars;
 
     const int tid = threadIdx.x, warp = tid >> 5;
-    const int per_jp = a.units * a.hsplit;
-    const int jp = blockIdx.x / per_jp;                // key-tile pair, heaviest first
-    const int unit = blockIdx.x % a.units;
-    const int hg = (blockIdx.x % per_jp) / a.units;    // head group (hsplit > 1)
+    int jp, unit, hg;                                  // key-tile pair (heaviest first), unit, head group
+    if (a.unit_major) {                                // unit by unit: the unit's Q stays in L2
+        const int per_unit = ((a.nT + 1) / 2) * a.hsplit;
+        unit = blockIdx.x / per_unit;
+        const int r = blockIdx.x % per_unit;
+        jp = r / a.hsplit;
+        hg = r % a.hsplit;
+    } else {
+        const int per_jp = a.units * a.hsplit;
+        jp = blockIdx.x / per_jp;
+        unit = blockIdx.x % a.units;
+        hg = (blockIdx.x % per_jp) / a.units;
+    }
     const int gh = a.G / a.hsplit;                     // query heads of this CTA
     const int b = unit / a.Hkv, hk = unit % a.Hkv;
     const int J0 = 2 * jp;
@@ -313,6 +322,11 @@ cudaError_t launch_colsum_tc(const ColArgs& a, const CUtensorMap& tk, const CUte
 // ~4 CTAs per SM (the heaviest key-tile pair otherwise dominates small unit counts).
 int colsum_hsplit(int G, int nT, int units) {
     const int pairs = (nT + 1) / 2;
+    static const int forced = [] {
+        const char* e = getenv("EMS_P2_HSPLIT");  // tuning override (power of two dividing G)
+        return e ? atoi(e) : 0;
+    }();
+    if (forced > 0 && G % forced == 0) return forced;
     int hs = 1;
     while (hs < G && G % (2 * hs) == 0 && (long long)pairs * units * hs < 4LL * 148) hs *= 2;
     return hs;

@@ -1,0 +1,640 @@
+// decode.cu -- (f2) the EMS decode step on the device: one CTA per KV unit.
+//
+// Restates, per head (unit), decode_step (proj/src/engine.cpp:150-210):
+//   append the raw (k, v) to the local window; expand the cache through its look-up table
+//   (expand_cache, engine.cpp:84-132: every non-zero LUT entry materialises its center's
+//   unit_key * key_norm RoPE'd at the entry's position (with_pos) or the center's
+//   (without_pos), then the locals RoPE'd at their own positions); attend the RoPE'd query
+//   over the expanded rows (attention_row_probs / weighted_value_sum); let the attention
+//   mass flow back into the owning entries' glo and loc_cur; rotate the score windows every
+//   l_win steps (cache.cpp:96-106); then decode_update (proj/src/compressor.cpp:376-398):
+//   graduate the oldest locals beyond l_win into center slots (lowest free slot, LUT entry
+//   appended, oldest zero-mapped / oldest LUT entry dropped at capacity) and, when the
+//   centers exceed their capacity, retire the least important center
+//   (retire_least_important_center, :286-372): merge it into its most redundant center
+//   (R = cos(unit keys) * cos(values) >= tau, weights = combined Glo-Loc scores) or send its
+//   LUT entries to the zero class / remove them.
+// GQA (contract D2): the G query heads of a unit attend the same cache; the mass flowing
+// back is the mean of their probabilities.
+// Numerics: keys/values fp32, logits fp32 dot products, softmax exp in fp32 with an fp64
+// normaliser, value sums and all score accumulators in fp64.  Every reduction runs in a
+// fixed order (no float atomics) -> deterministic.
+#include <float.h>
+
+#include "common.cuh"
+
+namespace ems {
+
+namespace {
+
+constexpr int kT = 256;  // threads per CTA
+constexpr int kWarps = kT / 32;
+
+struct DecArgs {
+    int G, d, S, W, T, R;          // query heads per unit; capacities: slots, locals, LUT, rows
+    int l_win, cap_c, lut_cap;
+    double tau;
+    int zero_class, with_pos;
+    long long position;
+    int max_pos;
+    const float2* table;           // [max_pos][d/2] (cos, sin)
+    const void* q;                 // [units*G][d] raw
+    const void* k;                 // [units][d] raw
+    const void* v;                 // [units][d]
+    int dtype;
+    void* out;                     // [units*G][d]
+    int32_t* argmax_pos;           // [units*G]
+    ems_decode_state st;
+    int32_t* row_owner;            // [units][R]
+    int32_t* row_pos;              // [units][R]
+    float* probs;                  // [units][G][R]
+    float* pmean;                  // [units][R]
+};
+
+__device__ __forceinline__ float ldx(const void* p, size_t i, int dtype) {
+    return dtype == EMS_F32 ? static_cast<const float*>(p)[i]
+                            : __bfloat162float(static_cast<const __nv_bfloat16*>(p)[i]);
+}
+__device__ __forceinline__ void stx(void* p, size_t i, int dtype, double x) {
+    if (dtype == EMS_F32) static_cast<float*>(p)[i] = (float)x;
+    else static_cast<__nv_bfloat16*>(p)[i] = __float2bfloat16_rn((float)x);
+}
+
+// ---- block-wide helpers (fixed reduction order -> deterministic) ----------------------
+__device__ double bsum(double v, double* sh) {
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    v = warp_sum(v);
+    __syncthreads();
+    if (l == 0) sh[w] = v;
+    __syncthreads();
+    double t = 0.0;
+    for (int i = 0; i < kWarps; ++i) t += sh[i];
+    __syncthreads();
+    return t;
+}
+__device__ float bmax(float v, float* sh) {
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    v = warp_max(v);
+    __syncthreads();
+    if (l == 0) sh[w] = v;
+    __syncthreads();
+    float t = -FLT_MAX;
+    for (int i = 0; i < kWarps; ++i) t = fmaxf(t, sh[i]);
+    __syncthreads();
+    return t;
+}
+// (key, tie, idx) lexicographic "better" selection; better(a, b) decides.  Keys/ties are
+// a total order on the candidates, so the result does not depend on reduction order.
+struct Cand {
+    double key;
+    long long tie;
+    int idx;
+};
+template <class Better>
+__device__ Cand bselect(Cand c, Better better, Cand* sh) {
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        Cand x;
+        x.key = __shfl_xor_sync(0xffffffffu, c.key, o);
+        x.tie = __shfl_xor_sync(0xffffffffu, c.tie, o);
+        x.idx = __shfl_xor_sync(0xffffffffu, c.idx, o);
+        if (better(x, c)) c = x;
+    }
+    __syncthreads();
+    if (l == 0) sh[w] = c;
+    __syncthreads();
+    Cand t = sh[0];
+    for (int i = 1; i < kWarps; ++i)
+        if (better(sh[i], t)) t = sh[i];
+    __syncthreads();
+    return t;
+}
+// exclusive scan of one int per thread; returns the total in *tot
+__device__ int bscan(int x, int* sh, int* tot) {
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    int inc = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (l >= o) inc += y;
+    }
+    __syncthreads();
+    if (l == 31) sh[w] = inc;
+    __syncthreads();
+    int base = 0, all = 0;
+    for (int i = 0; i < kWarps; ++i) {
+        if (i < w) base += sh[i];
+        all += sh[i];
+    }
+    __syncthreads();
+    *tot = all;
+    return base + inc - x;
+}
+
+// combined_entry_score, proj/src/compressor.cpp:261-267
+__device__ __forceinline__ double combined(const double* sc, double align) {
+    if (align <= 0.0) return sc[0];
+    return fmax(sc[0] * align, sc[1] + sc[2]);
+}
+
+__global__ void __launch_bounds__(kT) decode_step_kernel(DecArgs a) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    const int u = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int d = a.d, S = a.S, W = a.W, T = a.T, G = a.G, pairs = d / 2;
+    double* acc = reinterpret_cast<double*>(dsm);                  // [S + W] owner mass / R values
+    float* qrot = reinterpret_cast<float*>(acc + (S + W));          // [G][d]
+    __shared__ double shd[kWarps];
+    __shared__ float shf[kWarps];
+    __shared__ Cand shc[kWarps];
+    __shared__ int shi[kWarps];
+    __shared__ int s_meta[8];
+    __shared__ double s_w[4];
+    __shared__ int s_i[4];
+
+    const ems_decode_state& st = a.st;
+    float* skey = st.slot_key + (size_t)u * S * d;
+    float* snorm = st.slot_norm + (size_t)u * S;
+    float* sval = st.slot_value + (size_t)u * S * d;
+    int32_t* spos = st.slot_pos + (size_t)u * S;
+    double* sscore = st.slot_score + (size_t)u * S * 3;
+    int32_t* salive = st.slot_alive + (size_t)u * S;
+    float* lkey = st.local_key + (size_t)u * W * d;
+    float* lval = st.local_value + (size_t)u * W * d;
+    int32_t* lpos = st.local_pos + (size_t)u * W;
+    double* lscore = st.local_score + (size_t)u * W * 3;
+    int32_t* tpos = st.lut_pos + (size_t)u * T;
+    int32_t* tslot = st.lut_slot + (size_t)u * T;
+    int32_t* meta = st.meta + (size_t)u * 8;
+    int32_t* rown = a.row_owner + (size_t)u * a.R;
+    int32_t* rpos = a.row_pos + (size_t)u * a.R;
+    float* prob = a.probs + (size_t)u * G * a.R;
+    float* pm = a.pmean + (size_t)u * a.R;
+
+    if (tid < 8) s_meta[tid] = meta[tid];
+    __syncthreads();
+    int head = s_meta[0], count = s_meta[1], lut_n = s_meta[2];
+
+    // 1. append the incoming token to the local window (engine.cpp:166-172)
+    {
+        const int slot = (head + count) % W;
+        for (int i = tid; i < d; i += kT) {
+            lkey[(size_t)slot * d + i] = ldx(a.k, (size_t)u * d + i, a.dtype);
+            lval[(size_t)slot * d + i] = ldx(a.v, (size_t)u * d + i, a.dtype);
+        }
+        if (tid == 0) {
+            lpos[slot] = (int32_t)a.position;
+            lscore[3 * slot] = lscore[3 * slot + 1] = lscore[3 * slot + 2] = 0.0;
+        }
+        ++count;
+    }
+    // 2. RoPE'd queries (apply_rope at the new position, engine.cpp:175)
+    for (int x = tid; x < G * pairs; x += kT) {
+        const int h = x / pairs, p = x % pairs;
+        const float q0 = ldx(a.q, ((size_t)u * G + h) * d + 2 * p, a.dtype);
+        const float q1 = ldx(a.q, ((size_t)u * G + h) * d + 2 * p + 1, a.dtype);
+        const float2 cs = a.table[(size_t)a.position * pairs + p];
+        qrot[h * d + 2 * p] = q0 * cs.x - q1 * cs.y;
+        qrot[h * d + 2 * p + 1] = q0 * cs.y + q1 * cs.x;
+    }
+    // 3. expanded rows: non-zero LUT entries in LUT order, then the locals (expand_cache)
+    int n_rows;
+    {
+        int base = 0;
+        for (int c0 = 0; c0 < lut_n; c0 += kT) {
+            const int e = c0 + tid;
+            const int keep = e < lut_n && tslot[e] >= 0;
+            int tot;
+            const int off = bscan(keep, shi, &tot);
+            if (keep) {
+                rown[base + off] = tslot[e];
+                rpos[base + off] = tpos[e];
+            }
+            base += tot;
+        }
+        for (int li = tid; li < count; li += kT) {
+            const int ring = (head + li) % W;
+            rown[base + li] = S + ring;
+            rpos[base + li] = lpos[ring];
+        }
+        n_rows = base + count;
+    }
+    __syncthreads();
+    // 4. logits: one warp per row, lanes over RoPE pairs; all G heads share the key
+    const float scale = rsqrtf((float)d);
+    for (int r = warp; r < n_rows; r += kWarps) {
+        const int o = rown[r];
+        const bool center = o < S;
+        const float* kb = center ? skey + (size_t)o * d : lkey + (size_t)(o - S) * d;
+        const float kn = center ? snorm[o] : 1.f;
+        const int rp = center && !a.with_pos ? spos[o] : rpos[r];
+        float part[8];
+#pragma unroll
+        for (int h = 0; h < 8; ++h) part[h] = 0.f;
+        for (int p = lane; p < pairs; p += 32) {
+            const float k0 = kb[2 * p] * kn, k1 = kb[2 * p + 1] * kn;
+            const float2 cs = a.table[(size_t)rp * pairs + p];
+            const float r0 = k0 * cs.x - k1 * cs.y, r1 = k0 * cs.y + k1 * cs.x;
+#pragma unroll
+            for (int h = 0; h < 8; ++h)
+                if (h < G) part[h] += qrot[h * d + 2 * p] * r0 + qrot[h * d + 2 * p + 1] * r1;
+        }
+#pragma unroll
+        for (int h = 0; h < 8; ++h)
+            if (h < G) {
+                const float s = warp_sum(part[h]);
+                if (lane == 0) prob[(size_t)h * a.R + r] = s * scale;
+            }
+    }
+    __syncthreads();
+    // 5. softmax per query head (softmax_in_place: max-subtracted exp, fp64 normaliser)
+    for (int h = 0; h < G; ++h) {
+        float* ph = prob + (size_t)h * a.R;
+        float m = -FLT_MAX;
+        for (int r = tid; r < n_rows; r += kT) m = fmaxf(m, ph[r]);
+        m = bmax(m, shf);
+        double z = 0.0;
+        for (int r = tid; r < n_rows; r += kT) z += (double)expf(ph[r] - m);
+        z = bsum(z, shd);
+        for (int r = tid; r < n_rows; r += kT) ph[r] = (float)((double)expf(ph[r] - m) / z);
+        __syncthreads();
+    }
+    // 6. outputs (weighted_value_sum, fp64, rows in order) and 7. argmax positions
+    for (int x = tid; x < G * d; x += kT) {
+        const int h = x / d, i = x % d;
+        const float* ph = prob + (size_t)h * a.R;
+        double o = 0.0;
+        for (int r = 0; r < n_rows; ++r) {
+            const int ow = rown[r];
+            const float val = ow < S ? sval[(size_t)ow * d + i] : lval[(size_t)(ow - S) * d + i];
+            o += (double)ph[r] * (double)val;
+        }
+        stx(a.out, ((size_t)u * G + h) * d + i, a.dtype, o);
+    }
+    for (int h = 0; h < G; ++h) {
+        const float* ph = prob + (size_t)h * a.R;
+        Cand c{-1.0, 0, -1};
+        for (int r = tid; r < n_rows; r += kT)
+            if (c.idx < 0 || (double)ph[r] > c.key) c = Cand{(double)ph[r], r, r};
+        auto better = [](const Cand& x, const Cand& y) {
+            if (y.idx < 0) return x.idx >= 0;
+            if (x.idx < 0) return false;
+            return x.key > y.key || (x.key == y.key && x.tie < y.tie);  // first max (engine.cpp:188-191)
+        };
+        c = bselect(c, better, shc);
+        if (tid == 0) a.argmax_pos[(size_t)u * G + h] = c.idx >= 0 ? rpos[c.idx] : -1;
+    }
+    // 8. attention mass flows back to the owners (engine.cpp:184-195), GQA mean
+    for (int r = tid; r < n_rows; r += kT) {
+        double s = 0.0;
+        for (int h = 0; h < G; ++h) s += (double)prob[(size_t)h * a.R + r];
+        pm[r] = (float)(s / G);
+    }
+    for (int i = tid; i < S + W; i += kT) acc[i] = 0.0;
+    __syncthreads();
+    if (warp == 0) {  // ordered pass: rows in order, equal owners inside a 32-row chunk summed in lane order
+        for (int b = 0; b < n_rows; b += 32) {
+            const int r = b + lane;
+            const int o = r < n_rows ? rown[r] : -1 - lane;
+            const double p = r < n_rows ? (G == 1 ? (double)prob[r] : (double)pm[r]) : 0.0;
+            const unsigned grp = __match_any_sync(0xffffffffu, o);
+            double gs = 0.0;
+            for (unsigned m = grp; m; m &= m - 1) gs += __shfl_sync(grp, p, __ffs(m) - 1);
+            if (r < n_rows && lane == __ffs(grp) - 1) acc[o] += gs;
+            __syncwarp();
+        }
+    }
+    __syncthreads();
+    for (int s = tid; s < S; s += kT)
+        if (salive[s]) sscore[3 * s] += acc[s], sscore[3 * s + 2] += acc[s];
+    for (int li = tid; li < count; li += kT) {
+        const int ring = (head + li) % W;
+        lscore[3 * ring] += acc[S + ring];
+        lscore[3 * ring + 2] += acc[S + ring];
+    }
+    // 9. score window rotation every l_win steps (engine.cpp:196-200)
+    int wfill = s_meta[3] + 1;
+    if (wfill >= a.l_win) {
+        for (int s = tid; s < S; s += kT)
+            if (salive[s]) sscore[3 * s + 1] = sscore[3 * s + 2], sscore[3 * s + 2] = 0.0;
+        for (int li = tid; li < count; li += kT) {
+            const int ring = (head + li) % W;
+            lscore[3 * ring + 1] = lscore[3 * ring + 2];
+            lscore[3 * ring + 2] = 0.0;
+        }
+        wfill = 0;
+    }
+    __syncthreads();
+    // 10. decode_update (compressor.cpp:376-398)
+    int n_alive = s_meta[5], compressed = s_meta[4];
+    while (count > a.l_win) {
+        const int g = head;  // graduating local (front of the window)
+        // 10a. oldest zero-mapped (else oldest) LUT entry leaves at capacity (:272-284)
+        if (lut_n >= a.lut_cap) {
+            Cand c{0.0, 0, -1};
+            for (int e = tid; e < lut_n; e += kT)
+                if (tslot[e] < 0 && (c.idx < 0 || e < c.idx)) c = Cand{0.0, e, e};
+            auto first = [](const Cand& x, const Cand& y) {
+                return x.idx >= 0 && (y.idx < 0 || x.idx < y.idx);
+            };
+            c = bselect(c, first, shc);
+            const int at = c.idx >= 0 ? c.idx : 0;
+            for (int c0 = at + 1; c0 < lut_n; c0 += kT) {
+                const int e = c0 + tid;
+                int pp = 0, ss = 0;
+                if (e < lut_n) pp = tpos[e], ss = tslot[e];
+                __syncthreads();
+                if (e < lut_n) tpos[e - 1] = pp, tslot[e - 1] = ss;
+                __syncthreads();
+            }
+            --lut_n;
+        }
+        // 10b. insert_center: lowest free slot (cache.cpp:48-57)
+        Cand fs{0.0, 0, -1};
+        for (int s = tid; s < S; s += kT)
+            if (!salive[s] && (fs.idx < 0 || s < fs.idx)) fs = Cand{0.0, s, s};
+        auto lower = [](const Cand& x, const Cand& y) { return x.idx >= 0 && (y.idx < 0 || x.idx < y.idx); };
+        fs = bselect(fs, lower, shc);
+        const int slot = fs.idx;
+        double kk = 0.0;
+        for (int i = tid; i < d; i += kT) kk += (double)lkey[(size_t)g * d + i] * lkey[(size_t)g * d + i];
+        const double kn = sqrt(bsum(kk, shd));  // normalized_or_zero, :16-25
+        for (int i = tid; i < d; i += kT) {
+            const float x = lkey[(size_t)g * d + i];
+            skey[(size_t)slot * d + i] = kn > 0.0 ? (float)((double)x / kn) : x;
+            sval[(size_t)slot * d + i] = lval[(size_t)g * d + i];
+        }
+        if (tid == 0) {
+            snorm[slot] = (float)kn;
+            spos[slot] = lpos[g];
+            for (int t = 0; t < 3; ++t) sscore[3 * slot + t] = lscore[3 * g + t];
+            salive[slot] = 1;
+            tpos[lut_n] = lpos[g];
+            tslot[lut_n] = slot;
+        }
+        ++lut_n;
+        ++n_alive;
+        head = (head + 1) % W;
+        --count;
+        __syncthreads();
+        if (n_alive <= a.cap_c) continue;
+        // 10c. retire_least_important_center (:286-372)
+        double sg = 0.0, sl = 0.0;
+        for (int s = tid; s < S; s += kT)
+            if (salive[s]) sg += sscore[3 * s], sl += sscore[3 * s + 1] + sscore[3 * s + 2];
+        for (int li = tid; li < count; li += kT) {
+            const int ring = (head + li) % W;
+            sg += lscore[3 * ring];
+            sl += lscore[3 * ring + 1] + lscore[3 * ring + 2];
+        }
+        sg = bsum(sg, shd);
+        sl = bsum(sl, shd);
+        const double align = sg > 0.0 ? sl / sg : 0.0;  // alignment_ratio, :244-259
+        Cand tb{0.0, 0, -1};
+        for (int s = tid; s < S; s += kT)
+            if (salive[s]) {
+                const Cand x{combined(sscore + 3 * s, align), spos[s], s};
+                if (tb.idx < 0 || x.key < tb.key || (x.key == tb.key && x.tie < tb.tie)) tb = x;
+            }
+        auto least = [](const Cand& x, const Cand& y) {
+            if (y.idx < 0) return x.idx >= 0;
+            if (x.idx < 0) return false;
+            return x.key < y.key || (x.key == y.key && x.tie < y.tie);
+        };
+        tb = bselect(tb, least, shc);
+        const int ts = tb.idx;
+        // R(tbm, c) for every other alive center: one warp per center
+        double vv = 0.0;
+        for (int i = tid; i < d; i += kT) vv += (double)sval[(size_t)ts * d + i] * sval[(size_t)ts * d + i];
+        const double nv1 = sqrt(bsum(vv, shd));
+        const float tnorm = snorm[ts];
+        for (int c = warp; c < S; c += kWarps) {
+            if (!salive[c] || c == ts) continue;
+            double kd = 0.0, vd = 0.0, v2 = 0.0;
+            for (int i = lane; i < d; i += 32) {
+                kd += (double)skey[(size_t)ts * d + i] * skey[(size_t)c * d + i];
+                vd += (double)sval[(size_t)ts * d + i] * sval[(size_t)c * d + i];
+                v2 += (double)sval[(size_t)c * d + i] * sval[(size_t)c * d + i];
+            }
+            kd = warp_sum(kd);
+            vd = warp_sum(vd);
+            v2 = warp_sum(v2);
+            if (lane == 0) {
+                double r = 0.0;
+                if (tnorm > 0.f && snorm[c] > 0.f) {
+                    const double ck = fmin(fmax(kd, -1.0), 1.0);
+                    const double nv2 = sqrt(v2);
+                    const double cv = (nv1 > 0.0 && nv2 > 0.0) ? fmin(fmax(vd / (nv1 * nv2), -1.0), 1.0) : 0.0;
+                    r = ck * cv;
+                }
+                acc[c] = r;
+            }
+        }
+        __syncthreads();
+        Cand bs{0.0, 0, -1};
+        for (int c = tid; c < S; c += kT)
+            if (salive[c] && c != ts) {
+                const Cand x{acc[c], spos[c], c};
+                if (bs.idx < 0 || x.key > bs.key || (x.key == bs.key && x.tie < bs.tie)) bs = x;
+            }
+        auto most = [](const Cand& x, const Cand& y) {
+            if (y.idx < 0) return x.idx >= 0;
+            if (x.idx < 0) return false;
+            return x.key > y.key || (x.key == y.key && x.tie < y.tie);
+        };
+        bs = bselect(bs, most, shc);
+        const int best = bs.idx;
+        if (best >= 0 && bs.key >= a.tau) {  // merge into the most redundant center
+            if (tid == 0) {
+                double wd = combined(sscore + 3 * best, align), wt = combined(sscore + 3 * ts, align);
+                double ws = wd + wt;
+                if (ws <= 0.0) wd = 0.5, wt = 0.5, ws = 1.0;
+                s_w[0] = wd / ws;
+                s_w[1] = wt / ws;
+            }
+            __syncthreads();
+            const double fd = s_w[0], ft = s_w[1];
+            double mk2 = 0.0;
+            for (int i = tid; i < d; i += kT) {
+                const double m = fd * skey[(size_t)best * d + i] + ft * skey[(size_t)ts * d + i];
+                mk2 += m * m;
+            }
+            const double mn = sqrt(bsum(mk2, shd));
+            for (int i = tid; i < d; i += kT) {
+                const double m = fd * skey[(size_t)best * d + i] + ft * skey[(size_t)ts * d + i];
+                const double mv = fd * sval[(size_t)best * d + i] + ft * sval[(size_t)ts * d + i];
+                if (mn > 0.0) skey[(size_t)best * d + i] = (float)(m / mn);
+                sval[(size_t)best * d + i] = (float)mv;
+            }
+            if (tid == 0)
+                for (int t = 0; t < 3; ++t) sscore[3 * best + t] += sscore[3 * ts + t];
+            for (int e = tid; e < lut_n; e += kT)
+                if (tslot[e] == ts) tslot[e] = best;
+        } else if (a.zero_class) {
+            for (int e = tid; e < lut_n; e += kT)
+                if (tslot[e] == ts) tslot[e] = -1;
+        } else {  // explicit removal: stable in-place compaction of the LUT
+            int base = 0;
+            for (int c0 = 0; c0 < lut_n; c0 += kT) {
+                const int e = c0 + tid;
+                int pp = 0, ss = 0;
+                const int keep = e < lut_n && tslot[e] != ts;
+                if (e < lut_n) pp = tpos[e], ss = tslot[e];
+                int tot;
+                const int off = bscan(keep, shi, &tot);
+                if (keep) tpos[base + off] = pp, tslot[base + off] = ss;
+                base += tot;
+                __syncthreads();
+            }
+            lut_n = base;
+        }
+        __syncthreads();
+        if (tid == 0) salive[ts] = 0;
+        --n_alive;
+        compressed = 1;
+        __syncthreads();
+    }
+    if (tid == 0) {
+        meta[0] = head;
+        meta[1] = count;
+        meta[2] = lut_n;
+        meta[3] = wfill;
+        meta[4] = compressed;
+        meta[5] = n_alive;
+    }
+}
+
+// Decode state from a prefill cache (policy_prefill_compress output, slots in order).
+template <typename T>
+__global__ void decode_init_kernel(ems_cache c, ems_decode_state st, int d, int cap_c, int cap_l, int cap_lut,
+                                   int S, int W, int T_) {
+    const int u = blockIdx.x, tid = threadIdx.x;
+    const int32_t* cnt = c.counts + 4 * u;
+    const int nc = cnt[0], nl = cnt[1], nu = cnt[2];
+    const T* ck = static_cast<const T*>(c.center_key) + (size_t)u * cap_c * d;
+    const T* cv = static_cast<const T*>(c.center_value) + (size_t)u * cap_c * d;
+    const T* lk = static_cast<const T*>(c.local_key) + (size_t)u * cap_l * d;
+    const T* lv = static_cast<const T*>(c.local_value) + (size_t)u * cap_l * d;
+    for (int x = tid; x < S * d; x += blockDim.x) {
+        const int s = x / d;
+        st.slot_key[(size_t)u * S * d + x] = s < nc ? ld(ck + x) : 0.f;
+        st.slot_value[(size_t)u * S * d + x] = s < nc ? ld(cv + x) : 0.f;
+    }
+    for (int s = tid; s < S; s += blockDim.x) {
+        st.slot_alive[(size_t)u * S + s] = s < nc;
+        st.slot_norm[(size_t)u * S + s] = s < nc ? c.center_norm[(size_t)u * cap_c + s] : 0.f;
+        st.slot_pos[(size_t)u * S + s] = s < nc ? c.center_pos[(size_t)u * cap_c + s] : 0;
+        for (int t = 0; t < 3; ++t)
+            st.slot_score[((size_t)u * S + s) * 3 + t] = s < nc ? c.center_score[((size_t)u * cap_c + s) * 3 + t] : 0.0;
+    }
+    for (int x = tid; x < W * d; x += blockDim.x) {
+        const int l = x / d;
+        st.local_key[(size_t)u * W * d + x] = l < nl ? ld(lk + x) : 0.f;
+        st.local_value[(size_t)u * W * d + x] = l < nl ? ld(lv + x) : 0.f;
+    }
+    for (int l = tid; l < W; l += blockDim.x) {
+        st.local_pos[(size_t)u * W + l] = l < nl ? c.local_pos[(size_t)u * cap_l + l] : 0;
+        for (int t = 0; t < 3; ++t)
+            st.local_score[((size_t)u * W + l) * 3 + t] = l < nl ? c.local_score[((size_t)u * cap_l + l) * 3 + t] : 0.0;
+    }
+    for (int e = tid; e < T_; e += blockDim.x) {
+        st.lut_pos[(size_t)u * T_ + e] = e < nu ? c.lut_pos[(size_t)u * cap_lut + e] : 0;
+        st.lut_slot[(size_t)u * T_ + e] = e < nu ? c.lut_slot[(size_t)u * cap_lut + e] : 0;
+    }
+    if (tid == 0) {
+        int32_t* m = st.meta + 8 * u;
+        m[0] = 0;        // ring head
+        m[1] = nl;       // locals
+        m[2] = nu;       // LUT entries
+        m[3] = 0;        // window_fill (engine.cpp:74)
+        m[4] = cnt[3];   // compressed
+        m[5] = nc;       // alive centers
+        m[6] = m[7] = 0;
+    }
+}
+
+// RoPE table: (cos, sin) of pos * base^(-2i/d) in fp64, rounded to fp32 (rope.cpp:17-26)
+__global__ void rope_table_kernel(float2* t, int max_pos, int pairs, int d, double base) {
+    const size_t n = (size_t)max_pos * pairs;
+    for (size_t x = blockIdx.x * (size_t)blockDim.x + threadIdx.x; x < n; x += (size_t)gridDim.x * blockDim.x) {
+        const int p = (int)(x % pairs);
+        const long long pos = (long long)(x / pairs);
+        const double ang = (double)pos * pow(base, -(double)(2 * p) / (double)d);
+        double s, c;
+        sincos(ang, &s, &c);
+        t[x] = make_float2((float)c, (float)s);
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_rope_table(float2* table, int max_pos, int d, double base, cudaStream_t s) {
+    rope_table_kernel<<<4 * 148, 256, 0, s>>>(table, max_pos, d / 2, d, base);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_decode_init(const Dims& m, int dtype, const ems_cache& c, const ems_decode_state& st,
+                               int S, int W, int T, cudaStream_t s) {
+    if (dtype == EMS_F32)
+        decode_init_kernel<float><<<m.units, 256, 0, s>>>(c, st, m.d, m.cap_c, m.cap_l, m.cap_lut, S, W, T);
+    else
+        decode_init_kernel<__nv_bfloat16><<<m.units, 256, 0, s>>>(c, st, m.d, m.cap_c, m.cap_l, m.cap_lut, S, W,
+                                                                  T);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_decode_step(const Dims& m, int dtype, int S, int W, int T, int R, int l_win, int lut_cap,
+                               double tau, int zero_class, int with_pos, long long position, int max_pos,
+                               const float2* table, const void* q, const void* k, const void* v, void* out,
+                               int32_t* argmax_pos, const ems_decode_state& st, void* ws, cudaStream_t s) {
+    DecArgs a;
+    a.G = m.G;
+    a.d = m.d;
+    a.S = S;
+    a.W = W;
+    a.T = T;
+    a.R = R;
+    a.l_win = l_win;
+    a.cap_c = m.cap_c;
+    a.lut_cap = lut_cap;
+    a.tau = tau;
+    a.zero_class = zero_class;
+    a.with_pos = with_pos;
+    a.position = position;
+    a.max_pos = max_pos;
+    a.table = table;
+    a.q = q;
+    a.k = k;
+    a.v = v;
+    a.dtype = dtype;
+    a.out = out;
+    a.argmax_pos = argmax_pos;
+    a.st = st;
+    char* p = static_cast<char*>(ws);
+    auto take = [&](size_t bytes) {
+        char* r = p;
+        p += (bytes + 255) / 256 * 256;
+        return r;
+    };
+    const size_t U = m.units;
+    a.row_owner = reinterpret_cast<int32_t*>(take(U * R * 4));
+    a.row_pos = reinterpret_cast<int32_t*>(take(U * R * 4));
+    a.probs = reinterpret_cast<float*>(take(U * m.G * R * 4));
+    a.pmean = reinterpret_cast<float*>(take(U * R * 4));
+    const size_t smem = (size_t)(S + W) * 8 + (size_t)m.G * m.d * 4;
+    static size_t attr = 0;
+    if (smem > 48 * 1024 && smem > attr) {
+        cudaFuncSetAttribute(decode_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = smem;
+    }
+    decode_step_kernel<<<m.units, kT, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+size_t decode_workspace_bytes(const Dims& m, int R) {
+    auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+    const size_t U = m.units;
+    return al(U * R * 4) * 2 + al(U * m.G * R * 4) + al(U * R * 4);
+}
+
+}  // namespace ems

@@ -41,6 +41,7 @@ struct FwdArgs {
     __nv_bfloat16* out;            // [B*Hq][L][128] (may be null)
     float* nlse2;                  // [B*Hq][L] negated log2-domain LSE (always)
     float* lse_nat;                // [B*Hq][L] natural LSE (may be null)
+    int unit_major;                // CTA order: 1 = unit by unit (L2 reuse of K/V), 0 = tile-major
 };
 
 constexpr int kFwdStages = 2;
@@ -61,19 +62,28 @@ __device__ __forceinline__ void fwd_item(const FwdArgs& a, int bid, int& plane0,
                                          int& tile0, int& tile1, int& unit) {
     if (a.G >= 2) {
         const int pairs = a.G / 2;
-        const int per_tile = a.units * pairs;
-        const int I = a.nT - 1 - bid / per_tile;  // heaviest tiles first
-        const int rem = bid % per_tile;
-        unit = rem / pairs;
-        const int hp = rem % pairs;
+        int I, hp;
+        if (a.unit_major) {  // units in order, heaviest tiles first within a unit (K/V stay in L2)
+            const int per_unit = a.nT * pairs;
+            unit = bid / per_unit;
+            const int r = bid % per_unit;
+            I = a.nT - 1 - r / pairs;
+            hp = r % pairs;
+        } else {
+            const int per_tile = a.units * pairs;
+            I = a.nT - 1 - bid / per_tile;  // heaviest tiles first
+            const int rem = bid % per_tile;
+            unit = rem / pairs;
+            hp = rem % pairs;
+        }
         const int b = unit / a.Hkv, hk = unit % a.Hkv;
         plane0 = b * a.Hq + hk * a.G + 2 * hp;
         plane1 = plane0 + 1;
         tile0 = tile1 = I;
     } else {
         const int npair = a.nT / 2;
-        const int p = npair - 1 - bid / a.units;
-        unit = bid % a.units;
+        const int p = a.unit_major ? npair - 1 - bid % npair : npair - 1 - bid / a.units;
+        unit = a.unit_major ? bid / npair : bid % a.units;
         const int b = unit / a.Hkv, hk = unit % a.Hkv;
         plane0 = plane1 = b * a.Hq + hk;  // G == 1: query head == kv head
         tile0 = 2 * p;
@@ -389,6 +399,11 @@ cudaError_t score_tc(const Dims& dm, const void* q, const void* k, const void* v
     fa.out = static_cast<__nv_bfloat16*>(o);
     fa.nlse2 = nlse2;
     fa.lse_nat = lse;
+    static const int unit_major = [] {
+        const char* e = getenv("EMS_UNIT_MAJOR");  // tuning override
+        return e ? atoi(e) : 1;
+    }();
+    fa.unit_major = unit_major;
     const int n_fwd = dm.G >= 2 ? fa.nT * dm.units * (dm.G / 2) : (fa.nT / 2) * dm.units;
     // pairs (of every 8) whose exp2 runs on the FMA pipe; EMS_P1_POLY overrides (tuning)
     static const int poly = [] {
@@ -419,6 +434,13 @@ cudaError_t score_tc(const Dims& dm, const void* q, const void* k, const void* v
     }();
     ca.debug = p2_debug;
     ca.hsplit = colsum_hsplit(dm.G, fa.nT, dm.units);
+    // P2 keeps the global heaviest-first order: unit by unit leaves the last unit's heaviest
+    // key-tile pairs (the longest CTAs) to the end of the grid (measured +5% P2 time)
+    static const int p2_unit_major = [] {
+        const char* e = getenv("EMS_P2_UNIT_MAJOR");  // tuning override
+        return e ? atoi(e) : 0;
+    }();
+    ca.unit_major = p2_unit_major;
     // P2 variant: 2 = CTA-pair (cta_group::2, M = N = 256) kernel, 1 = single-CTA kernel
     static const int p2 = [] {
         const char* e = getenv("EMS_P2_IMPL");

@@ -38,6 +38,7 @@ struct ColArgs {
     // key-tile pair and writes fp64 partial sums part_{g,l}[unit][hsplit][L]; a reduce kernel
     // sums them in head-group order.  hsplit == 1 writes glo/loc directly.
     int hsplit = 1;
+    int unit_major = 1;    // CTA order: unit by unit (Q of one unit stays in L2) or pair-major
     double* part_g = nullptr;
     double* part_l = nullptr;
 };
