@@ -383,6 +383,9 @@ class RefLib:
         L.ems_ref_policy_prefill.argtypes = [C.c_int32, C.c_int64, _dp, _dp, _dp, _dp, C.c_int64, C.c_int64,
                                              C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_int64,
                                              C.c_int32]
+        L.ems_ref_engine_decode.argtypes = [_dp, _dp, _dp, _dp, _dp, _dp, C.c_int64, C.c_int64, C.c_int64,
+                                            C.c_int64, C.c_int64, C.c_int64, C.c_double, C.c_double,
+                                            C.c_int64, C.c_int32, C.c_int32, C.c_double, _dp, _i64p]
         L.ems_ref_gen_synthetic.argtypes = [C.c_int32, C.c_uint64, C.c_int64, C.c_int64, C.c_int64,
                                             C.c_int64, C.c_double, C.c_double, _dp, _dp, _dp]
 
@@ -455,6 +458,23 @@ class RefLib:
                                                   int(c.zero_class), rope_base, head),
                   "engine_prefill")
         return self.lib.ems_ref_last_json().decode()
+
+    def engine_decode(self, q, k, v, dq, dk, dv, c: Config, rope_base=10000.0, without_pos=False):
+        """engine::prefill + decode_step x steps (EMS).  q/k/v [H][n][d], dq/dk/dv [steps][H][d].
+        Returns (out [steps][H][d], argmax [steps][H], prefill caches, final caches)."""
+        q, k, v, dq, dk, dv = map(_f64, (q, k, v, dq, dk, dv))
+        H, n, d = q.shape
+        steps = dq.shape[0]
+        out = np.zeros((steps, H, d))
+        am = np.zeros((steps, H), dtype=np.int64)
+        self._chk(self.lib.ems_ref_engine_decode(_ptr(q), _ptr(k), _ptr(v), _ptr(dq), _ptr(dk), _ptr(dv), H, n, d,
+                                                 steps, c.n_budget, c.l_win, c.tau, c.gamma, c.kernel_size,
+                                                 int(c.zero_class), int(without_pos), rope_base, _ptr(out),
+                                                 _ptr(am, _i64p)), "engine_decode")
+        parts = self.lib.ems_ref_last_json().decode().split("\x1e")
+        pre = [Cache.from_dump_json(parts[2 * h]) for h in range(H)]
+        fin = [Cache.from_dump_json(parts[2 * h + 1]) for h in range(H)]
+        return out, am, pre, fin
 
     def gen_synthetic(self, kind: int, seed: int, tokens: int, heads: int, dim: int,
                       decode_steps: int = 0, level: float = 0.8, perturb: float = 0.05):

@@ -158,6 +158,52 @@ int ems_ref_policy_prefill(int32_t policy, int64_t sink, const double* k_raw, co
     });
 }
 
+// engine::prefill then `steps` decode_step calls (EMS policy, proj/src/engine.cpp:42-210):
+// q/k/v [H][n][d] raw prompt, dq/dk/dv [steps][H][d] raw decode tokens.  Writes
+// out [steps][H][d] and argmax [steps][H]; the json buffer receives, per head, the
+// prefill cache dump then the final cache dump, separated by '\x1e'.
+int ems_ref_engine_decode(const double* q, const double* k, const double* v, const double* dq,
+                          const double* dk, const double* dv, int64_t H, int64_t n, int64_t d,
+                          int64_t steps, int64_t n_budget, int64_t l_win, double tau, double gamma,
+                          int64_t kernel, int32_t zero_class, int32_t without_pos, double rope_base,
+                          double* out, int64_t* argmax) {
+    return guarded([&] {
+        auto cfg = make_config(n_budget, l_win, tau, gamma, kernel, zero_class);
+        if (without_pos) cfg.position_mode = ems::PositionMode::without_pos;
+        ems::EngineState e = ems::make_engine(H, d, ems::PolicyHandle{ems::PolicyKind::ems}, cfg, rope_base);
+        std::vector<ems::Matrix> qb, kb, vb;
+        for (int64_t h = 0; h < H; ++h) {
+            qb.push_back(to_matrix(q + h * n * d, n, d));
+            kb.push_back(to_matrix(k + h * n * d, n, d));
+            vb.push_back(to_matrix(v + h * n * d, n, d));
+        }
+        ems::prefill(e, qb, kb, vb);
+        std::vector<std::string> pre;
+        for (int64_t h = 0; h < H; ++h) pre.push_back(ems::cache_dump_json(e.heads[h]));
+        for (int64_t s = 0; s < steps; ++s) {
+            std::vector<ems::Vector> qs, ks, vs;
+            for (int64_t h = 0; h < H; ++h) {
+                const size_t o = (size_t)(s * H + h) * d;
+                qs.emplace_back(dq + o, dq + o + d);
+                ks.emplace_back(dk + o, dk + o + d);
+                vs.emplace_back(dv + o, dv + o + d);
+            }
+            const ems::DecodeResult r = ems::decode_step(e, qs, ks, vs);
+            for (int64_t h = 0; h < H; ++h) {
+                std::copy(r.per_head[h].begin(), r.per_head[h].end(), out + (size_t)(s * H + h) * d);
+                argmax[s * H + h] = r.argmax_position[h];
+            }
+        }
+        g_json.clear();
+        for (int64_t h = 0; h < H; ++h) {
+            g_json += pre[h];
+            g_json += '\x1e';
+            g_json += ems::cache_dump_json(e.heads[h]);
+            g_json += '\x1e';
+        }
+    });
+}
+
 // The timed composition of the reference arm for one KV
 // unit: per query head prefill_attention in parallel over heads (engine.cpp:65),
 // GQA mean (contract D2), init_score_state, compress_prefill.  q_rot [G][n][d].

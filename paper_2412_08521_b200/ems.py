@@ -58,7 +58,7 @@ class Desc(C.Structure):
                 ("l_win", C.c_int32), ("n_budget", C.c_int32), ("tau", C.c_double),
                 ("gamma", C.c_double), ("kernel_size", C.c_int32), ("zero_class", C.c_int32),
                 ("key_only", C.c_int32), ("score_impl", C.c_int32), ("first_position", C.c_int64),
-                ("policy", C.c_int32), ("sink_count", C.c_int32)]
+                ("policy", C.c_int32), ("sink_count", C.c_int32), ("position_mode", C.c_int32)]
 
 # ems_policy (include/ems_b200.h; PolicyKind, proj/include/ems/policies.hpp:12)
 POLICY = {"ems": 0, "full": 1, "streaming": 2, "h2o": 3, "snapkv": 4}
@@ -78,6 +78,19 @@ class CCache(C.Structure):
 class CStage(C.Structure):
     _fields_ = [(n, C.c_void_p) for n in ("pooled", "cls", "imp_idx", "tbm_idx", "part_counts",
                                           "dest")]
+
+
+class DecodeDims(C.Structure):
+    _fields_ = [("units", C.c_int32), ("slots", C.c_int32), ("locals", C.c_int32), ("lut", C.c_int32),
+                ("rows", C.c_int32)]
+
+
+DECODE_FIELDS = ("slot_key", "slot_norm", "slot_value", "slot_pos", "slot_score", "slot_alive", "local_key",
+                 "local_value", "local_pos", "local_score", "lut_pos", "lut_slot", "meta")
+
+
+class CDecode(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in DECODE_FIELDS]
 
 
 _lib = None
@@ -110,6 +123,13 @@ def lib() -> C.CDLL:
         L.ems_prefill_host.argtypes = [C.POINTER(Desc), C.c_double, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,
                                        fp, fp, fp, C.POINTER(CCache), C.POINTER(CCache), C.c_int32, vp,
                                        C.c_size_t, vp, vp]
+        L.ems_decode_dims_for.argtypes = [C.POINTER(Desc), C.POINTER(DecodeDims)]
+        L.ems_decode_workspace_bytes.restype = C.c_size_t
+        L.ems_decode_workspace_bytes.argtypes = [C.POINTER(Desc)]
+        L.ems_rope_table.argtypes = [C.c_int32, C.c_double, C.c_int32, vp, vp]
+        L.ems_decode_init.argtypes = [C.POINTER(Desc), C.POINTER(CCache), C.POINTER(CDecode), vp]
+        L.ems_decode_step.argtypes = [C.POINTER(Desc), C.c_int64, vp, C.c_int32, vp, vp, vp, vp, vp,
+                                      C.POINTER(CDecode), vp, C.c_size_t, vp]
         L.ems_rope.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_double, C.c_int64, vp, vp,
                                vp]
         L.ems_prefill.argtypes = [C.POINTER(Desc), C.c_double, vp, vp, vp, vp, vp, vp, fp, fp, fp,
@@ -145,6 +165,7 @@ class EmsConfig:
     key_only: bool = False
     policy: str = "ems"      # PolicyHandle::kind: ems | full | streaming | h2o | snapkv
     sink_count: int = 4      # PolicyHandle::sink_count (streaming)
+    position_mode: str = "with_pos"  # decode expansion RoPE (cache.hpp:11): with_pos | without_pos
 
     def center_capacity(self) -> int:
         return self.n_budget - self.l_win
@@ -167,7 +188,8 @@ def make_desc(B: int, Hq: int, Hkv: int, L: int, d: int, dtype: torch.dtype, cfg
         raise InvalidArgument(f"unknown policy: {cfg.policy}")  # policy_kind_from_name, policies.cpp:118-125
     return Desc(B, Hq, Hkv, L, d, _dtype_code(dtype), cfg.l_win, cfg.n_budget, float(cfg.tau),
                 float(cfg.gamma), cfg.kernel_size, int(cfg.zero_class), int(cfg.key_only),
-                SCORE_IMPL[score_impl], first_position, POLICY[cfg.policy], int(cfg.sink_count))
+                SCORE_IMPL[score_impl], first_position, POLICY[cfg.policy], int(cfg.sink_count),
+                {"with_pos": 0, "without_pos": 1}[cfg.position_mode])
 
 
 class Plan:
@@ -422,3 +444,91 @@ def redundancy_cross(k_rows, v_rows, k_cols, v_cols, key_only=False) -> torch.Te
     _check(lib().ems_redundancy_cross(_dtype_code(k_rows.dtype), d, _p(k_rows), _p(v_rows), nr,
                                       _p(k_cols), _p(v_cols), nc, int(key_only), _p(r), _stream()))
     return r
+
+
+class DecodeState:
+    """The EMS decode loop on the device (ems_decode_*): decode_step + decode_update
+    (proj/src/engine.cpp:150-210, proj/src/compressor.cpp:376-398) for every unit of a
+    problem, one CTA per unit per step.  State = fixed-capacity SoA (ems_decode_state)."""
+
+    def __init__(self, B: int, Hq: int, Hkv: int, L: int, d: int, dtype: torch.dtype, cfg: EmsConfig,
+                 rope_base: float, max_positions: int, device=None):
+        self.device = torch.device(device or "cuda")
+        self.desc = make_desc(B, Hq, Hkv, L, d, dtype, cfg)
+        self.dtype, self.cfg = dtype, cfg
+        L_ = lib()
+        dims = DecodeDims()
+        _check(L_.ems_decode_dims_for(C.byref(self.desc), C.byref(dims)))
+        self.dims = dims
+        U, S, W, T = dims.units, dims.slots, dims.locals, dims.lut
+        dev = self.device
+        z = lambda *shape, dt=torch.float32: torch.zeros(shape, dtype=dt, device=dev)  # noqa: E731
+        i32, f64 = torch.int32, torch.float64
+        self.state = dict(slot_key=z(U, S, d), slot_norm=z(U, S), slot_value=z(U, S, d), slot_pos=z(U, S, dt=i32),
+                          slot_score=z(U, S, 3, dt=f64), slot_alive=z(U, S, dt=i32), local_key=z(U, W, d),
+                          local_value=z(U, W, d), local_pos=z(U, W, dt=i32), local_score=z(U, W, 3, dt=f64),
+                          lut_pos=z(U, T, dt=i32), lut_slot=z(U, T, dt=i32), meta=z(U, 8, dt=i32))
+        self._c = CDecode(*[_p(self.state[f]) for f in DECODE_FIELDS])
+        self.max_positions = int(max_positions)
+        self.table = torch.empty((self.max_positions, d // 2, 2), dtype=torch.float32, device=dev)
+        _check(L_.ems_rope_table(d, float(rope_base), self.max_positions, _p(self.table), _stream()))
+        self.workspace = torch.empty(max(L_.ems_decode_workspace_bytes(C.byref(self.desc)), 16), dtype=torch.uint8,
+                                     device=dev)
+        self.out = torch.empty((B, Hq, d), dtype=dtype, device=dev)
+        self.argmax = torch.empty((B, Hq), dtype=torch.int32, device=dev)
+        self.position = L
+
+    def init_from_plan(self, plan: "Plan") -> None:
+        """Decode state from a prefill Plan's compressed cache (ems_decode_init)."""
+        _check(lib().ems_decode_init(C.byref(self.desc), C.byref(plan._ccache), C.byref(self._c), _stream()))
+        self.position = plan.desc.seq_len + plan.desc.first_position
+
+    def load_caches(self, caches, position: int) -> None:
+        """Test helper: state from reference HeadCacheState dumps (oracle.Cache objects with
+        extra['slots'] = the reference slot indices), one per unit; window_fill = 0."""
+        st = {k: v.cpu() for k, v in self.state.items()}
+        for k in st:
+            st[k].zero_()
+        for u, c in enumerate(caches):
+            for j, slot in enumerate(c.extra.get("slots", range(len(c.position)))):
+                st["slot_key"][u, slot] = torch.tensor(c.unit_key[j])
+                st["slot_norm"][u, slot] = float(c.key_norm[j])
+                st["slot_value"][u, slot] = torch.tensor(c.value[j])
+                st["slot_pos"][u, slot] = int(c.position[j])
+                st["slot_score"][u, slot] = torch.tensor(c.score[j], dtype=torch.float64)
+                st["slot_alive"][u, slot] = 1
+            nl = len(c.local_position)
+            st["local_key"][u, :nl] = torch.tensor(c.local_key)
+            st["local_value"][u, :nl] = torch.tensor(c.local_value)
+            st["local_pos"][u, :nl] = torch.tensor(c.local_position, dtype=torch.int32)
+            st["local_score"][u, :nl] = torch.tensor(c.local_score, dtype=torch.float64)
+            nu = len(c.lut_position)
+            st["lut_pos"][u, :nu] = torch.tensor(c.lut_position, dtype=torch.int32)
+            st["lut_slot"][u, :nu] = torch.tensor(c.lut_slot, dtype=torch.int32)
+            st["meta"][u] = torch.tensor([0, nl, nu, 0, int(c.compressed), len(c.position), 0, 0])
+        for k, v in st.items():
+            self.state[k].copy_(v)
+        self.position = position
+
+    def step(self, q, k, v, stream=None):
+        """One decode step: q [B][Hq][d], k/v [B][Hkv][d] raw (device, dtype) -> (out, argmax)."""
+        _check(lib().ems_decode_step(C.byref(self.desc), self.position, _p(self.table), self.max_positions, _p(q),
+                                     _p(k), _p(v), _p(self.out), _p(self.argmax), C.byref(self._c),
+                                     _p(self.workspace), self.workspace.numel(), _stream(stream)))
+        self.position += 1
+        return self.out, self.argmax
+
+    def unit_cache(self, u: int) -> dict:
+        """Host view of unit u's state, shaped like a reference HeadCacheState dump."""
+        st = {k: t[u].cpu() for k, t in self.state.items()}
+        head, nl, nu, wfill, comp, nalive = st["meta"][:6].tolist()
+        W = self.dims.locals
+        alive = [s for s in range(self.dims.slots) if st["slot_alive"][s]]
+        ring = [(head + i) % W for i in range(nl)]
+        return dict(compressed=bool(comp), window_fill=wfill, slots=alive,
+                    position=st["slot_pos"][alive].long().numpy(), unit_key=st["slot_key"][alive].double().numpy(),
+                    key_norm=st["slot_norm"][alive].double().numpy(), value=st["slot_value"][alive].double().numpy(),
+                    score=st["slot_score"][alive].numpy(), local_position=st["local_pos"][ring].long().numpy(),
+                    local_key=st["local_key"][ring].double().numpy(), local_value=st["local_value"][ring].double().numpy(),
+                    local_score=st["local_score"][ring].numpy(), lut_position=st["lut_pos"][:nu].long().numpy(),
+                    lut_slot=st["lut_slot"][:nu].numpy())

@@ -1,0 +1,130 @@
+"""The EMS decode loop on the device against the reference engine itself
+(oracle/_ref: engine::prefill, then decode_step x steps, proj/src/engine.cpp:42-210 with
+decode_update, proj/src/compressor.cpp:376-398).
+
+The device state is loaded from the reference's own prefill caches (slot indices included),
+so every step compares like with like: per-step attention outputs (fp32 keys/values vs the
+reference's fp64: <= 1e-4 relative), argmax positions, and the final caches (centers by
+slot, locals, LUT bit-exact; keys/values/scores within fp32 tolerance).
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+from oracle.oracle import Config  # noqa: E402
+from paper_2412_08521_b200 import ems  # noqa: E402
+
+
+def _run(reflib, H, n, d, steps, c: Config, seed, without_pos=False, rope=1e4):
+    rng = np.random.default_rng(seed)
+    f32 = lambda a: a.astype(np.float32).astype(np.float64)  # noqa: E731  fp32-exact inputs
+    q, k, v = (f32(rng.standard_normal((H, n, d))) for _ in range(3))
+    dq, dk, dv = (f32(rng.standard_normal((steps, H, d))) for _ in range(3))
+    out_ref, am_ref, pre, fin = reflib.engine_decode(q, k, v, dq, dk, dv, c, rope_base=rope, without_pos=without_pos)
+    cfg = ems.EmsConfig(c.n_budget, c.l_win, c.tau, c.gamma, c.kernel_size, c.zero_class,
+                        position_mode="without_pos" if without_pos else "with_pos")
+    ds = ems.DecodeState(1, H, H, n, d, torch.float32, cfg, rope, n + steps)
+    ds.load_caches(pre, position=n)
+    T = lambda a: torch.tensor(a, dtype=torch.float32, device="cuda").reshape(1, H, d).contiguous()  # noqa: E731
+    outs, ams = [], []
+    for s in range(steps):
+        o, a = ds.step(T(dq[s]), T(dk[s]), T(dv[s]))
+        outs.append(o[0].double().cpu().numpy())
+        ams.append(a[0].long().cpu().numpy())
+    return np.stack(outs), np.stack(ams), out_ref, am_ref, fin, ds
+
+
+def _check(outs, ams, out_ref, am_ref, fin, ds, H):
+    err = np.linalg.norm(outs - out_ref, axis=-1) / np.maximum(np.linalg.norm(out_ref, axis=-1), 1e-30)
+    assert err.max() < 1e-4, f"decode output rel err {err.max()}"
+    assert (ams != am_ref).mean() <= 0.01, f"argmax mismatches {(ams != am_ref).sum()}"
+    for h in range(H):
+        got, want = ds.unit_cache(h), fin[h]
+        assert got["compressed"] == want.compressed
+        assert got["slots"] == list(want.extra["slots"]), "live center slots differ"
+        np.testing.assert_array_equal(got["position"], want.position)
+        np.testing.assert_array_equal(got["local_position"], want.local_position)
+        np.testing.assert_array_equal(got["lut_position"], want.lut_position)
+        np.testing.assert_array_equal(got["lut_slot"], want.lut_slot)
+        np.testing.assert_allclose(got["unit_key"], want.unit_key, atol=2e-5)
+        np.testing.assert_allclose(got["value"], want.value, rtol=1e-4, atol=2e-5)
+        np.testing.assert_allclose(got["key_norm"], want.key_norm, rtol=1e-5)
+        np.testing.assert_allclose(got["score"], want.score, rtol=1e-4, atol=1e-7)
+        np.testing.assert_allclose(got["local_score"], want.local_score, rtol=1e-4, atol=1e-7)
+
+
+@pytest.mark.parametrize("tau,zero_class,without_pos", [(0.3, True, False), (0.0, True, False),
+                                                       (0.6, False, False), (0.3, True, True)])
+def test_decode_matches_reference(reflib, tau, zero_class, without_pos):
+    c = Config(n_budget=24, l_win=4, tau=tau, gamma=2.0, kernel_size=3, zero_class=zero_class)
+    outs, ams, out_ref, am_ref, fin, ds = _run(reflib, 3, 100, 16, 40, c, seed=5, without_pos=without_pos)
+    _check(outs, ams, out_ref, am_ref, fin, ds, 3)
+
+
+def test_decode_after_keep_all_prefill(reflib):
+    """Prompt shorter than the budget: the first decode steps graduate the whole prompt."""
+    c = Config(n_budget=24, l_win=4, tau=0.2, gamma=2.0, kernel_size=3)
+    outs, ams, out_ref, am_ref, fin, ds = _run(reflib, 2, 20, 32, 30, c, seed=9)
+    _check(outs, ams, out_ref, am_ref, fin, ds, 2)
+
+
+def test_decode_window_rotation_and_long_run(reflib):
+    """More steps than several score windows; LUT at capacity (oldest zero-mapped entry drops)."""
+    c = Config(n_budget=16, l_win=4, tau=0.5, gamma=1.5, kernel_size=3)
+    outs, ams, out_ref, am_ref, fin, ds = _run(reflib, 2, 64, 16, 120, c, seed=13)
+    _check(outs, ams, out_ref, am_ref, fin, ds, 2)
+
+
+def test_decode_gqa_identical_heads_equal_single_head():
+    """GQA (contract D2): G identical query heads give the G = 1 result."""
+    rng = np.random.default_rng(2)
+    n, d, steps = 200, 64, 10
+    cfg = ems.EmsConfig(n_budget=48, l_win=8, tau=0.3, gamma=2.0, kernel_size=3)
+    q = torch.tensor(rng.standard_normal((1, 1, n, d)), dtype=torch.float32, device="cuda")
+    k = torch.tensor(rng.standard_normal((1, 1, n, d)), dtype=torch.float32, device="cuda")
+    v = torch.tensor(rng.standard_normal((1, 1, n, d)), dtype=torch.float32, device="cuda")
+    p1 = ems.prefill(q, k, v, cfg, 1e4)
+    p2 = ems.prefill(q.repeat(1, 2, 1, 1).contiguous(), k, v, cfg, 1e4)
+    d1 = ems.DecodeState(1, 1, 1, n, d, torch.float32, cfg, 1e4, n + steps)
+    d2 = ems.DecodeState(1, 2, 1, n, d, torch.float32, cfg, 1e4, n + steps)
+    d1.init_from_plan(p1)
+    d2.init_from_plan(p2)
+    for s in range(steps):
+        dq = torch.tensor(rng.standard_normal((1, 1, d)), dtype=torch.float32, device="cuda")
+        dk = torch.tensor(rng.standard_normal((1, 1, d)), dtype=torch.float32, device="cuda")
+        dv = torch.tensor(rng.standard_normal((1, 1, d)), dtype=torch.float32, device="cuda")
+        o1, a1 = d1.step(dq, dk, dv)
+        o2, a2 = d2.step(dq.repeat(1, 2, 1).contiguous(), dk, dv)
+        torch.testing.assert_close(o2[:, 0], o1[:, 0], rtol=1e-5, atol=1e-6)
+        torch.testing.assert_close(o2[:, 1], o1[:, 0], rtol=1e-5, atol=1e-6)
+        assert torch.equal(a2[:, 0], a1[:, 0])
+    c1, c2 = d1.unit_cache(0), d2.unit_cache(0)
+    np.testing.assert_array_equal(c1["lut_position"], c2["lut_position"])
+    np.testing.assert_array_equal(c1["lut_slot"], c2["lut_slot"])
+
+
+def test_decode_from_device_prefill_bf16_deterministic():
+    """ems_prefill (bf16, RoPE on device) -> ems_decode_init -> steps; two runs bit-identical."""
+    rng = np.random.default_rng(4)
+    B, H, G, n, d, steps = 2, 2, 4, 512, 128, 12
+    cfg = ems.EmsConfig(n_budget=64, l_win=8, tau=0.3, gamma=3.0, kernel_size=5)
+    t = lambda *s: torch.tensor(rng.standard_normal(s), dtype=torch.float32).to(torch.bfloat16).cuda()  # noqa: E731
+    q, k, v = t(B, H * G, n, d), t(B, H, n, d), t(B, H, n, d)
+    dqs = [(t(B, H * G, d), t(B, H, d), t(B, H, d)) for _ in range(steps)]
+    res = []
+    for _ in range(2):
+        plan = ems.prefill(q, k, v, cfg, 5e5)
+        ds = ems.DecodeState(B, H * G, H, n, d, torch.bfloat16, cfg, 5e5, n + steps)
+        ds.init_from_plan(plan)
+        outs = [ds.step(*x)[0].clone() for x in dqs]
+        res.append((outs, {kk: vv.clone() for kk, vv in ds.state.items()}))
+    for a, b in zip(res[0][0], res[1][0]):
+        assert torch.equal(a, b)
+    for kk in res[0][1]:
+        assert torch.equal(res[0][1][kk], res[1][1][kk]), kk
+    meta = res[0][1]["meta"].cpu()
+    assert (meta[:, 1] == cfg.l_win).all()            # locals back at the window size
+    assert (meta[:, 5] == cfg.n_budget - cfg.l_win).all()  # centers at capacity
