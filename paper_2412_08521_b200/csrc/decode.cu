@@ -142,8 +142,8 @@ __global__ void __launch_bounds__(kT) decode_step_kernel(DecArgs a) {
     extern __shared__ __align__(16) unsigned char dsm[];
     const int u = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int d = a.d, S = a.S, W = a.W, T = a.T, G = a.G, pairs = d / 2;
-    double* acc = reinterpret_cast<double*>(dsm);                  // [S + W] owner mass / R values
-    float* qrot = reinterpret_cast<float*>(acc + (S + W));          // [G][d]
+    double* acc = reinterpret_cast<double*>(dsm);                  // [max(S + W, 8 d)] owner mass / R / partials
+    float* qrot = reinterpret_cast<float*>(acc + max(S + W, kWarps * d));  // [G][d]
     __shared__ double shd[kWarps];
     __shared__ float shf[kWarps];
     __shared__ Cand shc[kWarps];
@@ -259,17 +259,36 @@ __global__ void __launch_bounds__(kT) decode_step_kernel(DecArgs a) {
         for (int r = tid; r < n_rows; r += kT) ph[r] = (float)((double)expf(ph[r] - m) / z);
         __syncthreads();
     }
-    // 6. outputs (weighted_value_sum, fp64, rows in order) and 7. argmax positions
-    for (int x = tid; x < G * d; x += kT) {
-        const int h = x / d, i = x % d;
-        const float* ph = prob + (size_t)h * a.R;
-        double o = 0.0;
-        for (int r = 0; r < n_rows; ++r) {
-            const int ow = rown[r];
-            const float val = ow < S ? sval[(size_t)ow * d + i] : lval[(size_t)(ow - S) * d + i];
-            o += (double)ph[r] * (double)val;
+    // 6. outputs (weighted_value_sum in fp64): warp w sums a contiguous block of rows (in
+    //    order) for every head, lanes over d; the 8 warp partials combine in warp order.
+    {
+        const int per = (n_rows + kWarps - 1) / kWarps;
+        const int r0 = min(n_rows, warp * per), r1 = min(n_rows, r0 + per);
+        const int epl = (d + 31) / 32;  // elements per lane (d <= 128 -> <= 4)
+        double* part = acc;              // [kWarps][d] for one head at a time (acc is free here)
+        for (int h = 0; h < G; ++h) {
+            const float* ph = prob + (size_t)h * a.R;
+            double o[4] = {0.0, 0.0, 0.0, 0.0};
+            for (int r = r0; r < r1; ++r) {
+                const int ow = rown[r];
+                const float* vr = ow < S ? sval + (size_t)ow * d : lval + (size_t)(ow - S) * d;
+                const double p = (double)ph[r];
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    if (e < epl && lane * epl + e < d) o[e] += p * (double)vr[lane * epl + e];
+            }
+            __syncthreads();
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                if (e < epl && lane * epl + e < d) part[warp * d + lane * epl + e] = o[e];
+            __syncthreads();
+            for (int i = tid; i < d; i += kT) {
+                double t = 0.0;
+                for (int w2 = 0; w2 < kWarps; ++w2) t += part[w2 * d + i];
+                stx(a.out, ((size_t)u * G + h) * d + i, a.dtype, t);
+            }
         }
-        stx(a.out, ((size_t)u * G + h) * d + i, a.dtype, o);
+        __syncthreads();
     }
     for (int h = 0; h < G; ++h) {
         const float* ph = prob + (size_t)h * a.R;
@@ -621,7 +640,7 @@ cudaError_t launch_decode_step(const Dims& m, int dtype, int S, int W, int T, in
     a.row_pos = reinterpret_cast<int32_t*>(take(U * R * 4));
     a.probs = reinterpret_cast<float*>(take(U * m.G * R * 4));
     a.pmean = reinterpret_cast<float*>(take(U * R * 4));
-    const size_t smem = (size_t)(S + W) * 8 + (size_t)m.G * m.d * 4;
+    const size_t smem = (size_t)max(S + W, kWarps * m.d) * 8 + (size_t)m.G * m.d * 4;
     static size_t attr = 0;
     if (smem > 48 * 1024 && smem > attr) {
         cudaFuncSetAttribute(decode_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -1,4 +1,4 @@
-for rep in 1 2; do
-EMS_P2_UNIT_MAJOR=0 EMS_P2_HSPLIT=1 python tools/energy.py --steps 150
-EMS_P2_UNIT_MAJOR=1 EMS_P2_HSPLIT=2 python tools/energy.py --steps 150
-done
+python -m pytest tests/test_gpu_decode.py -x -q 2>&1 | tail -2
+python tools/bench_decode.py --config cfg3
+python tools/bench_decode.py --config cfg4 --batch 32
+python tools/bench_decode.py --config cfg5 --seq-len 32768
