@@ -1,0 +1,430 @@
+// fwd2_tc.cu -- (P1, CTA-pair variant) causal FlashAttention forward on cta_group::2 with
+// 256-key tiles: O, row LSE.  Reference semantics: streaming_pass, proj/src/scoring.cpp:20-64.
+//
+// A cluster of two CTAs owns 256 query rows: the same query tile of two heads of a GQA
+// group (G >= 2) or query tiles 2p, 2p+1 of one head (G == 1); CTA r holds its 128 rows.
+// The leader issues, per 256-key tile j,
+//   S_j  = Q K_j^T        tcgen05.mma.cta_group::2, M = 256, N = 256, K = 128 (SS): each CTA
+//                          supplies its 128 query rows (A) and one 128-key half of K_j (B)
+//   O   += P_j V_j        M = 256, N = 128, K = 256 (TS: P from TMEM): each CTA supplies its
+//                          P rows and a 64-column half of V_j (B, MN-major)
+// so every instruction is a 256 x 256 / 256 x 128 tile (the 2-SM rates, ~92% / ~69% of peak,
+// against ~60% / ~69% for the single-CTA N = 128 instructions of fwd_tc_kernel) at the same
+// K/V bytes per FLOP.  TMEM per CTA: S [0,256) | P (bf16) [256,384) | O [384,512): P has its own
+// columns, so S_{j+1} is issued as soon as both CTAs have read S_j into registers and runs
+// under the softmax of tile j; PV_j follows once P_j is stored.  Softmax: four warpgroups per
+// CTA, thread = (row, 64 keys); row maxima exchanged through shared memory; lazily updated
+// reference max (O rescaled only when a row max grows by > 8 in log2 units).
+#include <cuda.h>
+#include <stdlib.h>
+
+#include "score_tc.cuh"
+
+namespace ems {
+
+namespace {
+
+using namespace tc;
+using namespace sc;
+
+constexpr float kRescale2 = 8.0f;
+// A tile whose logits provably stay below m_ref + kSkip (|q.k| <= |q| max|k|) needs neither its
+// row max nor the max exchange: its p = 2^(s c - m_ref) <= 2^kSkip cannot overflow fp32/bf16.
+constexpr float kSkip = 64.0f;
+constexpr int kT2 = 576;  // w0 TMA, w1 MMA (leader), w2-17 softmax (warpgroup q = keys [64q, 64q+64))
+constexpr int kStages2 = 2;
+// Q 32 KB | K stages (this CTA's 128-key half) | V stages (256 keys x this CTA's 64 d cols)
+constexpr size_t kSmem2 = 1024 + kTileBytes + 2 * kStages2 * kTileBytes + 2 * 4 * 128 * 4;
+
+struct Fwd2Args {
+    int L, Hq, Hkv, G, nT, units;
+    float c;
+    __nv_bfloat16* out;
+    float* nlse2;
+    float* lse_nat;
+    int debug;  // profiling only: 1 = no softmax math (P = 0), 2 = no MMAs
+    const float* kmax;  // [units][nT2] max ||k|| over each 256-key tile (Cauchy-Schwarz bound)
+    int nT2;
+};
+
+struct Bars2 {
+    uint64_t q_full;
+    uint64_t k_full[kStages2], v_full[kStages2];    // leader: both halves landed
+    uint64_t k_empty[kStages2], v_empty[kStages2];  // local (multicast commit)
+    uint64_t s_full, o_full;                        // local (multicast commit)
+    uint64_t s_free, p_full;                        // leader: 32 warp arrivals (16 per CTA)
+    uint32_t tmem_base;
+};
+
+__device__ __forceinline__ void pair_item(const Fwd2Args& a, int pair, int rank, int& plane, int& tile,
+                                          int& unit, int& jmax) {
+    if (a.G >= 2) {  // unit by unit, heaviest query tiles first; CTA r takes head 2 hp + r
+        const int hps = a.G / 2;
+        const int per_unit = a.nT * hps;
+        unit = pair / per_unit;
+        const int r = pair % per_unit;
+        tile = a.nT - 1 - r / hps;
+        const int hp = r % hps;
+        const int b = unit / a.Hkv, hk = unit % a.Hkv;
+        plane = b * a.Hq + hk * a.G + 2 * hp + rank;
+    } else {  // query tiles 2p, 2p+1 of one head
+        const int np = a.nT / 2;
+        unit = pair / np;
+        const int p = np - 1 - pair % np;
+        const int b = unit / a.Hkv, hk = unit % a.Hkv;
+        plane = b * a.Hq + hk;
+        tile = 2 * p + rank;
+    }
+    // 256-key tiles 0 .. jmax cover every key <= the last query row of both CTAs
+    jmax = (a.G >= 2 ? tile : (tile | 1)) / 2;
+}
+
+template <int kPoly>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT2, 1)
+    fwd2_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
+                   const __grid_constant__ CUtensorMap tv, const Fwd2Args a) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sq = sm;                                   // 32 KB: this CTA's 128 query rows
+    uint8_t* sk = sq + kTileBytes;                      // stages x 32 KB: 128 keys x 128 d
+    uint8_t* sv = sk + kStages2 * kTileBytes;           // stages x 32 KB: 256 keys x 64 d
+    float* xch = reinterpret_cast<float*>(sv + kStages2 * kTileBytes);  // [2 buf][4 quarters][128]
+    __shared__ Bars2 bars;
+
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const uint32_t rank = cluster_ctarank();
+    int plane, tile, unit, jmax;
+    pair_item(a, blockIdx.x >> 1, (int)rank, plane, tile, unit, jmax);
+
+    if (warp == 0) {
+        tmem_alloc_2sm<512>(&bars.tmem_base);
+    } else if (warp == 1 && elect_one()) {
+        mbar_init(&bars.q_full, 1);
+        for (int s = 0; s < kStages2; ++s) {
+            mbar_init(&bars.k_full[s], 1);
+            mbar_init(&bars.v_full[s], 1);
+            mbar_init(&bars.k_empty[s], 1);
+            mbar_init(&bars.v_empty[s], 1);
+        }
+        mbar_init(&bars.s_full, 1);
+        mbar_init(&bars.o_full, 1);
+        mbar_init(&bars.s_free, 32);
+        mbar_init(&bars.p_full, 32);
+        fence_barrier_init();
+    }
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem = bars.tmem_base;
+    const uint32_t tS = tmem, tP = tmem + 256, tO = tmem + 384;
+
+    if (warp == 0) {
+        // ---------------------------------------------------------------- TMA (both CTAs)
+        if (elect_one()) {
+            tma_prefetch(&tq);
+            tma_prefetch(&tk);
+            tma_prefetch(&tv);
+            if (rank == 0) mbar_expect_tx(&bars.q_full, 2 * kTileBytes);
+            tma_load_3d_2sm(sq, &tq, &bars.q_full, 0, tile * kTile, plane);
+            tma_load_3d_2sm(sq + 16384, &tq, &bars.q_full, 64, tile * kTile, plane);
+            for (int j = 0; j <= jmax; ++j) {
+                const int s = j % kStages2;
+                const uint32_t ph = ((j / kStages2) - 1) & 1;
+                if (j >= kStages2) mbar_wait(&bars.k_empty[s], ph);
+                if (rank == 0) mbar_expect_tx(&bars.k_full[s], 2 * kTileBytes);
+                uint8_t* dk = sk + s * kTileBytes;
+                const int krow = 2 * j * kTile + (int)rank * kTile;  // this CTA's 128-key half
+                tma_load_3d_2sm(dk, &tk, &bars.k_full[s], 0, krow, unit);
+                tma_load_3d_2sm(dk + 16384, &tk, &bars.k_full[s], 64, krow, unit);
+                if (j >= kStages2) mbar_wait(&bars.v_empty[s], ph);
+                if (rank == 0) mbar_expect_tx(&bars.v_full[s], 2 * kTileBytes);
+                uint8_t* dv = sv + s * kTileBytes;  // keys 256j .. +255, d cols 64 rank .. +63
+                tma_load_3d_2sm(dv, &tv, &bars.v_full[s], 64 * (int)rank, 2 * j * kTile, unit);
+                tma_load_3d_2sm(dv + 16384, &tv, &bars.v_full[s], 64 * (int)rank, 2 * j * kTile + kTile, unit);
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------------------------------------------------------- MMA (leader only)
+        if (rank == 0 && elect_one()) {
+            const uint32_t id_s = idesc_bf16(256, 256, 0, 0);  // Q (K-major) x K^T (K-major)
+            const uint32_t id_o = idesc_bf16(256, 128, 0, 1);  // P (TMEM) x V (MN-major)
+            const uint32_t qa = smem_u32(sq);
+            auto issue_s = [&](int j) {
+                const uint32_t ka = smem_u32(sk + (j % kStages2) * kTileBytes);
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    if (a.debug != 2) mma_ss_2sm(tS, sdesc(kmajor_addr(qa, k), 16, 1024), sdesc(kmajor_addr(ka, k), 16, 1024), id_s,
+                               k > 0);
+                mma_commit_2sm(&bars.s_full, 0x3);
+                mma_commit_2sm(&bars.k_empty[j % kStages2], 0x3);
+            };
+            mbar_wait(&bars.q_full, 0);
+            mbar_wait(&bars.k_full[0], 0);
+            tc_fence_after();
+            issue_s(0);
+            for (int j = 0; j <= jmax; ++j) {
+                if (j + 1 <= jmax) {
+                    mbar_wait(&bars.s_free, j & 1);  // both CTAs hold S_j in registers
+                    mbar_wait(&bars.k_full[(j + 1) % kStages2], ((j + 1) / kStages2) & 1);
+                    tc_fence_after();
+                    issue_s(j + 1);
+                }
+                mbar_wait(&bars.p_full, j & 1);
+                mbar_wait(&bars.v_full[j % kStages2], (j / kStages2) & 1);
+                tc_fence_after();
+                const uint32_t va = smem_u32(sv + (j % kStages2) * kTileBytes);
+#pragma unroll
+                for (int k = 0; k < 16; ++k)
+                    if (a.debug != 2) mma_ts_2sm(tO, tP + k * 8, sdesc(va + k * 2048, 16384, 1024), id_o, (j > 0 || k > 0) ? 1u : 0u);
+                mma_commit_2sm(&bars.o_full, 0x3);
+                mma_commit_2sm(&bars.v_empty[j % kStages2], 0x3);
+            }
+        }
+    } else {
+        // ---------------------------------------------------------------- softmax
+        const int q = (warp - 2) >> 2;          // key quarter: columns [64q, 64q + 64) of S
+        const int wi = warp & 3;
+        const int m = wi * 32 + (tid & 31);     // row within the CTA's tile
+        const int qrow = tile * kTile + m;       // query position
+        const uint32_t lane_off = (uint32_t)(wi * 32) << 16;
+        const uint32_t sS = tS + lane_off + 64 * q;
+        const uint32_t sP = tP + lane_off + 32 * q;
+        const uint32_t sO = tO + lane_off + 32 * q;
+        const uint32_t s_free_l = mapa(smem_u32(&bars.s_free), 0);
+        const uint32_t p_full_l = mapa(smem_u32(&bars.p_full), 0);
+        float m_ref = -INFINITY, l = 0.f, qn = 0.f;
+        int n_x = 0;  // max exchanges so far (selects the xch buffer; identical across a row's quarters)
+        for (int j = 0; j <= jmax; ++j) {
+            mbar_wait(&bars.s_full, j & 1);
+            tc_fence_after();
+            if (j == 0) {  // |q_row| from the (swizzled) smem tile: the norm is order-free
+                float ss = 0.f;
+#pragma unroll
+                for (int bx = 0; bx < 2; ++bx)
+#pragma unroll
+                    for (int ch = 0; ch < 8; ++ch) {
+                        const float4 w4 = lds128(smem_u32(sq + bx * 16384 + m * 128 + ch * 16));
+                        const uint32_t wv[4] = {__float_as_uint(w4.x), __float_as_uint(w4.y), __float_as_uint(w4.z),
+                                                __float_as_uint(w4.w)};
+#pragma unroll
+                        for (int t = 0; t < 4; ++t) {
+                            const float lo = __uint_as_float(wv[t] << 16), hi = __uint_as_float(wv[t] & 0xFFFF0000u);
+                            ss = fmaf(lo, lo, fmaf(hi, hi, ss));
+                        }
+                    }
+                qn = sqrtf(ss) * 1.0001f;  // rounding margin
+            }
+            uint32_t r[2][32];
+            tmem_ld32(sS, r[0]);
+            tmem_ld32(sS + 32, r[1]);
+            tmem_ld_wait();
+            tc_fence_before();
+            __syncwarp();
+            if ((tid & 31) == 0) mbar_arrive_cluster(s_free_l);  // S_j may be overwritten
+            if (a.debug == 1) {  // profiling: skip the softmax math
+                uint32_t z[16] = {};
+                if (j > 0) mbar_wait(&bars.o_full, (j - 1) & 1);
+                tc_fence_after();
+                tmem_st16(sP, z);
+                tmem_st16(sP + 16, z);
+                tmem_st_wait();
+                tc_fence_before();
+                __syncwarp();
+                if ((tid & 31) == 0) mbar_arrive_cluster(p_full_l);
+                l = 1.f;
+                m_ref = 0.f;
+                continue;
+            }
+            const int key0 = 2 * j * kTile + 64 * q;
+            if (key0 + 63 > qrow) {  // causal mask near the diagonal
+#pragma unroll
+                for (int c = 0; c < 2; ++c)
+#pragma unroll
+                    for (int x = 0; x < 32; ++x)
+                        if (key0 + c * 32 + x > qrow) r[c][x] = __float_as_uint(-INFINITY);
+            }
+            // warp-uniform (the exchange below is a named barrier); the four warps sharing these rows
+            // see the same rows, hence the same vote
+            const bool skip =
+                __all_sync(0xffffffffu, j > 0 && qn * a.kmax[(size_t)unit * a.nT2 + j] * a.c <= m_ref + kSkip);
+            float corr = 1.f;
+            bool warp_need = false;
+            if (!skip) {
+            float hmv[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+            for (int c = 0; c < 2; ++c)
+#pragma unroll
+                for (int x = 0; x < 32; x += 8)
+#pragma unroll
+                    for (int g = 0; g < 4; g += 2) {
+                        hmv[g] = fmax3(hmv[g], __uint_as_float(r[c][x + 2 * g]), __uint_as_float(r[c][x + 2 * g + 1]));
+                        hmv[g + 1] = fmax3(hmv[g + 1], __uint_as_float(r[c][x + 2 * g + 2]),
+                                           __uint_as_float(r[c][x + 2 * g + 3]));
+                    }
+            const float hm = fmax3(hmv[0], hmv[1], fmaxf(hmv[2], hmv[3]));
+            float* xb = xch + (n_x++ & 1) * 512;
+            const uint32_t xs = smem_u32(xb);
+            sts32(xs + 4 * (q * 128 + m), hm);
+            asm volatile("bar.sync %0, 128;" ::"r"(1 + wi) : "memory");  // the 4 warps sharing these rows
+            const float4 o4 = make_float4(lds32(xs + 4 * m), lds32(xs + 4 * (128 + m)), lds32(xs + 4 * (256 + m)),
+                                          lds32(xs + 4 * (384 + m)));
+            const float mx = fmax3(o4.x, o4.y, fmaxf(o4.z, o4.w));
+            const float mx2 = mx * a.c;
+            const bool need = mx2 > m_ref + kRescale2;
+            warp_need = __any_sync(0xffffffffu, need);
+            const float new_m = need ? mx2 : m_ref;
+            corr = need ? ex2(m_ref - new_m) : 1.f;
+            m_ref = new_m;
+            l *= corr;
+            }
+            const float2 c2 = make_float2(a.c, a.c), nm2 = make_float2(-m_ref, -m_ref);
+            float2 rs2 = make_float2(0.f, 0.f);
+            uint32_t pk[2][16];
+#pragma unroll
+            for (int c = 0; c < 2; ++c)
+#pragma unroll
+                for (int x = 0; x < 16; ++x) {
+                    const float2 arg = __ffma2_rn(
+                        make_float2(__uint_as_float(r[c][2 * x]), __uint_as_float(r[c][2 * x + 1])), c2, nm2);
+                    const float2 p = (x & 7) < kPoly ? ex2_poly2(arg) : make_float2(ex2(arg.x), ex2(arg.y));
+                    rs2 = __fadd2_rn(rs2, p);
+                    pk[c][x] = pack_bf16(p.x, p.y);
+                }
+            l += rs2.x + rs2.y;
+            if (j > 0) {  // P region free and O stable once PV_{j-1} is done
+                mbar_wait(&bars.o_full, (j - 1) & 1);
+                tc_fence_after();
+                if (warp_need) {  // rescale this quarter of O (rare)
+                    uint32_t o[32];
+                    tmem_ld32(sO, o);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int x = 0; x < 32; ++x) o[x] = __float_as_uint(__uint_as_float(o[x]) * corr);
+                    tmem_st32(sO, o);
+                }
+            }
+            tmem_st16(sP, pk[0]);
+            tmem_st16(sP + 16, pk[1]);
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if ((tid & 31) == 0) mbar_arrive_cluster(p_full_l);
+        }
+        // epilogue: l = sum of the four quarters (fixed order), O / l -> bf16, LSE
+        float* xb = xch + (n_x & 1) * 512;
+        const uint32_t xs = smem_u32(xb);
+        sts32(xs + 4 * (q * 128 + m), l);
+        asm volatile("bar.sync %0, 128;" ::"r"(1 + wi) : "memory");  // the 4 warps sharing these rows
+        const float lt = ((lds32(xs + 4 * m) + lds32(xs + 4 * (128 + m))) + lds32(xs + 4 * (256 + m))) +
+                         lds32(xs + 4 * (384 + m));
+        mbar_wait(&bars.o_full, jmax & 1);
+        tc_fence_after();
+        const size_t row = (size_t)plane * a.L + qrow;
+        const float inv = 1.f / lt;
+        if (a.out) {
+            uint32_t o[32];
+            tmem_ld32(sO, o);
+            tmem_ld_wait();
+            uint4* dst = reinterpret_cast<uint4*>(a.out + row * kD + 32 * q);
+#pragma unroll
+            for (int x = 0; x < 4; ++x) {
+                uint4 v;
+                v.x = pack_bf16(__uint_as_float(o[8 * x + 0]) * inv, __uint_as_float(o[8 * x + 1]) * inv);
+                v.y = pack_bf16(__uint_as_float(o[8 * x + 2]) * inv, __uint_as_float(o[8 * x + 3]) * inv);
+                v.z = pack_bf16(__uint_as_float(o[8 * x + 4]) * inv, __uint_as_float(o[8 * x + 5]) * inv);
+                v.w = pack_bf16(__uint_as_float(o[8 * x + 6]) * inv, __uint_as_float(o[8 * x + 7]) * inv);
+                dst[x] = v;
+            }
+        }
+        if (q == 0) {
+            const float lse2 = m_ref + __log2f(lt);
+            a.nlse2[row] = -lse2;
+            if (a.lse_nat) a.lse_nat[row] = lse2 * kLn2;
+        }
+    }
+    tc_fence_before();
+    cluster_sync();
+    if (warp == 0) tmem_dealloc_2sm<512>(tmem);
+}
+
+// max ||k|| over each 256-key tile of each unit (fp32): the per-tile logit bound of fwd2
+__global__ void key_tile_norm_kernel(const __nv_bfloat16* __restrict__ k, int L, int nT2, float* __restrict__ kmax) {
+    __shared__ float sh[8];
+    const int t = blockIdx.x % nT2, u = blockIdx.x / nT2;
+    const int key = t * 256 + threadIdx.x;
+    float ss = 0.f;
+    if (key < L) {
+        const uint4* row = reinterpret_cast<const uint4*>(k + ((size_t)u * L + key) * kD);
+#pragma unroll
+        for (int c = 0; c < kD / 8; ++c) {
+            const uint4 w = row[c];
+            const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+            for (int x = 0; x < 4; ++x) {
+                const float lo = __uint_as_float(wv[x] << 16), hi = __uint_as_float(wv[x] & 0xFFFF0000u);
+                ss = fmaf(lo, lo, fmaf(hi, hi, ss));
+            }
+        }
+    }
+    float n = sqrtf(ss);
+    n = warp_max(n);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = n;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float mx = sh[0];
+        for (int i = 1; i < 8; ++i) mx = fmaxf(mx, sh[i]);
+        kmax[blockIdx.x] = mx * 1.0001f;
+    }
+}
+
+}  // namespace
+
+size_t fwd2_workspace(int units, int L) { return sizeof(float) * (size_t)units * ((L + 255) / 256); }
+
+bool fwd2_tc_supported(int G, int nT) { return (G >= 2 && G % 2 == 0) || (G == 1 && nT % 2 == 0); }
+
+cudaError_t launch_fwd2_tc(int L, int Hq, int Hkv, int G, int units, float c, void* out, float* nlse2,
+                           float* lse_nat, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+                           const void* k, float* kmax, cudaStream_t s) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(fwd2_tc_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem2);
+        cudaFuncSetAttribute(fwd2_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem2);
+        cudaFuncSetAttribute(fwd2_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem2);
+        cudaFuncSetAttribute(fwd2_tc_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem2);
+        attr = true;
+    }
+    static const int poly = [] {  // pairs (of every 8) whose exp2 runs on the FMA pipe
+        const char* e = getenv("EMS_P1_POLY");
+        return e ? atoi(e) : 2;
+    }();
+    Fwd2Args a;
+    a.L = L;
+    a.Hq = Hq;
+    a.Hkv = Hkv;
+    a.G = G;
+    a.nT = L / kTile;
+    a.units = units;
+    a.c = c;
+    a.out = static_cast<__nv_bfloat16*>(out);
+    a.nlse2 = nlse2;
+    a.lse_nat = lse_nat;
+    static const int dbg = [] {
+        const char* e = getenv("EMS_P1_DEBUG");
+        return e ? atoi(e) : 0;
+    }();
+    a.debug = dbg;
+    a.nT2 = (L + 255) / 256;
+    a.kmax = kmax;
+    key_tile_norm_kernel<<<units * a.nT2, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(k), L, a.nT2, kmax);
+    const int pairs = G >= 2 ? a.nT * units * (G / 2) : (a.nT / 2) * units;
+    switch (poly) {
+        case 1: fwd2_tc_kernel<1><<<2 * pairs, kT2, kSmem2, s>>>(tq, tk, tv, a); break;
+        case 2: fwd2_tc_kernel<2><<<2 * pairs, kT2, kSmem2, s>>>(tq, tk, tv, a); break;
+        case 3: fwd2_tc_kernel<3><<<2 * pairs, kT2, kSmem2, s>>>(tq, tk, tv, a); break;
+        default: fwd2_tc_kernel<0><<<2 * pairs, kT2, kSmem2, s>>>(tq, tk, tv, a); break;
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace ems

@@ -374,9 +374,12 @@ bool score_tc_supported(const Dims& dm, int dtype) {
 static size_t nlse2_bytes(const Dims& dm) {
     return (sizeof(float) * (size_t)dm.B * dm.Hq * dm.L + 255) / 256 * 256;
 }
-size_t score_tc_workspace(const Dims& dm) {
+static size_t part_bytes(const Dims& dm) {
     const int hs = colsum_hsplit(dm.G, dm.L / kTile, dm.units);
-    return nlse2_bytes(dm) + (hs > 1 ? 2 * sizeof(double) * (size_t)dm.units * hs * dm.L : 0);
+    return hs > 1 ? 2 * sizeof(double) * (size_t)dm.units * hs * dm.L : 0;
+}
+size_t score_tc_workspace(const Dims& dm) {
+    return nlse2_bytes(dm) + part_bytes(dm) + (fwd2_workspace(dm.units, dm.L) + 255) / 256 * 256;
 }
 
 cudaError_t score_tc(const Dims& dm, const void* q, const void* k, const void* v, void* o,
@@ -410,6 +413,18 @@ cudaError_t score_tc(const Dims& dm, const void* q, const void* k, const void* v
         const char* e = getenv("EMS_P1_POLY");
         return e ? atoi(e) : 0;
     }();
+    // P1 variant: 2 = CTA-pair kernel with 256-key tiles (fwd2_tc.cu, default: 4% faster and
+    // 3% less energy per step on config 3), 1 = the single-CTA two-slot kernel above
+    static const int p1 = [] {
+        const char* e = getenv("EMS_P1_IMPL");
+        return e ? atoi(e) : 2;
+    }();
+    if (p1 == 2 && fwd2_tc_supported(dm.G, fa.nT)) {
+        float* kmax = reinterpret_cast<float*>(static_cast<char*>(ws) + nlse2_bytes(dm) + part_bytes(dm));
+        cudaError_t e = launch_fwd2_tc(dm.L, dm.Hq, dm.Hkv, dm.G, dm.units, fa.c, o, nlse2, lse, tq, tk, tv, k,
+                                       kmax, s);
+        if (e != cudaSuccess) return e;
+    } else
     switch (poly) {
         case 1: fwd_launch<1>(n_fwd, tq, tk, tv, fa, s); break;
         case 2: fwd_launch<2>(n_fwd, tq, tk, tv, fa, s); break;
