@@ -47,6 +47,17 @@ def peaks():
         return dict(FALLBACK_PEAKS)
 
 
+def traffic_bytes(w):
+    """ncu-measured DRAM bytes per score pass (profiles/r1_traffic.json; config 3 only)."""
+    if not w.name.startswith("cfg3") or w.seq_len != 32768 or w.batch != 1 or w.n_budget != 256:
+        return None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as f:
+            return json.load(f)["score_pass_bytes"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def f_alg(w) -> float:
     """Algorithmic FLOPs of the score pass per step: QK^T + PV over the causal triangle."""
     L = w.seq_len
@@ -386,7 +397,7 @@ def main():
             "attention_roofline_frac": roof_ms / ms_step,
             "stage_ms": {"score": score_ms, "select+merge+compact": tail_ms},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
-                         "frac": achieved / peak_tf, "traffic": None,
+                         "frac": achieved / peak_tf, "traffic": traffic_bytes(w),
                          "frac_of_sustained_peak": achieved / pk.get("bf16_tflops_sustained", peak_tf),
                          "kernel": "score pass (O+LSE and glo/loc column sums)",
                          "peak_source": f"{pk['source']} bf16_tflops (burst)",
