@@ -386,6 +386,8 @@ class RefLib:
         L.ems_ref_engine_decode.argtypes = [_dp, _dp, _dp, _dp, _dp, _dp, C.c_int64, C.c_int64, C.c_int64,
                                             C.c_int64, C.c_int64, C.c_int64, C.c_double, C.c_double,
                                             C.c_int64, C.c_int32, C.c_int32, C.c_double, _dp, _i64p]
+        L.ems_ref_gen_trace.argtypes = [C.c_int32, C.c_uint64, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
+                                        C.c_double, C.c_double, _dp, _dp, _dp]
         L.ems_ref_gen_synthetic.argtypes = [C.c_int32, C.c_uint64, C.c_int64, C.c_int64, C.c_int64,
                                             C.c_int64, C.c_double, C.c_double, _dp, _dp, _dp]
 
@@ -475,6 +477,18 @@ class RefLib:
         pre = [Cache.from_dump_json(parts[2 * h]) for h in range(H)]
         fin = [Cache.from_dump_json(parts[2 * h + 1]) for h in range(H)]
         return out, am, pre, fin
+
+    def gen_trace(self, kind: int, seed: int, tokens: int, heads: int, dim: int, decode_steps: int,
+                  level: float = 0.8, depth: float = 0.5):
+        """gen_synthetic with its decode steps: q/k/v [heads][tokens + decode_steps][dim]
+        (kind: 0 random, 1 redundant, 2 needle)."""
+        T = tokens + decode_steps
+        q = np.zeros((heads, T, dim))
+        k = np.zeros_like(q)
+        v = np.zeros_like(q)
+        self._chk(self.lib.ems_ref_gen_trace(kind, seed, tokens, heads, dim, decode_steps, level, depth, _ptr(q),
+                                             _ptr(k), _ptr(v)), "gen_trace")
+        return q, k, v
 
     def gen_synthetic(self, kind: int, seed: int, tokens: int, heads: int, dim: int,
                       decode_steps: int = 0, level: float = 0.8, perturb: float = 0.05):

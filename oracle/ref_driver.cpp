@@ -283,4 +283,34 @@ int ems_ref_gen_synthetic(int32_t kind, uint64_t seed, int64_t tokens, int64_t h
     });
 }
 
+// gen_synthetic (proj/src/trace.cpp:239-410) with every step: q/k/v [heads][tokens + steps][dim],
+// prompt rows first, then one row per decode step.  depth: needle position fraction.
+int ems_ref_gen_trace(int32_t kind, uint64_t seed, int64_t tokens, int64_t heads, int64_t dim,
+                      int64_t decode_steps, double level, double depth, double* q, double* k, double* v) {
+    return guarded([&] {
+        ems::SynthParams p;
+        p.tokens = tokens;
+        p.heads = heads;
+        p.dim = dim;
+        p.decode_steps = decode_steps;
+        p.level = level;
+        p.depth = depth;
+        const ems::Trace t = ems::gen_synthetic(static_cast<ems::SynthKind>(kind), seed, p);
+        const int64_t T = tokens + decode_steps;
+        for (int64_t h = 0; h < heads; ++h) {
+            const ems::TraceStep& s0 = t.steps.at(0);
+            std::memcpy(q + h * T * dim, s0.q[h].data.data(), sizeof(double) * tokens * dim);
+            std::memcpy(k + h * T * dim, s0.k[h].data.data(), sizeof(double) * tokens * dim);
+            std::memcpy(v + h * T * dim, s0.v[h].data.data(), sizeof(double) * tokens * dim);
+            for (int64_t s = 0; s < decode_steps; ++s) {
+                const ems::TraceStep& st = t.steps.at(1 + s);
+                const size_t o = (size_t)(h * T + tokens + s) * dim;
+                std::memcpy(q + o, st.q[h].data.data(), sizeof(double) * dim);
+                std::memcpy(k + o, st.k[h].data.data(), sizeof(double) * dim);
+                std::memcpy(v + o, st.v[h].data.data(), sizeof(double) * dim);
+            }
+        }
+    });
+}
+
 }  // extern "C"
