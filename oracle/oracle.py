@@ -386,6 +386,9 @@ class RefLib:
         L.ems_ref_engine_decode.argtypes = [_dp, _dp, _dp, _dp, _dp, _dp, C.c_int64, C.c_int64, C.c_int64,
                                             C.c_int64, C.c_int64, C.c_int64, C.c_double, C.c_double,
                                             C.c_int64, C.c_int32, C.c_int32, C.c_double, _dp, _i64p]
+        L.ems_ref_save_synthetic.argtypes = [C.c_int32, C.c_uint64, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
+                                             C.c_double, C.c_double, C.c_char_p]
+        L.ems_ref_load_trace.argtypes = [C.c_char_p, C.POINTER(C.c_int64)]
         L.ems_ref_gen_trace.argtypes = [C.c_int32, C.c_uint64, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
                                         C.c_double, C.c_double, _dp, _dp, _dp]
         L.ems_ref_gen_synthetic.argtypes = [C.c_int32, C.c_uint64, C.c_int64, C.c_int64, C.c_int64,
@@ -477,6 +480,18 @@ class RefLib:
         pre = [Cache.from_dump_json(parts[2 * h]) for h in range(H)]
         fin = [Cache.from_dump_json(parts[2 * h + 1]) for h in range(H)]
         return out, am, pre, fin
+
+    def save_synthetic(self, path: str, kind: int, seed: int, tokens: int, heads: int, dim: int,
+                       decode_steps: int, level: float = 0.8, depth: float = 0.5) -> None:
+        """gen_synthetic + the reference's own save_trace (KVTR writer)."""
+        self._chk(self.lib.ems_ref_save_synthetic(kind, seed, tokens, heads, dim, decode_steps, level, depth,
+                                                  path.encode()), "save_synthetic")
+
+    def load_trace_status(self, path: str):
+        """(accepted, FormatError offset or None) from the reference's own load_trace."""
+        off = C.c_int64(-1)
+        rc = self.lib.ems_ref_load_trace(path.encode(), C.byref(off))
+        return rc == 0, (off.value if rc == 3 else None)
 
     def gen_trace(self, kind: int, seed: int, tokens: int, heads: int, dim: int, decode_steps: int,
                   level: float = 0.8, depth: float = 0.5):

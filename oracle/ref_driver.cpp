@@ -283,6 +283,37 @@ int ems_ref_gen_synthetic(int32_t kind, uint64_t seed, int64_t tokens, int64_t h
     });
 }
 
+// gen_synthetic + save_trace (proj/src/trace.cpp:157-179): a reference-written KVTR file.
+int ems_ref_save_synthetic(int32_t kind, uint64_t seed, int64_t tokens, int64_t heads, int64_t dim,
+                           int64_t decode_steps, double level, double depth, const char* path) {
+    return guarded([&] {
+        ems::SynthParams p;
+        p.tokens = tokens;
+        p.heads = heads;
+        p.dim = dim;
+        p.decode_steps = decode_steps;
+        p.level = level;
+        p.depth = depth;
+        ems::save_trace(ems::gen_synthetic(static_cast<ems::SynthKind>(kind), seed, p), path);
+    });
+}
+
+// load_trace (proj/src/trace.cpp:119-155): 0 if the reference reader accepts the file, else the
+// FormatError offset is written to *offset and 3 returned.
+int ems_ref_load_trace(const char* path, int64_t* offset) {
+    try {
+        ems::load_trace(path);
+        return 0;
+    } catch (const ems::FormatError& e) {
+        *offset = (int64_t)e.offset;
+        g_err = e.what();
+        return 3;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+
 // gen_synthetic (proj/src/trace.cpp:239-410) with every step: q/k/v [heads][tokens + steps][dim],
 // prompt rows first, then one row per decode step.  depth: needle position fraction.
 int ems_ref_gen_trace(int32_t kind, uint64_t seed, int64_t tokens, int64_t heads, int64_t dim,
