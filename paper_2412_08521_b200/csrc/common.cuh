@@ -66,6 +66,31 @@ __device__ __forceinline__ float warp_max(float v) {
     return v;
 }
 
+// Inclusive block-wide prefix sum of one int per thread (blockDim.x = 32 * nwarps <= 1024):
+// warp shuffles + one pass over the warp totals.  sh: >= 32 ints of shared memory.
+__device__ __forceinline__ int block_incl_scan(int x, int* sh) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    __syncthreads();
+    if (lane == 31) sh[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        int t = lane < nw ? sh[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, t, o);
+            if (lane >= o) t += y;
+        }
+        if (lane < nw) sh[lane] = t;
+    }
+    __syncthreads();
+    return x + (warp > 0 ? sh[warp - 1] : 0);
+}
+
 // Host-side helpers shared by the launchers.
 struct Dims {
     int B, Hq, Hkv, G, L, d, units;

@@ -96,7 +96,7 @@ __global__ void __launch_bounds__(kLutThreads) compact_lut_kernel(
     int L, const int8_t* __restrict__ cls_all, const int32_t* __restrict__ dest_all,
     const int32_t* __restrict__ counts, int cap_t, int cap_lut, int zero_class, int64_t first_pos,
     int32_t* __restrict__ lut_pos, int32_t* __restrict__ lut_slot, int32_t* __restrict__ out_counts) {
-    __shared__ int scan[3][kLutThreads];
+    __shared__ int shs[32];
     const int u = blockIdx.x, tid = threadIdx.x;
     const int8_t* cls = cls_all + (size_t)u * L;
     const int32_t* dest = dest_all + (size_t)u * cap_t;
@@ -106,17 +106,8 @@ __global__ void __launch_bounds__(kLutThreads) compact_lut_kernel(
     // token's destination is found through its TBM rank, so ranks are scanned first.
     int ci = 0, ct = 0;
     for (int i = s0; i < s1; ++i) ci += cls[i] == 2, ct += cls[i] == 1;
-    scan[0][tid] = ci;
-    scan[1][tid] = ct;
-    __syncthreads();
-    for (int o = 1; o < kLutThreads; o <<= 1) {
-        const int a = tid >= o ? scan[0][tid - o] : 0, b = tid >= o ? scan[1][tid - o] : 0;
-        __syncthreads();
-        scan[0][tid] += a;
-        scan[1][tid] += b;
-        __syncthreads();
-    }
-    const int ri0 = scan[0][tid] - ci, rt0 = scan[1][tid] - ct;
+    const int ri0 = block_incl_scan(ci, shs) - ci;
+    const int rt0 = block_incl_scan(ct, shs) - ct;
     int cl = 0;
     {
         int rt = rt0;
@@ -125,15 +116,8 @@ __global__ void __launch_bounds__(kLutThreads) compact_lut_kernel(
             else if (cls[i] == 1) cl += (zero_class || dest[rt++] >= 0);
         }
     }
-    scan[2][tid] = cl;
-    __syncthreads();
-    for (int o = 1; o < kLutThreads; o <<= 1) {
-        const int a = tid >= o ? scan[2][tid - o] : 0;
-        __syncthreads();
-        scan[2][tid] += a;
-        __syncthreads();
-    }
-    int rl = scan[2][tid] - cl, ri = ri0, rt = rt0;
+    const int cl_incl = block_incl_scan(cl, shs);
+    int rl = cl_incl - cl, ri = ri0, rt = rt0;
     int32_t* lp = lut_pos + (size_t)u * cap_lut;
     int32_t* ls = lut_slot + (size_t)u * cap_lut;
     for (int i = s0; i < s1; ++i) {
@@ -154,7 +138,7 @@ __global__ void __launch_bounds__(kLutThreads) compact_lut_kernel(
         int32_t* oc = out_counts + 4 * u;
         oc[0] = counts[4 * u];
         oc[1] = counts[4 * u + 3];
-        oc[2] = scan[2][kLutThreads - 1];
+        oc[2] = cl_incl;  // the last thread's inclusive count = all LUT entries
         oc[3] = 1;
     }
 }

@@ -20,6 +20,8 @@
 // targets at once) finds the n_imp-th and (n_imp+n_tbm)-th largest keys; every
 // token is then classified by comparison, and ascending index lists come out of
 // a block-wide prefix sum.  Integer histograms make the result deterministic.
+#include <stdlib.h>
+
 #include "common.cuh"
 
 namespace ems {
@@ -229,11 +231,218 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(
     }
 }
 
+// ---------------------------------------------------------------------------------------
+// Cluster version: kClu CTAs per unit, each owning a contiguous slice of the tokens.  The
+// fp64 alignment sums, the radix histograms and the index-list offsets are exchanged through
+// distributed shared memory and always combined in rank order, so the result is identical to
+// the single-CTA kernel (same keys, same cut values, same ascending lists).
+constexpr int kClu = 8;
+constexpr int kCThreads = 512;
+
+__device__ __forceinline__ const void* dsm_map(const void* p, int rank) {
+    uint32_t a;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"((uint32_t)__cvta_generic_to_shared(p)),
+                 "r"(rank));
+    return reinterpret_cast<const void*>((uintptr_t)a);  // shared::cluster address, read with ld.shared::cluster
+}
+__device__ __forceinline__ int ld_dsm_i32(const void* p, int rank) {
+    uint32_t a;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"((uint32_t)__cvta_generic_to_shared(p)),
+                 "r"(rank));
+    int v;
+    asm volatile("ld.shared::cluster.s32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ double ld_dsm_f64(const void* p, int rank) {
+    uint32_t a;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"((uint32_t)__cvta_generic_to_shared(p)),
+                 "r"(rank));
+    double v;
+    asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void cl_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ unsigned cl_rank() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+
+__device__ double cblock_sum(double v, double* sh) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    v = warp_sum(v);
+    __syncthreads();
+    if (lane == 0) sh[warp] = v;
+    __syncthreads();
+    double t = 0.0;
+    for (int i = 0; i < kCThreads / 32; ++i) t += sh[i];
+    __syncthreads();
+    return t;
+}
+
+__global__ void __cluster_dims__(kClu, 1, 1) __launch_bounds__(kCThreads) select_cluster_kernel(
+    const float* __restrict__ glo, const float* __restrict__ loc, int L, int l_win, int n_imp, int n_tbm,
+    int kernel, float* __restrict__ pooled_all, int8_t* __restrict__ cls_all, int32_t* __restrict__ imp_idx_all,
+    int32_t* __restrict__ tbm_idx_all, int32_t* __restrict__ counts_all, int cap_c, int cap_tbm, DevStatus* status,
+    int unit_base, int policy, int sink, int n_budget) {
+    __shared__ double sh[32];
+    __shared__ double s_part[2];           // this CTA's alignment partials (read remotely)
+    __shared__ int hist[2][2][256];        // [parity][target][bin] (read remotely)
+    __shared__ int s_cnt[2];               // this CTA's important / TBM counts (read remotely)
+    __shared__ int scan[2][kCThreads];
+    __shared__ int sel_bin[2], sel_above[2];
+    const int rank = (int)cl_rank();
+    const int u = blockIdx.x / kClu;
+    const int tid = threadIdx.x;
+    const float* g = glo + (size_t)u * L;
+    const float* lo = loc + (size_t)u * L;
+    float* pooled = pooled_all + (size_t)u * L;
+    const int per_cta = (L + kClu - 1) / kClu;
+    const int c0 = min(L, rank * per_cta), c1 = min(L, c0 + per_cta);
+    const int half = kernel / 2;
+    // 1. pooled score of this CTA's slice (+ 2. alignment over all L tokens for EMS)
+    double align = 0.0;
+    if (policy == EMS_POLICY_EMS) {
+        double sg = 0.0, sl = 0.0;
+        for (int i = c0 + tid; i < c1; i += kCThreads) sg += (double)g[i], sl += (double)lo[i];
+        sg = cblock_sum(sg, sh);
+        sl = cblock_sum(sl, sh);
+        if (tid == 0) s_part[0] = sg, s_part[1] = sl;
+        cl_sync();
+        double tg = 0.0, tl = 0.0;
+        for (int r = 0; r < kClu; ++r) tg += ld_dsm_f64(&s_part[0], r), tl += ld_dsm_f64(&s_part[1], r);
+        if (!(tg > 0.0)) {
+            if (tid == 0 && rank == 0) record_status(status, EMS_DEGENERATE_INPUT, unit_base + u);
+            cl_sync();
+            return;
+        }
+        align = tl / tg;
+    }
+    const int n_cand_b = L - l_win;
+    const int lo_recent = max(L - (n_budget - sink), sink);
+    for (int i = c0 + tid; i < c1; i += kCThreads) {
+        float v;
+        if (policy == EMS_POLICY_H2O) {
+            v = g[i];
+        } else if (policy == EMS_POLICY_STREAMING) {
+            v = (i < sink || (i >= lo_recent && i < n_cand_b)) ? 1.f : 0.f;
+        } else {
+            const int a = max(0, i - half), bnd = min(L - 1, i + half);
+            double acc = 0.0;
+            for (int jj = a; jj <= bnd; ++jj) {
+                if (policy == EMS_POLICY_SNAPKV) {
+                    acc += (double)lo[jj];
+                } else {
+                    const double x = (double)g[jj] * align, y = (double)lo[jj];
+                    acc += x > y ? x : y;
+                }
+            }
+            v = (float)(acc / (double)(bnd - a + 1));
+        }
+        pooled[i] = v;
+    }
+    __syncthreads();
+    // 3. radix select of the k1-th / k2-th largest candidate keys, histograms summed over the cluster
+    const int n_cand = L - l_win;
+    const int e0 = min(n_cand, c0), e1 = min(n_cand, c1);
+    unsigned long long pre[2] = {0ull, 0ull};
+    int rem[2] = {n_imp, n_imp + n_tbm};
+    for (int pass = 0; pass < 8; ++pass) {
+        const int par = pass & 1;
+        const int shift = 56 - 8 * pass;
+        const unsigned long long hi_mask = pass == 0 ? 0ull : (~0ull << (shift + 8));
+        for (int e = tid; e < 512; e += kCThreads) (&hist[par][0][0])[e] = 0;
+        __syncthreads();
+        for (int i = e0 + tid; i < e1; i += kCThreads) {
+            const unsigned long long key = sel_key(pooled, i);
+            const int bin = (int)((key >> shift) & 255ull);
+            if ((key & hi_mask) == pre[0]) atomicAdd(&hist[par][0][bin], 1);
+            if ((key & hi_mask) == pre[1]) atomicAdd(&hist[par][1][bin], 1);
+        }
+        cl_sync();  // every CTA's histogram complete (and last pass's reads done: other parity)
+        // global histogram = sum over the cluster, in rank order (all CTAs compute the same)
+        for (int e = tid; e < 512; e += kCThreads) {
+            int tsum = 0;
+            for (int r = 0; r < kClu; ++r) tsum += ld_dsm_i32(&hist[par][0][0] + e, r);
+            scan[0][e] = tsum;  // scan[0] reused as a 512-entry staging area
+        }
+        __syncthreads();
+        const int warp = tid >> 5;
+        if (warp < 2) find_bin(&scan[0][256 * warp], rem[warp], &sel_bin[warp], &sel_above[warp]);
+        __syncthreads();
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+            pre[t] |= (unsigned long long)sel_bin[t] << shift;
+            rem[t] -= sel_above[t];
+        }
+        __syncthreads();
+    }
+    const unsigned long long T1 = pre[0];
+    const unsigned long long T2 = n_tbm > 0 ? pre[1] : pre[0];
+    // 4. classify; ascending lists: CTA offset = counts of lower ranks, then a block scan
+    const int per = (c1 - c0 + kCThreads - 1) / kCThreads;
+    const int s0 = min(c1, c0 + tid * per), s1 = min(c1, s0 + per);
+    int ci = 0, ct = 0;
+    for (int i = s0; i < s1; ++i)
+        if (i < n_cand) {
+            const unsigned long long key = sel_key(pooled, i);
+            ci += key >= T1;
+            ct += (key < T1 && key >= T2);
+        }
+    __shared__ int shs[32];
+    const int inc_i = block_incl_scan(ci, shs);
+    const int inc_t = block_incl_scan(ct, shs);
+    if (tid == kCThreads - 1) s_cnt[0] = inc_i, s_cnt[1] = inc_t;
+    cl_sync();
+    int bi = 0, bt = 0;
+    for (int r = 0; r < rank; ++r) bi += ld_dsm_i32(&s_cnt[0], r), bt += ld_dsm_i32(&s_cnt[1], r);
+    int8_t* cls = cls_all + (size_t)u * L;
+    int32_t* imp_idx = imp_idx_all + (size_t)u * cap_c;
+    int32_t* tbm_idx = tbm_idx_all + (size_t)u * cap_tbm;
+    int ri = bi + inc_i - ci, rt = bt + inc_t - ct;
+    for (int i = s0; i < s1; ++i) {
+        int8_t c = 3;
+        if (i < n_cand) {
+            const unsigned long long key = sel_key(pooled, i);
+            if (key >= T1) {
+                c = 2;
+                imp_idx[ri++] = i;
+            } else if (key >= T2) {
+                c = 1;
+                tbm_idx[rt++] = i;
+            } else {
+                c = 0;
+            }
+        }
+        cls[i] = c;
+    }
+    if (tid == 0 && rank == 0) {
+        int32_t* cnt = counts_all + 4 * u;
+        cnt[0] = n_imp;
+        cnt[1] = n_tbm;
+        cnt[2] = n_cand - n_imp - n_tbm;
+        cnt[3] = l_win;
+    }
+    cl_sync();  // no CTA exits while a peer may still read its shared memory
+}
+
 }  // namespace
 
 cudaError_t launch_select(const Dims& dm, int l_win, int n_imp, int n_tbm, int kernel,
                           const float* glo, const float* loc, const ems_stage& sg,
                           DevStatus* status, cudaStream_t s, int policy, int sink, int n_budget) {
+    static const int clustered = [] {
+        const char* e = getenv("EMS_SELECT_CLUSTER");  // A/B override
+        return e ? atoi(e) : 1;
+    }();
+    if (clustered && dm.L >= 8 * kClu) {
+        select_cluster_kernel<<<dm.units * kClu, kCThreads, 0, s>>>(
+            glo, loc, dm.L, l_win, n_imp, n_tbm, kernel, sg.pooled, sg.cls, sg.imp_idx, sg.tbm_idx, sg.part_counts,
+            dm.cap_c, dm.cap_tbm, status, dm.unit_base, policy, sink, n_budget);
+        return cudaGetLastError();
+    }
     select_kernel<<<dm.units, kSelThreads, 0, s>>>(glo, loc, dm.L, l_win, n_imp, n_tbm, kernel,
                                                    sg.pooled, sg.cls, sg.imp_idx, sg.tbm_idx,
                                                    sg.part_counts, dm.cap_c, dm.cap_tbm, status, dm.unit_base,
