@@ -232,7 +232,10 @@ EMS_API int ems_prefill_host(const ems_desc* desc, double rope_base, const void*
  * slots (slot_alive marks live std::optional slots; a freed slot is reused lowest-first), a
  * ring buffer of exact locals, the position-sorted LUT, and meta[8] = {ring head, locals,
  * LUT entries, window_fill, compressed, live centers, 0, 0}.  Keys/values fp32, scores fp64.
- * EMS policy only (the baselines' decode rules are not ported). */
+ * Every policy's decode rule (policy_decode_compress, proj/src/policies.cpp:182-242): EMS
+ * decode_update; SnapKV graduates locals (decode tokens accumulate); H2O graduates and drops
+ * the lowest-glo center; StreamingLLM graduates and drops the oldest non-sink center; full
+ * keeps every token. */
 typedef struct {
     float* slot_key;      /* [u][slots][d] unit-norm raw key */
     float* slot_norm;     /* [u][slots] */
@@ -251,14 +254,15 @@ typedef struct {
 
 typedef struct {
     int32_t units;
-    int32_t slots;   /* center_capacity + 1 */
-    int32_t locals;  /* max(l_win, n_budget) + 1 (a keep-all prefill leaves up to n_budget locals) */
-    int32_t lut;     /* lut_capacity = floor(gamma * n_budget) (cache.hpp:36-38) */
+    int32_t slots;   /* center_capacity + 1 (SnapKV: + decode horizon; full: 1) */
+    int32_t locals;  /* max(l_win, n_budget) + 1 (full: the whole prompt + decode horizon + 1) */
+    int32_t lut;     /* EMS: lut_capacity = floor(gamma * n_budget) (cache.hpp:36-38); else slots */
     int32_t rows;    /* lut + locals: the most expanded rows one step can attend */
 } ems_decode_dims;
 
-EMS_API int ems_decode_dims_for(const ems_desc* desc, ems_decode_dims* out);
-EMS_API size_t ems_decode_workspace_bytes(const ems_desc* desc);
+/* max_positions = the RoPE table size = seq_len + the decode horizon (SnapKV and full grow). */
+EMS_API int ems_decode_dims_for(const ems_desc* desc, int32_t max_positions, ems_decode_dims* out);
+EMS_API size_t ems_decode_workspace_bytes(const ems_desc* desc, int32_t max_positions);
 
 /* (cos, sin) of position * base^(-2i/d) for positions [0, max_positions), fp64 rounded to
  * fp32: table = float2 [max_positions][head_dim / 2] (device).  Shared by all decode steps. */
@@ -267,8 +271,8 @@ EMS_API int ems_rope_table(int32_t head_dim, double base, int32_t max_positions,
 
 /* Decode state from a prefill cache (ems_prefill / ems_prefill_compress output); window_fill
  * starts at 0 as engine::prefill leaves it (engine.cpp:74). */
-EMS_API int ems_decode_init(const ems_desc* desc, const ems_cache* cache, const ems_decode_state* state,
-                    cudaStream_t stream);
+EMS_API int ems_decode_init(const ems_desc* desc, int32_t max_positions, const ems_cache* cache,
+                    const ems_decode_state* state, cudaStream_t stream);
 
 /* One decode step for every unit at logical `position` (engine::next_position):
  *   q [B][Hq][d], k / v [B][Hkv][d] raw (pre-RoPE), dtype -> out [B][Hq][d] (dtype),

@@ -385,7 +385,8 @@ class RefLib:
                                              C.c_int32]
         L.ems_ref_engine_decode.argtypes = [_dp, _dp, _dp, _dp, _dp, _dp, C.c_int64, C.c_int64, C.c_int64,
                                             C.c_int64, C.c_int64, C.c_int64, C.c_double, C.c_double,
-                                            C.c_int64, C.c_int32, C.c_int32, C.c_double, _dp, _i64p]
+                                            C.c_int64, C.c_int32, C.c_int32, C.c_double, _dp, _i64p,
+                                            C.c_int32, C.c_int64]
         L.ems_ref_save_synthetic.argtypes = [C.c_int32, C.c_uint64, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
                                              C.c_double, C.c_double, C.c_char_p]
         L.ems_ref_load_trace.argtypes = [C.c_char_p, C.POINTER(C.c_int64)]
@@ -464,7 +465,8 @@ class RefLib:
                   "engine_prefill")
         return self.lib.ems_ref_last_json().decode()
 
-    def engine_decode(self, q, k, v, dq, dk, dv, c: Config, rope_base=10000.0, without_pos=False):
+    def engine_decode(self, q, k, v, dq, dk, dv, c: Config, rope_base=10000.0, without_pos=False, policy=0,
+                      sink=4):
         """engine::prefill + decode_step x steps (EMS).  q/k/v [H][n][d], dq/dk/dv [steps][H][d].
         Returns (out [steps][H][d], argmax [steps][H], prefill caches, final caches)."""
         q, k, v, dq, dk, dv = map(_f64, (q, k, v, dq, dk, dv))
@@ -475,7 +477,7 @@ class RefLib:
         self._chk(self.lib.ems_ref_engine_decode(_ptr(q), _ptr(k), _ptr(v), _ptr(dq), _ptr(dk), _ptr(dv), H, n, d,
                                                  steps, c.n_budget, c.l_win, c.tau, c.gamma, c.kernel_size,
                                                  int(c.zero_class), int(without_pos), rope_base, _ptr(out),
-                                                 _ptr(am, _i64p)), "engine_decode")
+                                                 _ptr(am, _i64p), int(policy), int(sink)), "engine_decode")
         parts = self.lib.ems_ref_last_json().decode().split("\x1e")
         pre = [Cache.from_dump_json(parts[2 * h]) for h in range(H)]
         fin = [Cache.from_dump_json(parts[2 * h + 1]) for h in range(H)]

@@ -166,11 +166,16 @@ int ems_ref_engine_decode(const double* q, const double* k, const double* v, con
                           const double* dk, const double* dv, int64_t H, int64_t n, int64_t d,
                           int64_t steps, int64_t n_budget, int64_t l_win, double tau, double gamma,
                           int64_t kernel, int32_t zero_class, int32_t without_pos, double rope_base,
-                          double* out, int64_t* argmax) {
+                          double* out, int64_t* argmax, int32_t policy, int64_t sink) {
     return guarded([&] {
         auto cfg = make_config(n_budget, l_win, tau, gamma, kernel, zero_class);
         if (without_pos) cfg.position_mode = ems::PositionMode::without_pos;
-        ems::EngineState e = ems::make_engine(H, d, ems::PolicyHandle{ems::PolicyKind::ems}, cfg, rope_base);
+        static const ems::PolicyKind kinds[] = {ems::PolicyKind::ems, ems::PolicyKind::full,
+                                                ems::PolicyKind::streaming_llm, ems::PolicyKind::h2o,
+                                                ems::PolicyKind::snapkv};
+        ems::PolicyHandle ph{kinds[policy]};
+        ph.sink_count = (std::size_t)sink;
+        ems::EngineState e = ems::make_engine(H, d, ph, cfg, rope_base);
         std::vector<ems::Matrix> qb, kb, vb;
         for (int64_t h = 0; h < H; ++h) {
             qb.push_back(to_matrix(q + h * n * d, n, d));

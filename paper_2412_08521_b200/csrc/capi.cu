@@ -44,7 +44,8 @@ cudaError_t launch_decode_init(const Dims& m, int dtype, const ems_cache& c, con
 cudaError_t launch_decode_step(const Dims& m, int dtype, int S, int W, int T, int R, int l_win, int lut_cap,
                                double tau, int zero_class, int with_pos, long long position, int max_pos,
                                const float2* table, const void* q, const void* k, const void* v, void* out,
-                               int32_t* argmax_pos, const ems_decode_state& st, void* ws, cudaStream_t s);
+                               int32_t* argmax_pos, const ems_decode_state& st, void* ws, cudaStream_t s,
+                               int policy, int sink, int n_budget);
 size_t decode_workspace_bytes(const Dims& m, int R);
 cudaError_t launch_redundancy_cross(int dtype, int d, const void* kr, const void* vr, int nr,
                                     const void* kc, const void* vc, int nc, int key_only,
@@ -690,20 +691,40 @@ extern "C" int ems_prefill_host(const ems_desc* d, double rope_base, const void*
 // Decode (decode_step / decode_update).
 namespace ems {
 namespace {
-void decode_caps(const ems_desc& d, int& S, int& W, int& T, int& R) {
+// Per-unit capacities.  EMS / H2O / StreamingLLM keep the centers at capacity (one extra
+// slot for the graduating token); SnapKV and full let decode tokens accumulate
+// (policies.cpp:186-191), so they are sized by the decode horizon max_pos - seq_len.
+void decode_caps(const ems_desc& d, int max_pos, int& S, int& W, int& T, int& R) {
     const Dims m = make_dims(d);
-    S = m.cap_c + 1;
-    W = (d.l_win > d.n_budget ? d.l_win : d.n_budget) + 1;
-    T = (int)(d.gamma * (double)d.n_budget);  // lut_capacity, cache.hpp:36-38
-    if (T < m.cap_lut) T = m.cap_lut;
+    const int steps = max_pos > d.seq_len ? max_pos - d.seq_len : 0;
+    const int wl = (d.l_win > d.n_budget ? d.l_win : d.n_budget) + 1;
+    switch (d.policy) {
+        case EMS_POLICY_FULL:
+            S = 1;
+            W = (d.seq_len > d.n_budget ? d.seq_len : d.n_budget) + steps + 1;
+            T = 1;
+            break;
+        case EMS_POLICY_SNAPKV:
+            S = m.cap_c + steps + 1;
+            W = wl;
+            T = S;
+            break;
+        case EMS_POLICY_H2O:
+        case EMS_POLICY_STREAMING:
+            S = m.cap_c + 1;
+            W = wl;
+            T = S;
+            break;
+        default:
+            S = m.cap_c + 1;
+            W = wl;
+            T = (int)(d.gamma * (double)d.n_budget);  // lut_capacity, cache.hpp:36-38
+            if (T < m.cap_lut) T = m.cap_lut;
+    }
     R = T + W;
 }
 int decode_check(const ems_desc* d) {
     if (int rc = ems_validate(d)) return rc;
-    if (d->policy != EMS_POLICY_EMS) {
-        set_error("decode: only the EMS policy's decode_update is implemented on the device");
-        return EMS_UNSUPPORTED;
-    }
     if (d->heads_q / d->heads_kv > 8) {
         set_error("decode: at most 8 query heads per KV head");
         return EMS_UNSUPPORTED;
@@ -719,11 +740,11 @@ int decode_check(const ems_desc* d) {
 
 extern "C" {
 
-int ems_decode_dims_for(const ems_desc* d, ems_decode_dims* out) {
+int ems_decode_dims_for(const ems_desc* d, int32_t max_pos, ems_decode_dims* out) {
     using namespace ems;
     if (int rc = decode_check(d)) return rc;
     int S, W, T, R;
-    decode_caps(*d, S, W, T, R);
+    decode_caps(*d, max_pos, S, W, T, R);
     out->units = d->batch * d->heads_kv;
     out->slots = S;
     out->locals = W;
@@ -732,11 +753,11 @@ int ems_decode_dims_for(const ems_desc* d, ems_decode_dims* out) {
     return EMS_OK;
 }
 
-size_t ems_decode_workspace_bytes(const ems_desc* d) {
+size_t ems_decode_workspace_bytes(const ems_desc* d, int32_t max_pos) {
     using namespace ems;
     if (decode_check(d) != EMS_OK) return 0;
     int S, W, T, R;
-    decode_caps(*d, S, W, T, R);
+    decode_caps(*d, max_pos, S, W, T, R);
     return decode_workspace_bytes(make_dims(*d), R);
 }
 
@@ -754,7 +775,8 @@ int ems_rope_table(int32_t d, double base, int32_t max_pos, void* table, cudaStr
     return EMS_OK;
 }
 
-int ems_decode_init(const ems_desc* d, const ems_cache* c, const ems_decode_state* st, cudaStream_t s) {
+int ems_decode_init(const ems_desc* d, int32_t max_pos, const ems_cache* c, const ems_decode_state* st,
+                    cudaStream_t s) {
     using namespace ems;
     if (int rc = decode_check(d)) return rc;
     if (!c || !st) {
@@ -762,7 +784,7 @@ int ems_decode_init(const ems_desc* d, const ems_cache* c, const ems_decode_stat
         return EMS_INVALID_ARGUMENT;
     }
     int S, W, T, R;
-    decode_caps(*d, S, W, T, R);
+    decode_caps(*d, max_pos, S, W, T, R);
     cudaError_t e = launch_decode_init(make_dims(*d), d->dtype, *c, *st, S, W, T, s);
     if (e != cudaSuccess) {
         set_error("decode init launch: %s", cudaGetErrorString(e));
@@ -785,7 +807,7 @@ int ems_decode_step(const ems_desc* d, int64_t position, const void* table, int3
         return EMS_INVALID_ARGUMENT;
     }
     int S, W, T, R;
-    decode_caps(*d, S, W, T, R);
+    decode_caps(*d, max_pos, S, W, T, R);
     const Dims m = make_dims(*d);
     if (!ws || ws_bytes < decode_workspace_bytes(m, R)) {
         set_error("ems_decode_step: workspace too small (need %zu)", decode_workspace_bytes(m, R));
@@ -793,7 +815,8 @@ int ems_decode_step(const ems_desc* d, int64_t position, const void* table, int3
     }
     cudaError_t e = launch_decode_step(m, d->dtype, S, W, T, R, d->l_win, T, d->tau, d->zero_class,
                                        d->position_mode == 0, position, max_pos, static_cast<const float2*>(table),
-                                       q, k, v, out, argmax_pos, *st, ws, s);
+                                       q, k, v, out, argmax_pos, *st, ws, s, d->policy, d->sink_count,
+                                       d->n_budget);
     if (e != cudaSuccess) {
         set_error("decode step launch: %s", cudaGetErrorString(e));
         return EMS_CUDA_ERROR;

@@ -49,6 +49,7 @@ struct DecArgs {
     int32_t* row_pos;              // [units][R]
     float* probs;                  // [units][G][R]
     float* pmean;                  // [units][R]
+    int policy, sink, n_budget;    // ems_policy, PolicyHandle::sink_count, n_budget
 };
 
 __device__ __forceinline__ float ldx(const void* p, size_t i, int dtype) {
@@ -188,6 +189,7 @@ __global__ void __launch_bounds__(kT) decode_step_kernel(DecArgs a) {
         }
         ++count;
     }
+    __syncthreads();  // the appended row's position is read by another warp in step 3
     // 2. RoPE'd queries (apply_rope at the new position, engine.cpp:175)
     for (int x = tid; x < G * pairs; x += kT) {
         const int h = x / pairs, p = x % pairs;
@@ -344,12 +346,14 @@ __global__ void __launch_bounds__(kT) decode_step_kernel(DecArgs a) {
         wfill = 0;
     }
     __syncthreads();
-    // 10. decode_update (compressor.cpp:376-398)
+    // 10. policy_decode_compress (policies.cpp:182-242): EMS decode_update (compressor.cpp:376-398);
+    //     SnapKV / H2O / StreamingLLM graduate_locals (policies.cpp:88-98) then drop; full: identity
     int n_alive = s_meta[5], compressed = s_meta[4];
-    while (count > a.l_win) {
+    const bool ems = a.policy == EMS_POLICY_EMS;
+    while (a.policy != EMS_POLICY_FULL && count > a.l_win) {
         const int g = head;  // graduating local (front of the window)
         // 10a. oldest zero-mapped (else oldest) LUT entry leaves at capacity (:272-284)
-        if (lut_n >= a.lut_cap) {
+        if (ems && lut_n >= a.lut_cap) {
             Cand c{0.0, 0, -1};
             for (int e = tid; e < lut_n; e += kT)
                 if (tslot[e] < 0 && (c.idx < 0 || e < c.idx)) c = Cand{0.0, e, e};
@@ -396,7 +400,7 @@ __global__ void __launch_bounds__(kT) decode_step_kernel(DecArgs a) {
         head = (head + 1) % W;
         --count;
         __syncthreads();
-        if (n_alive <= a.cap_c) continue;
+        if (!ems || n_alive <= a.cap_c) continue;
         // 10c. retire_least_important_center (:286-372)
         double sg = 0.0, sl = 0.0;
         for (int s = tid; s < S; s += kT)
@@ -513,6 +517,46 @@ __global__ void __launch_bounds__(kT) decode_step_kernel(DecArgs a) {
         compressed = 1;
         __syncthreads();
     }
+    // 10d. H2O: drop the lowest-glo centers beyond capacity (ties -> lower position);
+    //      StreamingLLM: drop the oldest non-sink center while over budget (policies.cpp:200-241)
+    while ((a.policy == EMS_POLICY_H2O && n_alive > a.cap_c) ||
+           (a.policy == EMS_POLICY_STREAMING && n_alive + count > a.n_budget)) {
+        Cand w{0.0, 0, -1};
+        for (int s = tid; s < S; s += kT)
+            if (salive[s]) {
+                Cand x;
+                if (a.policy == EMS_POLICY_H2O) x = Cand{sscore[3 * s], spos[s], s};
+                else if (spos[s] >= a.sink) x = Cand{(double)spos[s], spos[s], s};
+                else continue;
+                if (w.idx < 0 || x.key < w.key || (x.key == w.key && x.tie < w.tie)) w = x;
+            }
+        auto least2 = [](const Cand& x, const Cand& y) {
+            if (y.idx < 0) return x.idx >= 0;
+            if (x.idx < 0) return false;
+            return x.key < y.key || (x.key == y.key && x.tie < y.tie);
+        };
+        w = bselect(w, least2, shc);
+        if (w.idx < 0) break;  // nothing evictable
+        const int ds_ = w.idx;
+        // drop_center (policies.cpp:100-106): erase its LUT entries (stable), free the slot
+        int base = 0;
+        for (int c0 = 0; c0 < lut_n; c0 += kT) {
+            const int e = c0 + tid;
+            int pp = 0, ss = 0;
+            const int keep = e < lut_n && tslot[e] != ds_;
+            if (e < lut_n) pp = tpos[e], ss = tslot[e];
+            int tot;
+            const int off = bscan(keep, shi, &tot);
+            if (keep) tpos[base + off] = pp, tslot[base + off] = ss;
+            base += tot;
+            __syncthreads();
+        }
+        lut_n = base;
+        if (tid == 0) salive[ds_] = 0;
+        --n_alive;
+        compressed = 1;
+        __syncthreads();
+    }
     if (tid == 0) {
         meta[0] = head;
         meta[1] = count;
@@ -605,8 +649,12 @@ cudaError_t launch_decode_init(const Dims& m, int dtype, const ems_cache& c, con
 cudaError_t launch_decode_step(const Dims& m, int dtype, int S, int W, int T, int R, int l_win, int lut_cap,
                                double tau, int zero_class, int with_pos, long long position, int max_pos,
                                const float2* table, const void* q, const void* k, const void* v, void* out,
-                               int32_t* argmax_pos, const ems_decode_state& st, void* ws, cudaStream_t s) {
+                               int32_t* argmax_pos, const ems_decode_state& st, void* ws, cudaStream_t s,
+                               int policy, int sink, int n_budget) {
     DecArgs a;
+    a.policy = policy;
+    a.sink = sink;
+    a.n_budget = n_budget;
     a.G = m.G;
     a.d = m.d;
     a.S = S;

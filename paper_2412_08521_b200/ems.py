@@ -123,11 +123,11 @@ def lib() -> C.CDLL:
         L.ems_prefill_host.argtypes = [C.POINTER(Desc), C.c_double, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,
                                        fp, fp, fp, C.POINTER(CCache), C.POINTER(CCache), C.c_int32, vp,
                                        C.c_size_t, vp, vp]
-        L.ems_decode_dims_for.argtypes = [C.POINTER(Desc), C.POINTER(DecodeDims)]
+        L.ems_decode_dims_for.argtypes = [C.POINTER(Desc), C.c_int32, C.POINTER(DecodeDims)]
         L.ems_decode_workspace_bytes.restype = C.c_size_t
-        L.ems_decode_workspace_bytes.argtypes = [C.POINTER(Desc)]
+        L.ems_decode_workspace_bytes.argtypes = [C.POINTER(Desc), C.c_int32]
         L.ems_rope_table.argtypes = [C.c_int32, C.c_double, C.c_int32, vp, vp]
-        L.ems_decode_init.argtypes = [C.POINTER(Desc), C.POINTER(CCache), C.POINTER(CDecode), vp]
+        L.ems_decode_init.argtypes = [C.POINTER(Desc), C.c_int32, C.POINTER(CCache), C.POINTER(CDecode), vp]
         L.ems_decode_step.argtypes = [C.POINTER(Desc), C.c_int64, vp, C.c_int32, vp, vp, vp, vp, vp,
                                       C.POINTER(CDecode), vp, C.c_size_t, vp]
         L.ems_rope.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_double, C.c_int64, vp, vp,
@@ -447,9 +447,11 @@ def redundancy_cross(k_rows, v_rows, k_cols, v_cols, key_only=False) -> torch.Te
 
 
 class DecodeState:
-    """The EMS decode loop on the device (ems_decode_*): decode_step + decode_update
-    (proj/src/engine.cpp:150-210, proj/src/compressor.cpp:376-398) for every unit of a
-    problem, one CTA per unit per step.  State = fixed-capacity SoA (ems_decode_state)."""
+    """The decode loop on the device (ems_decode_*): decode_step (proj/src/engine.cpp:150-210)
+    with the policy's decode rule (policy_decode_compress, proj/src/policies.cpp:182-242; EMS:
+    decode_update, proj/src/compressor.cpp:376-398) for every unit of a problem, one CTA per
+    unit per step.  State = fixed-capacity SoA (ems_decode_state); max_positions bounds the
+    RoPE table and the growth of the SnapKV / full caches."""
 
     def __init__(self, B: int, Hq: int, Hkv: int, L: int, d: int, dtype: torch.dtype, cfg: EmsConfig,
                  rope_base: float, max_positions: int, device=None):
@@ -458,7 +460,8 @@ class DecodeState:
         self.dtype, self.cfg = dtype, cfg
         L_ = lib()
         dims = DecodeDims()
-        _check(L_.ems_decode_dims_for(C.byref(self.desc), C.byref(dims)))
+        self.max_positions = int(max_positions)
+        _check(L_.ems_decode_dims_for(C.byref(self.desc), self.max_positions, C.byref(dims)))
         self.dims = dims
         U, S, W, T = dims.units, dims.slots, dims.locals, dims.lut
         dev = self.device
@@ -469,18 +472,18 @@ class DecodeState:
                           local_value=z(U, W, d), local_pos=z(U, W, dt=i32), local_score=z(U, W, 3, dt=f64),
                           lut_pos=z(U, T, dt=i32), lut_slot=z(U, T, dt=i32), meta=z(U, 8, dt=i32))
         self._c = CDecode(*[_p(self.state[f]) for f in DECODE_FIELDS])
-        self.max_positions = int(max_positions)
         self.table = torch.empty((self.max_positions, d // 2, 2), dtype=torch.float32, device=dev)
         _check(L_.ems_rope_table(d, float(rope_base), self.max_positions, _p(self.table), _stream()))
-        self.workspace = torch.empty(max(L_.ems_decode_workspace_bytes(C.byref(self.desc)), 16), dtype=torch.uint8,
-                                     device=dev)
+        self.workspace = torch.empty(max(L_.ems_decode_workspace_bytes(C.byref(self.desc), self.max_positions), 16),
+                                     dtype=torch.uint8, device=dev)
         self.out = torch.empty((B, Hq, d), dtype=dtype, device=dev)
         self.argmax = torch.empty((B, Hq), dtype=torch.int32, device=dev)
         self.position = L
 
     def init_from_plan(self, plan: "Plan") -> None:
         """Decode state from a prefill Plan's compressed cache (ems_decode_init)."""
-        _check(lib().ems_decode_init(C.byref(self.desc), C.byref(plan._ccache), C.byref(self._c), _stream()))
+        _check(lib().ems_decode_init(C.byref(self.desc), self.max_positions, C.byref(plan._ccache), C.byref(self._c),
+                                     _stream()))
         self.position = plan.desc.seq_len + plan.desc.first_position
 
     def load_caches(self, caches, position: int) -> None:

@@ -7,8 +7,8 @@
   with the byte offset the reference reports (bad magic 0, bad version 4, truncation at the
   read position, non-finite payload at the row start); a trace must be one prefill step then
   single-token decode steps (Trace::validate, :101-114).
-* ``run_experiment`` is run_experiment_multi (proj/src/experiment.cpp:152-264) for the EMS
-  policy with the compressed engine on the GPU (device RoPE + prefill + the device decode loop)
+* ``run_experiment`` is run_experiment_multi (proj/src/experiment.cpp:152-264) for any list of
+  policies (ems, full, streaming, h2o, snapkv) with the compressed engine on the GPU (device RoPE + prefill + the device decode loop)
   and the dense full-cache reference run (run_reference, :42-80) as plain fp64 tensor math on
   the same device (report infrastructure, not the accelerated path).  ``report_json`` /
   ``report_csv`` emit the reference's schema (report_json :271-326, report_csv :328-344).
@@ -176,8 +176,11 @@ def _cos_error(a, b) -> float:  # concat_cos_error, experiment.cpp:97-120
 
 
 def run_experiment(tr: Trace, cfg, label: str = "", needle_pos: int | None = None, rope_base: float = 10000.0,
-                   device="cuda") -> dict:
-    """run_experiment_multi (experiment.cpp:152-264), EMS policy, compressed engine on the GPU."""
+                   device="cuda", policies=None) -> dict:
+    """run_experiment_multi (experiment.cpp:152-264): the compressed engine on the GPU, once per
+    policy (``policies`` = policy names, default ``[cfg.policy]``), against one dense run."""
+    import dataclasses
+
     import torch
 
     from paper_2412_08521_b200 import ems
@@ -187,45 +190,49 @@ def run_experiment(tr: Trace, cfg, label: str = "", needle_pos: int | None = Non
     n = tr.prefill_tokens
     ref_pre, ref_outs, ref_am = _dense_reference(q, k, v, n, rope_base, device)
     t = lambda a: torch.tensor(np.ascontiguousarray(a), dtype=torch.float32, device=device)  # noqa: E731
-    plan = ems.prefill(t(q[None, :, :n]), t(k[None, :, :n]), t(v[None, :, :n]), cfg, rope_base)
-    ds = ems.DecodeState(1, H, H, n, d, torch.float32, cfg, rope_base, T + 1, device=device)
-    ds.init_from_plan(plan)
+    reports = []
+    for pol in (policies or [cfg.policy]):
+        pc = dataclasses.replace(cfg, policy=pol)
+        plan = ems.prefill(t(q[None, :, :n]), t(k[None, :, :n]), t(v[None, :, :n]), pc, rope_base)
+        ds = ems.DecodeState(1, H, H, n, d, torch.float32, pc, rope_base, T + 1, device=device)
+        ds.init_from_plan(plan)
 
-    def accounting():  # stored_entries / bytes_stored per head (cache.hpp:92-99, cache.cpp:40-46)
-        meta = ds.state["meta"].cpu().numpy()
-        e = meta[:, 1] + meta[:, 5]
-        return int(e.sum()), int((8 * (2 * e * d + 4 * e + meta[:, 2])).sum())
+        def accounting():  # stored_entries / bytes_stored per head (cache.hpp:92-99, cache.cpp:40-46)
+            meta = ds.state["meta"].cpu().numpy()
+            e = meta[:, 1] + meta[:, 5]
+            return int(e.sum()), int((8 * (2 * e * d + 4 * e + meta[:, 2])).sum())
 
-    steps = []
-    e0, b0 = accounting()
-    pre = plan.out[0].double()
-    steps.append(dict(step=0, l2_error=_l2(pre, ref_pre), cos_error=_cos_error(pre, ref_pre), entries=e0, bytes=b0,
-                      argmax_match=True))
-    retained = True
-    for s in range(T - n):
-        o, am = ds.step(t(q[None, :, n + s]), t(k[None, :, n + s]), t(v[None, :, n + s]))
-        out = o[0].double()
-        match = bool((am[0].long() == ref_am[s]).all())
-        e, b = accounting()
-        steps.append(dict(step=s + 1, l2_error=_l2(out, ref_outs[s]), cos_error=_cos_error(out, ref_outs[s]),
-                          entries=e, bytes=b, argmax_match=match))
-        retained = retained and match
-    dec = steps[1:]
-    agg = dict(mean_l2=float(np.mean([m["l2_error"] for m in dec])) if dec else 0.0,
-               max_l2=float(max([m["l2_error"] for m in dec], default=0.0)),
-               mean_cos_error=float(np.mean([m["cos_error"] for m in dec])) if dec else 0.0,
-               argmax_match_rate=float(np.mean([m["argmax_match"] for m in dec])) if dec else 1.0)
-    needle = None
-    if needle_pos is not None:
-        in_lut = all(_position_represented(ds.unit_cache(h), needle_pos) for h in range(H))
-        needle = dict(position=int(needle_pos), retained=retained and bool(dec), in_lut_final=in_lut)
+        steps = []
+        e0, b0 = accounting()
+        pre = plan.out[0].double()
+        steps.append(dict(step=0, l2_error=_l2(pre, ref_pre), cos_error=_cos_error(pre, ref_pre), entries=e0,
+                          bytes=b0, argmax_match=True))
+        retained = True
+        for s in range(T - n):
+            o, am = ds.step(t(q[None, :, n + s]), t(k[None, :, n + s]), t(v[None, :, n + s]))
+            out = o[0].double()
+            match = bool((am[0].long() == ref_am[s]).all())
+            e, b = accounting()
+            steps.append(dict(step=s + 1, l2_error=_l2(out, ref_outs[s]), cos_error=_cos_error(out, ref_outs[s]),
+                              entries=e, bytes=b, argmax_match=match))
+            retained = retained and match
+        dec = steps[1:]
+        agg = dict(mean_l2=float(np.mean([m["l2_error"] for m in dec])) if dec else 0.0,
+                   max_l2=float(max([m["l2_error"] for m in dec], default=0.0)),
+                   mean_cos_error=float(np.mean([m["cos_error"] for m in dec])) if dec else 0.0,
+                   argmax_match_rate=float(np.mean([m["argmax_match"] for m in dec])) if dec else 1.0)
+        needle = None
+        if needle_pos is not None:
+            in_lut = all(_position_represented(ds.unit_cache(h), needle_pos) for h in range(H))
+            needle = dict(position=int(needle_pos), retained=retained and bool(dec), in_lut_final=in_lut)
+        reports.append(dict(policy=pol, compression_applied=bool(plan.cache["counts"][0, 3].item()), steps=steps,
+                            aggregate=agg, needle=needle, diagnostics=[]))
     return {"schema_version": 1,
             "trace": dict(label=label, num_heads=H, head_dim=d, prefill_tokens=n, decode_steps=T - n),
             "config": dict(n_budget=cfg.n_budget, l_win=cfg.l_win, tau=cfg.tau, gamma=cfg.gamma, zeta=0.95,
                            kernel_size=cfg.kernel_size, position_mode=cfg.position_mode,
                            eviction="zero_class" if cfg.zero_class else "explicit_removal"),
-            "policies": [dict(policy="ems", compression_applied=bool(plan.cache["counts"][0, 3].item()),
-                              steps=steps, aggregate=agg, needle=needle, diagnostics=[])]}
+            "policies": reports}
 
 
 def _position_represented(c: dict, pos: int) -> bool:  # HeadCacheState::position_represented, cache.cpp:82-94

@@ -18,14 +18,18 @@ from oracle.oracle import Config  # noqa: E402
 from paper_2412_08521_b200 import ems  # noqa: E402
 
 
-def _run(reflib, H, n, d, steps, c: Config, seed, without_pos=False, rope=1e4):
+POLICY = {"ems": 0, "full": 1, "streaming": 2, "h2o": 3, "snapkv": 4}
+
+
+def _run(reflib, H, n, d, steps, c: Config, seed, without_pos=False, rope=1e4, policy="ems"):
     rng = np.random.default_rng(seed)
     f32 = lambda a: a.astype(np.float32).astype(np.float64)  # noqa: E731  fp32-exact inputs
     q, k, v = (f32(rng.standard_normal((H, n, d))) for _ in range(3))
     dq, dk, dv = (f32(rng.standard_normal((steps, H, d))) for _ in range(3))
-    out_ref, am_ref, pre, fin = reflib.engine_decode(q, k, v, dq, dk, dv, c, rope_base=rope, without_pos=without_pos)
+    out_ref, am_ref, pre, fin = reflib.engine_decode(q, k, v, dq, dk, dv, c, rope_base=rope, without_pos=without_pos,
+                                                     policy=POLICY[policy])
     cfg = ems.EmsConfig(c.n_budget, c.l_win, c.tau, c.gamma, c.kernel_size, c.zero_class,
-                        position_mode="without_pos" if without_pos else "with_pos")
+                        position_mode="without_pos" if without_pos else "with_pos", policy=policy)
     ds = ems.DecodeState(1, H, H, n, d, torch.float32, cfg, rope, n + steps)
     ds.load_caches(pre, position=n)
     T = lambda a: torch.tensor(a, dtype=torch.float32, device="cuda").reshape(1, H, d).contiguous()  # noqa: E731
@@ -62,6 +66,16 @@ def test_decode_matches_reference(reflib, tau, zero_class, without_pos):
     c = Config(n_budget=24, l_win=4, tau=tau, gamma=2.0, kernel_size=3, zero_class=zero_class)
     outs, ams, out_ref, am_ref, fin, ds = _run(reflib, 3, 100, 16, 40, c, seed=5, without_pos=without_pos)
     _check(outs, ams, out_ref, am_ref, fin, ds, 3)
+
+
+@pytest.mark.parametrize("policy", ["full", "streaming", "h2o", "snapkv"])
+def test_baseline_policy_decode_matches_reference(reflib, policy):
+    """policy_decode_compress (policies.cpp:182-242) for the baselines, 60 steps."""
+    c = Config(n_budget=24, l_win=4, tau=0.6, gamma=2.0, kernel_size=3)
+    outs, ams, out_ref, am_ref, fin, ds = _run(reflib, 2, 80, 16, 60, c, seed=17, policy=policy)
+    _check(outs, ams, out_ref, am_ref, fin, ds, 2)
+    if policy == "full":  # identity policy: the dense attention itself (criterion 4 analog)
+        assert len(ds.unit_cache(0)["local_position"]) == 80 + 60
 
 
 def test_decode_after_keep_all_prefill(reflib):
