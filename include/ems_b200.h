@@ -289,6 +289,21 @@ EMS_API int ems_redundancy_cross(int32_t dtype, int32_t d, const void* k_rows, c
                          int32_t n_rows, const void* k_cols, const void* v_cols, int32_t n_cols,
                          int32_t key_only, float* r, cudaStream_t stream);
 
+/* analyze_trace's per-head diagnostics (proj/src/experiment.cpp:133-150) for `units`
+ * independent token sequences of length L; workspace >= ems_diagnostics_workspace_bytes(units,
+ * L); data-dependent errors are read back with ems_sync_status(NULL, workspace, stream).
+ *   ems_sparsity_rate:   sparsity_rate(combine_glo_loc(glo, loc), zeta)  analysis.cpp:71-91,
+ *                        scoring.cpp:105-124; glo / loc [units][L] fp32 -> rate [units] fp64
+ *                        (device); zeta in (0, 1]; no mass -> EMS_DEGENERATE_INPUT.
+ *   ems_redundancy_rate: redundancy_rate_direct(k_raw, v_raw, tau)  analysis.cpp:93-118;
+ *                        k / v [units][L][d] (dtype) -> rate [units] fp64 (device). */
+EMS_API size_t ems_diagnostics_workspace_bytes(int32_t units, int32_t L);
+EMS_API int ems_sparsity_rate(int32_t units, int32_t L, const float* glo, const float* loc, double zeta,
+                              double* rate, void* workspace, size_t workspace_bytes, cudaStream_t stream);
+EMS_API int ems_redundancy_rate(int32_t dtype, int32_t d, int32_t units, int32_t L, const void* k, const void* v,
+                                double tau, double* rate, void* workspace, size_t workspace_bytes,
+                                cudaStream_t stream);
+
 /* Synchronises `stream` and returns the first data-dependent error the kernels
  * recorded in the workspace (EMS_DEGENERATE_INPUT, EMS_CORRUPTION) or EMS_OK. */
 EMS_API int ems_sync_status(const ems_desc* desc, void* workspace, cudaStream_t stream);

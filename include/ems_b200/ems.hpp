@@ -475,6 +475,33 @@ inline Matrix redundancy_cross(const Matrix& k_rows, const Matrix& v_rows, const
     return out;
 }
 
+// sparsity_rate, proj/include/ems/analysis.hpp:22-25 (analysis.cpp:71-91), on the device
+// (diag.cu).  The score is rounded to fp32, the device score precision (contract D9).
+inline double sparsity_rate(const Vector& score, double zeta) {
+    if (score.empty()) throw std::invalid_argument("sparsity_rate: empty score");
+    const int32_t n = static_cast<int32_t>(score.size());
+    std::vector<float> h(score.begin(), score.end());
+    detail::DevBuf s(h.size() * 4), rate(8), ws(ems_diagnostics_workspace_bytes(1, n));
+    detail::cuda(cudaMemcpy(s.p, h.data(), h.size() * 4, cudaMemcpyHostToDevice));
+    // glo = loc = score: align = 1 and the combined score is the score itself
+    detail::check(ems_sparsity_rate(1, n, s.as<float>(), s.as<float>(), zeta, rate.as<double>(), ws.p, ws.n,
+                                    nullptr));
+    detail::check(ems_sync_status(nullptr, ws.p, nullptr));
+    return detail::download_raw<double>(rate.p, 1)[0];
+}
+
+// redundancy_rate_direct, proj/include/ems/analysis.hpp (analysis.cpp:93-118), on the device.
+inline double redundancy_rate_direct(const Matrix& k_raw, const Matrix& v_raw, double tau, int dtype = EMS_F32) {
+    if (k_raw.rows != v_raw.rows || k_raw.rows == 0)
+        throw std::invalid_argument("redundancy_rate_direct: bad token count");
+    const int32_t n = static_cast<int32_t>(k_raw.rows);
+    detail::DevBuf k = detail::upload({&k_raw}, dtype), v = detail::upload({&v_raw}, dtype);
+    detail::DevBuf rate(8), ws(ems_diagnostics_workspace_bytes(1, n));
+    detail::check(ems_redundancy_rate(dtype, static_cast<int32_t>(k_raw.cols), 1, n, k.p, v.p, tau,
+                                      rate.as<double>(), ws.p, ws.n, nullptr));
+    return detail::download_raw<double>(rate.p, 1)[0];
+}
+
 // engine::prefill's per-head work (proj/src/engine.cpp:65-76) for pre-rotated
 // blocks: score + attention on (q_rot, k_rot, v), compress on (k_raw, v).
 // With GQA (q_rot.size() = G * k_raw.size()) the KV head's scores are the mean of

@@ -249,6 +249,54 @@ int ems_oracle_redundancy_cross(const double* k_rows, const double* v_rows, int6
     return EMS_ORACLE_OK;
 }
 
+/* sparsity_rate, analysis.cpp:71-91: the fraction of tokens NOT needed to reach zeta of
+ * the total mass, scanning scores in descending order (cum += s / total, first cum >= zeta). */
+static int cmp_desc_f64(const void* a, const void* b) {
+    const double x = *(const double*)a, y = *(const double*)b;
+    return x > y ? -1 : (x < y);
+}
+int ems_oracle_sparsity_rate(const double* score, int64_t n, double zeta, double* rate) {
+    if (zeta <= 0.0 || zeta > 1.0 || n <= 0) return EMS_ORACLE_INVALID_ARGUMENT;
+    double total = 0.0;
+    for (int64_t i = 0; i < n; ++i) total += score[i];
+    if (total <= 0.0) return EMS_ORACLE_DEGENERATE_INPUT;
+    double* sorted = (double*)malloc((size_t)n * sizeof(double));
+    if (!sorted) return EMS_ORACLE_INVALID_ARGUMENT;
+    memcpy(sorted, score, (size_t)n * sizeof(double));
+    qsort(sorted, (size_t)n, sizeof(double), cmp_desc_f64);
+    double cum = 0.0;
+    int64_t needed = n;
+    for (int64_t i = 0; i < n; ++i) {
+        cum += sorted[i] / total;
+        if (cum >= zeta) {
+            needed = i + 1;
+            break;
+        }
+    }
+    free(sorted);
+    *rate = 1.0 - (double)needed / (double)n;
+    return EMS_ORACLE_OK;
+}
+
+/* redundancy_rate_direct, analysis.cpp:93-118: the fraction of tokens k >= 1 whose best
+ * R = cos(k_k, k_j) cos(v_k, v_j) over the earlier tokens j < k reaches tau. */
+int ems_oracle_redundancy_rate_direct(const double* k, const double* v, int64_t n, int64_t d,
+                                      double tau, double* rate) {
+    if (n <= 0) return EMS_ORACLE_INVALID_ARGUMENT;
+    int64_t redundant = 0;
+#pragma omp parallel for schedule(dynamic, 16) reduction(+ : redundant)
+    for (int64_t t = 1; t < n; ++t) {
+        double best = 0.0;
+        for (int64_t j = 0; j < t; ++j) {
+            const double r = cos_or_zero(k + t * d, k + j * d, d) * cos_or_zero(v + t * d, v + j * d, d);
+            if (j == 0 || r > best) best = r;
+        }
+        if (best >= tau) ++redundant;
+    }
+    *rate = (double)redundant / (double)n;
+    return EMS_ORACLE_OK;
+}
+
 /* assign_merge_destinations, compressor.cpp:76-95 */
 int ems_oracle_assign(const double* r, int64_t n_rows, int64_t n_cols, double tau, int32_t* dest) {
     for (int64_t i = 0; i < n_rows; ++i) {

@@ -108,6 +108,12 @@ int ems_oracle_redundancy_cross(const double* k_rows, const double* v_rows, int6
                                 const double* k_cols, const double* v_cols, int64_t n_cols,
                                 int64_t d, int32_t key_only, double* r);
 
+/* Diagnostics: sparsity_rate (proj/src/analysis.cpp:71-91) of a score vector and
+ * redundancy_rate_direct (:93-118) of raw K/V rows [n][d]. */
+int ems_oracle_sparsity_rate(const double* score, int64_t n, double zeta, double* rate);
+int ems_oracle_redundancy_rate_direct(const double* k, const double* v, int64_t n, int64_t d,
+                                      double tau, double* rate);
+
 /* assign_merge_destinations, proj/src/compressor.cpp:76-95. */
 int ems_oracle_assign(const double* r, int64_t n_rows, int64_t n_cols, double tau, int32_t* dest);
 

@@ -184,6 +184,8 @@ class Oracle:
         L.ems_oracle_redundancy_cross.argtypes = [_dp, _dp, C.c_int64, _dp, _dp, C.c_int64,
                                                   C.c_int64, C.c_int32, _dp]
         L.ems_oracle_assign.argtypes = [_dp, C.c_int64, C.c_int64, C.c_double, _i32p]
+        L.ems_oracle_sparsity_rate.argtypes = [_dp, C.c_int64, C.c_double, C.c_void_p]
+        L.ems_oracle_redundancy_rate_direct.argtypes = [_dp, _dp, C.c_int64, C.c_int64, C.c_double, C.c_void_p]
         L.ems_oracle_compress_prefill.argtypes = [_dp, _dp, _dp, _dp, _dp, C.c_int64, C.c_int64,
                                                   C.POINTER(_CConfig), C.c_int64,
                                                   C.POINTER(_CCache), _dp, _i8p, _i32p]
@@ -264,6 +266,19 @@ class Oracle:
                                                     _ptr(vc), kc.shape[0], kr.shape[1],
                                                     int(key_only), _ptr(r)), "redundancy_cross")
         return r
+
+    def sparsity_rate(self, score, zeta):
+        """sparsity_rate, analysis.cpp:71-91."""
+        score, out = _f64(score), C.c_double()
+        _check(self.lib.ems_oracle_sparsity_rate(_ptr(score), score.size, zeta, C.byref(out)), "sparsity_rate")
+        return out.value
+
+    def redundancy_rate_direct(self, k, v, tau):
+        """redundancy_rate_direct, analysis.cpp:93-118."""
+        k, v, out = _f64(k), _f64(v), C.c_double()
+        _check(self.lib.ems_oracle_redundancy_rate_direct(_ptr(k), _ptr(v), k.shape[0], k.shape[1], tau,
+                                                          C.byref(out)), "redundancy_rate_direct")
+        return out.value
 
     def assign(self, r, tau):
         r = _f64(r)
@@ -371,6 +386,8 @@ class RefLib:
                                                 _dp, _dp, _dp]
         L.ems_ref_three_step_scores.argtypes = [_dp, _dp, C.c_int64, C.c_int64, C.c_int64, _dp, _dp]
         L.ems_ref_effective_score.argtypes = [_dp, _dp, _dp, C.c_int64, C.c_int64, _dp]
+        L.ems_ref_sparsity_rate.argtypes = [_dp, C.c_int64, C.c_double, C.c_void_p]
+        L.ems_ref_redundancy_rate_direct.argtypes = [_dp, _dp, C.c_int64, C.c_int64, C.c_double, C.c_void_p]
         L.ems_ref_compress_prefill.argtypes = [_dp, _dp, _dp, _dp, C.c_int64, C.c_int64, C.c_int64,
                                                C.c_int64, C.c_double, C.c_double, C.c_int64,
                                                C.c_int32]
@@ -400,6 +417,18 @@ class RefLib:
 
     def max_threads(self) -> int:
         return int(self.lib.ems_ref_max_threads())
+
+    def sparsity_rate(self, score, zeta):
+        score, out = _f64(score), C.c_double()
+        self._chk(self.lib.ems_ref_sparsity_rate(_ptr(score), score.size, C.c_double(zeta), C.byref(out)),
+                  "sparsity_rate")
+        return out.value
+
+    def redundancy_rate_direct(self, k, v, tau):
+        k, v, out = _f64(k), _f64(v), C.c_double()
+        self._chk(self.lib.ems_ref_redundancy_rate_direct(_ptr(k), _ptr(v), k.shape[0], k.shape[1], C.c_double(tau),
+                                                          C.byref(out)), "redundancy_rate_direct")
+        return out.value
 
     def prefill_attention(self, q, k, v=None, l_win=32):
         q, k = _f64(q), _f64(k)

@@ -20,6 +20,7 @@
 
 #include <omp.h>
 
+#include "ems/analysis.hpp"
 #include "ems/compressor.hpp"
 #include "ems/engine.hpp"
 #include "ems/errors.hpp"
@@ -118,6 +119,15 @@ int ems_ref_effective_score(const double* glo, const double* loc_past, const dou
         const ems::Vector p = ems::effective_score(s, kernel);
         std::memcpy(out, p.data(), sizeof(double) * n);
     });
+}
+
+int ems_ref_sparsity_rate(const double* score, int64_t n, double zeta, double* rate) {
+    return guarded([&] { *rate = ems::sparsity_rate(ems::Vector(score, score + n), zeta); });
+}
+
+int ems_ref_redundancy_rate_direct(const double* k, const double* v, int64_t n, int64_t d, double tau,
+                                   double* rate) {
+    return guarded([&] { *rate = ems::redundancy_rate_direct(to_matrix(k, n, d), to_matrix(v, n, d), tau); });
 }
 
 // compress_prefill on one head; the resulting HeadCacheState is returned as

@@ -50,6 +50,11 @@ size_t decode_workspace_bytes(const Dims& m, int R);
 cudaError_t launch_redundancy_cross(int dtype, int d, const void* kr, const void* vr, int nr,
                                     const void* kc, const void* vc, int nc, int key_only,
                                     float* r, cudaStream_t s);
+size_t diag_workspace_bytes(int units, int L);
+cudaError_t launch_sparsity(int units, int L, const float* glo, const float* loc, double zeta, double* rate,
+                            void* ws, int unit_base, cudaStream_t s);
+cudaError_t launch_redundancy(int units, int L, int d, int dtype, const void* k, const void* v, double tau,
+                              double* rate, void* ws, cudaStream_t s);
 
 namespace {
 thread_local char g_err[1024] = "";
@@ -517,6 +522,55 @@ int ems_redundancy_cross(int32_t dtype, int32_t d, const void* k_rows, const voi
                                             n_cols, key_only, r, s);
     if (e != cudaSuccess) {
         set_error("redundancy_cross launch: %s", cudaGetErrorString(e));
+        return EMS_CUDA_ERROR;
+    }
+    return EMS_OK;
+}
+
+size_t ems_diagnostics_workspace_bytes(int32_t units, int32_t L) {
+    if (units <= 0 || L <= 0) return 0;
+    return ems::diag_workspace_bytes(units, L);
+}
+
+int ems_sparsity_rate(int32_t units, int32_t L, const float* glo, const float* loc, double zeta, double* rate,
+                      void* ws, size_t ws_bytes, cudaStream_t s) {
+    using namespace ems;
+    if (units <= 0 || L <= 0 || !glo || !loc || !rate || !ws) {
+        set_error("ems_sparsity_rate: bad arguments");
+        return EMS_INVALID_ARGUMENT;
+    }
+    if (!(zeta > 0.0 && zeta <= 1.0)) {  // analysis.cpp:72-74
+        set_error("sparsity_rate: zeta must be in (0, 1]");
+        return EMS_INVALID_ARGUMENT;
+    }
+    if (ws_bytes < diag_workspace_bytes(units, L)) {
+        set_error("ems_sparsity_rate: workspace too small (%zu < %zu)", ws_bytes, diag_workspace_bytes(units, L));
+        return EMS_INVALID_ARGUMENT;
+    }
+    cudaError_t e = launch_sparsity(units, L, glo, loc, zeta, rate, ws, 0, s);
+    if (e != cudaSuccess) {
+        set_error("sparsity launch: %s", cudaGetErrorString(e));
+        return EMS_CUDA_ERROR;
+    }
+    return EMS_OK;
+}
+
+int ems_redundancy_rate(int32_t dtype, int32_t d, int32_t units, int32_t L, const void* k, const void* v,
+                        double tau, double* rate, void* ws, size_t ws_bytes, cudaStream_t s) {
+    using namespace ems;
+    if ((dtype != EMS_F32 && dtype != EMS_BF16) || !supported_dim(d) || units <= 0 || L <= 0 || !k || !v ||
+        !rate || !ws) {
+        set_error("ems_redundancy_rate: bad arguments");
+        return EMS_INVALID_ARGUMENT;
+    }
+    if (ws_bytes < diag_workspace_bytes(units, L)) {
+        set_error("ems_redundancy_rate: workspace too small (%zu < %zu)", ws_bytes,
+                  diag_workspace_bytes(units, L));
+        return EMS_INVALID_ARGUMENT;
+    }
+    cudaError_t e = launch_redundancy(units, L, d, dtype, k, v, tau, rate, ws, s);
+    if (e != cudaSuccess) {
+        set_error("redundancy launch: %s", cudaGetErrorString(e));
         return EMS_CUDA_ERROR;
     }
     return EMS_OK;

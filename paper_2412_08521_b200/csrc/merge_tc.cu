@@ -85,6 +85,7 @@ __global__ void __launch_bounds__(256) gather_kernel(
 
 // ------------------------------------------------------------------ similarity + argmax
 constexpr int kStages = 2;
+static_assert(kStages == 2, "stage s of tile c is TMEM buffer c & 1 (the producer waits on d_empty[s])");
 constexpr int kThreads = 384;  // w0 TMA, w1 MMA, w4-7 epilogue A, w8-11 epilogue B
 constexpr size_t kSmem = 1024 + 2 * kTileBytes + kStages * (2 * kTileBytes + 1024) + 2 * 128 * 8;
 
@@ -157,7 +158,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_load_3d(svt + 16384, &tvt, &bars.t_full, 64, t0, u);
             for (int c = 0; c < n_ct; ++c) {
                 const int s = c % kStages;
-                if (c >= kStages) mbar_wait(&bars.c_empty[s], ((c / kStages) - 1) & 1);
+                if (c >= kStages) {
+                    mbar_wait(&bars.c_empty[s], ((c / kStages) - 1) & 1);
+                    // the epilogue of tile c - 2 still reads this stage's column norms
+                    mbar_wait(&bars.d_empty[s], ((c >> 1) - 1) & 1);
+                }
                 uint8_t* st = sring + s * (2 * kTileBytes + 1024);
                 mbar_expect_tx(&bars.c_full[s], 2 * kTileBytes + 1024);
                 tma_load_3d(st, &tkc, &bars.c_full[s], 0, c * 128, u);

@@ -120,6 +120,11 @@ def lib() -> C.CDLL:
         L.ems_redundancy_cross.argtypes = [C.c_int32, C.c_int32, vp, vp, C.c_int32, vp, vp,
                                            C.c_int32, C.c_int32, fp, vp]
         L.ems_sync_status.argtypes = [C.POINTER(Desc), vp, vp]
+        L.ems_diagnostics_workspace_bytes.restype = C.c_size_t
+        L.ems_diagnostics_workspace_bytes.argtypes = [C.c_int32, C.c_int32]
+        L.ems_sparsity_rate.argtypes = [C.c_int32, C.c_int32, fp, fp, C.c_double, vp, vp, C.c_size_t, vp]
+        L.ems_redundancy_rate.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_int32, vp, vp, C.c_double, vp, vp,
+                                          C.c_size_t, vp]
         L.ems_prefill_host.argtypes = [C.POINTER(Desc), C.c_double, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,
                                        fp, fp, fp, C.POINTER(CCache), C.POINTER(CCache), C.c_int32, vp,
                                        C.c_size_t, vp, vp]
@@ -166,6 +171,7 @@ class EmsConfig:
     policy: str = "ems"      # PolicyHandle::kind: ems | full | streaming | h2o | snapkv
     sink_count: int = 4      # PolicyHandle::sink_count (streaming)
     position_mode: str = "with_pos"  # decode expansion RoPE (cache.hpp:11): with_pos | without_pos
+    zeta: float = 0.95       # sparsity mass fraction (diagnostics only), (0, 1]
 
     def center_capacity(self) -> int:
         return self.n_budget - self.l_win
@@ -444,6 +450,46 @@ def redundancy_cross(k_rows, v_rows, k_cols, v_cols, key_only=False) -> torch.Te
     _check(lib().ems_redundancy_cross(_dtype_code(k_rows.dtype), d, _p(k_rows), _p(v_rows), nr,
                                       _p(k_cols), _p(v_cols), nc, int(key_only), _p(r), _stream()))
     return r
+
+
+def _diag_ws(units: int, L: int, device) -> torch.Tensor:
+    return torch.empty(lib().ems_diagnostics_workspace_bytes(units, L), dtype=torch.uint8, device=device)
+
+
+def sparsity_rate(glo: torch.Tensor, loc: torch.Tensor, zeta: float) -> torch.Tensor:
+    """sparsity_rate(combine_glo_loc(glo, loc), zeta) (analysis.cpp:71-91, scoring.cpp:105-124)
+    for every sequence of glo / loc [..., L] fp32 -> fp64 [...] on the device."""
+    L = glo.shape[-1]
+    units = glo.numel() // max(L, 1)
+    rate = torch.empty(glo.shape[:-1], dtype=torch.float64, device=glo.device)
+    ws = _diag_ws(units, L, glo.device)
+    glo, loc = glo.float().contiguous(), loc.float().contiguous()
+    _check(lib().ems_sparsity_rate(units, L, _p(glo), _p(loc), float(zeta), _p(rate), _p(ws), ws.numel(),
+                                   _stream()))
+    _check(lib().ems_sync_status(None, _p(ws), _stream()))
+    return rate
+
+
+def redundancy_rate(k_raw: torch.Tensor, v_raw: torch.Tensor, tau: float) -> torch.Tensor:
+    """redundancy_rate_direct(k_raw, v_raw, tau) (analysis.cpp:93-118) for every sequence of
+    k / v [..., L, d] -> fp64 [...] on the device."""
+    L, d = k_raw.shape[-2], k_raw.shape[-1]
+    units = k_raw.numel() // max(L * d, 1)
+    rate = torch.empty(k_raw.shape[:-2], dtype=torch.float64, device=k_raw.device)
+    ws = _diag_ws(units, L, k_raw.device)
+    k_raw, v_raw = k_raw.contiguous(), v_raw.contiguous()
+    _check(lib().ems_redundancy_rate(_dtype_code(k_raw.dtype), d, units, L, _p(k_raw), _p(v_raw), float(tau),
+                                     _p(rate), _p(ws), ws.numel(), _stream()))
+    return rate
+
+
+def analyze(q, k, v, cfg: EmsConfig, rope_base: float = 10000.0):
+    """analyze_trace (proj/src/experiment.cpp:133-150) on raw [B][H][L][d] device tensors:
+    RoPE, prefill_scores with min(l_win, L), sparsity of the combined score and redundancy of
+    the raw K/V per unit.  Returns (sparsity, redundancy), fp64 [B][H_kv]."""
+    L = q.shape[2]
+    glo, loc = prefill_scores(rope(q.contiguous(), rope_base), rope(k.contiguous(), rope_base), min(cfg.l_win, L))
+    return sparsity_rate(glo, loc, cfg.zeta), redundancy_rate(k, v, cfg.tau)
 
 
 class DecodeState:

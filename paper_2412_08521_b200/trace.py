@@ -176,7 +176,7 @@ def _cos_error(a, b) -> float:  # concat_cos_error, experiment.cpp:97-120
 
 
 def run_experiment(tr: Trace, cfg, label: str = "", needle_pos: int | None = None, rope_base: float = 10000.0,
-                   device="cuda", policies=None) -> dict:
+                   device="cuda", policies=None, compute_diagnostics: bool = True) -> dict:
     """run_experiment_multi (experiment.cpp:152-264): the compressed engine on the GPU, once per
     policy (``policies`` = policy names, default ``[cfg.policy]``), against one dense run."""
     import dataclasses
@@ -190,6 +190,10 @@ def run_experiment(tr: Trace, cfg, label: str = "", needle_pos: int | None = Non
     n = tr.prefill_tokens
     ref_pre, ref_outs, ref_am = _dense_reference(q, k, v, n, rope_base, device)
     t = lambda a: torch.tensor(np.ascontiguousarray(a), dtype=torch.float32, device=device)  # noqa: E731
+    diags = []
+    if compute_diagnostics:  # analyze_trace (experiment.cpp:133-150) on the prompt
+        sp, rd = ems.analyze(t(q[None, :, :n]), t(k[None, :, :n]), t(v[None, :, :n]), cfg, rope_base)
+        diags = [dict(head=h, sparsity=float(sp[0, h]), redundancy=float(rd[0, h])) for h in range(H)]
     reports = []
     for pol in (policies or [cfg.policy]):
         pc = dataclasses.replace(cfg, policy=pol)
@@ -226,10 +230,10 @@ def run_experiment(tr: Trace, cfg, label: str = "", needle_pos: int | None = Non
             in_lut = all(_position_represented(ds.unit_cache(h), needle_pos) for h in range(H))
             needle = dict(position=int(needle_pos), retained=retained and bool(dec), in_lut_final=in_lut)
         reports.append(dict(policy=pol, compression_applied=bool(plan.cache["counts"][0, 3].item()), steps=steps,
-                            aggregate=agg, needle=needle, diagnostics=[]))
+                            aggregate=agg, needle=needle, diagnostics=diags))
     return {"schema_version": 1,
             "trace": dict(label=label, num_heads=H, head_dim=d, prefill_tokens=n, decode_steps=T - n),
-            "config": dict(n_budget=cfg.n_budget, l_win=cfg.l_win, tau=cfg.tau, gamma=cfg.gamma, zeta=0.95,
+            "config": dict(n_budget=cfg.n_budget, l_win=cfg.l_win, tau=cfg.tau, gamma=cfg.gamma, zeta=cfg.zeta,
                            kernel_size=cfg.kernel_size, position_mode=cfg.position_mode,
                            eviction="zero_class" if cfg.zero_class else "explicit_removal"),
             "policies": reports}

@@ -120,6 +120,28 @@ int main() {
     for (std::size_t i = 0; i < rr.size(); ++i) re = std::max(re, std::abs(r.data[i] - rr[i]));
     CHECK(re < 1e-5, "redundancy abs err %g", re);
 
+    // --- diagnostics (analysis.cpp:71-118) vs the oracle restatement
+    {
+        Vector sc(300);
+        for (std::size_t i = 0; i < sc.size(); ++i) sc[i] = (double)(float)(0.001 + (double)((i * 7919) % 997) / 997.0);
+        for (double zeta : {0.1, 0.5, 0.95}) {
+            double want = 0.0;
+            ems_oracle_sparsity_rate(sc.data(), (int64_t)sc.size(), zeta, &want);
+            CHECK(sparsity_rate(sc, zeta) == want, "sparsity_rate zeta %g", zeta);
+        }
+        bool threw = false;
+        try {
+            sparsity_rate(Vector(8, 0.0), 0.5);
+        } catch (const DegenerateInputError&) {
+            threw = true;
+        }
+        CHECK(threw, "sparsity_rate of a zero score must throw DegenerateInputError");
+        double want_r = 0.0;
+        const double got_r = redundancy_rate_direct(k, v, 0.2);
+        ems_oracle_redundancy_rate_direct(k.data.data(), v.data.data(), (int64_t)n, (int64_t)d, 0.2, &want_r);
+        CHECK(std::abs(got_r - want_r) * n <= 1.0, "redundancy_rate_direct %g vs %g", got_r, want_r);
+    }
+
     // --- baseline policies (policies.cpp:131-180) vs the oracle restatement
     {
         const PolicyKind kinds[] = {PolicyKind::full, PolicyKind::streaming_llm, PolicyKind::h2o,

@@ -180,6 +180,20 @@ __global__ void __launch_bounds__(512, 1) micro_kernel(int kind, int iters, long
                 float2 y = ex2_poly2(a2[i]);
                 a2[i] = make_float2(-0.5f * y.x, -0.5f * y.y);
             }
+    } else if (kind == 6 || kind == 7) {
+        // packed exp2: 6 = ex2.approx.f16x2, 7 = ex2.approx.ftz.bf16x2 (2 results per lane)
+        uint32_t p[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) p[i] = __float_as_uint(acc[i]) & 0x3b003b00u;
+        for (int it = 0; it < iters; ++it)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                if (kind == 6) asm volatile("ex2.approx.f16x2 %0, %0;" : "+r"(p[i]));
+                else asm volatile("ex2.approx.ftz.bf16x2 %0, %0;" : "+r"(p[i]));
+                p[i] ^= 0x80008000u;
+            }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] = __uint_as_float(p[i]);
     }
     const long long t1 = clock64();
     float s = 0.f;

@@ -184,13 +184,17 @@ def test_gpu_redundancy_cross_matches_oracle(oracle):
     assert abs(r[5, 7] - 1.0) < 1e-5 and np.all(r[:, 3] == 0.0)
 
 
-@pytest.mark.parametrize("wname,L,key_only", [("cfgM", 2048, False), ("cfgM", 2048, True), ("cfg3b", 4096, False)])
-def test_gpu_tc_merge_matches_simt_and_oracle(wname, L, key_only, oracle):
-    """Tensor-core similarity/argmax (merge_tc.cu) vs the SIMT kernels and the oracle."""
+@pytest.mark.parametrize("wname,L,key_only,budget", [("cfgM", 2048, False, None), ("cfgM", 2048, True, None),
+                                                    ("cfg3b", 4096, False, None), ("cfgM", 4096, False, 1024)])
+def test_gpu_tc_merge_matches_simt_and_oracle(wname, L, key_only, budget, oracle):
+    """Tensor-core similarity/argmax (merge_tc.cu) vs the SIMT kernels and the oracle; the
+    budget-1024 merge case streams 8 center tiles through the 2-stage ring (stage reuse)."""
     w = CONFIGS[wname]
     units = [make_unit_np(w, seed=5, seq_len=L, unit=u) for u in range(2)]
     cfg = _cfg_of(w)
     cfg.key_only = key_only
+    if budget:
+        cfg.n_budget = budget
     a = run_gpu(units, w.dtype, cfg, score_impl="auto")
     b = run_gpu(units, w.dtype, cfg, score_impl="simt")
     for i, un in enumerate(units):

@@ -42,6 +42,7 @@ def test_golden_report(reflib, tmp_path):
         assert abs(g["cos_error"] - w["cos_error"]) <= 1e-5 + 1e-4 * abs(w["cos_error"]), g
     for key in ("mean_l2", "max_l2", "mean_cos_error", "argmax_match_rate"):
         assert abs(got_p["aggregate"][key] - want_p["aggregate"][key]) <= 1e-4 * max(1.0, abs(want_p["aggregate"][key]))
+    assert got_p["diagnostics"] == want_p["diagnostics"]  # analyze_trace: sparsity / redundancy per head
     csv = kv.report_csv(rep).splitlines()
     assert csv[0] == "policy,step,l2_error,cos_error,entries,bytes,argmax_match" and len(csv) == 6
 
