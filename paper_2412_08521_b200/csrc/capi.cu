@@ -682,9 +682,17 @@ extern "C" int ems_prefill_host(const ems_desc* d, double rope_base, const void*
     // the copy stream must not overwrite device inputs that earlier work on `s` still reads
     EMS_CUDA_CHECK(cudaEventRecord(ev[2 * nc], s));
     EMS_CUDA_CHECK(cudaStreamWaitEvent(cs, ev[2 * nc], 0));
+    // Geometric groups (U / 2^(nc-1), ..., U / 4, U / 2 units): the first group's inputs land
+    // after a small copy, so compute starts early; later groups are large (efficient grids)
+    // and their copies finish while earlier groups compute.
+    auto group_end = [&](int c) {
+        if (c >= nc - 1) return U;
+        const long long e = ((long long)U + (1ll << (nc - 1 - c)) - 1) >> (nc - 1 - c);
+        return (int)(e < c + 1 ? c + 1 : e);
+    };
     auto unit_range = [&](int c, int& u0, int& n) {
-        u0 = (int)((long long)U * c / nc);
-        n = (int)((long long)U * (c + 1) / nc) - u0;
+        u0 = c == 0 ? 0 : group_end(c - 1);
+        n = group_end(c) - u0;
     };
     // (1) H2D of every chunk, in chunk order (score inputs first, the raw K of a pre-rotated
     //     problem last since only the merge/compact stages read it)
