@@ -27,8 +27,11 @@ namespace ems {
 
 namespace {
 
-constexpr int kT = 256;  // threads per CTA
-constexpr int kWarps = kT / 32;
+// threads per CTA: 512 when there are few units (the per-unit phases are latency-bound, more
+// warps per unit help), 256 when the grid already fills the SMs; reductions use the
+// launched width, so results are a function of the problem shape only (deterministic)
+constexpr int kTMax = 512;
+constexpr int kWarpsMax = kTMax / 32;
 
 struct DecArgs {
     int G, d, S, W, T, R;          // query heads per unit; capacities: slots, locals, LUT, rows
@@ -69,7 +72,7 @@ __device__ double bsum(double v, double* sh) {
     if (l == 0) sh[w] = v;
     __syncthreads();
     double t = 0.0;
-    for (int i = 0; i < kWarps; ++i) t += sh[i];
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += sh[i];
     __syncthreads();
     return t;
 }
@@ -80,7 +83,7 @@ __device__ float bmax(float v, float* sh) {
     if (l == 0) sh[w] = v;
     __syncthreads();
     float t = -FLT_MAX;
-    for (int i = 0; i < kWarps; ++i) t = fmaxf(t, sh[i]);
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t = fmaxf(t, sh[i]);
     __syncthreads();
     return t;
 }
@@ -106,7 +109,7 @@ __device__ Cand bselect(Cand c, Better better, Cand* sh) {
     if (l == 0) sh[w] = c;
     __syncthreads();
     Cand t = sh[0];
-    for (int i = 1; i < kWarps; ++i)
+    for (int i = 1; i < (int)(blockDim.x >> 5); ++i)
         if (better(sh[i], t)) t = sh[i];
     __syncthreads();
     return t;
@@ -124,7 +127,7 @@ __device__ int bscan(int x, int* sh, int* tot) {
     if (l == 31) sh[w] = inc;
     __syncthreads();
     int base = 0, all = 0;
-    for (int i = 0; i < kWarps; ++i) {
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
         if (i < w) base += sh[i];
         all += sh[i];
     }
@@ -139,16 +142,17 @@ __device__ __forceinline__ double combined(const double* sc, double align) {
     return fmax(sc[0] * align, sc[1] + sc[2]);
 }
 
-__global__ void __launch_bounds__(kT) decode_step_kernel(DecArgs a) {
+__global__ void __launch_bounds__(kTMax) decode_step_kernel(DecArgs a) {
     extern __shared__ __align__(16) unsigned char dsm[];
     const int u = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int kT = blockDim.x, kWarps = kT >> 5;
     const int d = a.d, S = a.S, W = a.W, T = a.T, G = a.G, pairs = d / 2;
     double* acc = reinterpret_cast<double*>(dsm);                  // [max(S + W, 8 d)] owner mass / R / partials
     float* qrot = reinterpret_cast<float*>(acc + max(S + W, kWarps * d));  // [G][d]
-    __shared__ double shd[kWarps];
-    __shared__ float shf[kWarps];
-    __shared__ Cand shc[kWarps];
-    __shared__ int shi[kWarps];
+    __shared__ double shd[kWarpsMax];
+    __shared__ float shf[kWarpsMax];
+    __shared__ Cand shc[kWarpsMax];
+    __shared__ int shi[kWarpsMax];
     __shared__ int s_meta[8];
     __shared__ double s_w[4];
     __shared__ int s_i[4];
@@ -688,13 +692,14 @@ cudaError_t launch_decode_step(const Dims& m, int dtype, int S, int W, int T, in
     a.row_pos = reinterpret_cast<int32_t*>(take(U * R * 4));
     a.probs = reinterpret_cast<float*>(take(U * m.G * R * 4));
     a.pmean = reinterpret_cast<float*>(take(U * R * 4));
-    const size_t smem = (size_t)max(S + W, kWarps * m.d) * 8 + (size_t)m.G * m.d * 4;
+    const int threads = m.units >= 148 ? 256 : kTMax;
+    const size_t smem = (size_t)max(S + W, (threads / 32) * m.d) * 8 + (size_t)m.G * m.d * 4;
     static size_t attr = 0;
     if (smem > 48 * 1024 && smem > attr) {
         cudaFuncSetAttribute(decode_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = smem;
     }
-    decode_step_kernel<<<m.units, kT, smem, s>>>(a);
+    decode_step_kernel<<<m.units, threads, smem, s>>>(a);
     return cudaGetLastError();
 }
 
