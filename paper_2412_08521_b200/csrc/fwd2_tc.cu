@@ -45,6 +45,7 @@ struct Fwd2Args {
     int debug;  // profiling only: 1 = no softmax math (P = 0), 2 = no MMAs
     const float* kmax;  // [units][nT2] max ||k|| over each 256-key tile (Cauchy-Schwarz bound)
     int nT2;
+    const __nv_bfloat16* q;  // [planes][L][128]: |q_row| for the bound, read before the first S
 };
 
 struct Bars2 {
@@ -192,28 +193,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT2, 1)
         const uint32_t sO = tO + lane_off + 32 * q;
         const uint32_t s_free_l = mapa(smem_u32(&bars.s_free), 0);
         const uint32_t p_full_l = mapa(smem_u32(&bars.p_full), 0);
-        float m_ref = -INFINITY, l = 0.f, qn = 0.f;
+        float m_ref = -INFINITY, l = 0.f, qn;
         int n_x = 0;  // max exchanges so far (selects the xch buffer; identical across a row's quarters)
+        {  // |q_row| before the first S arrives (off the critical path): quarter q sums dims
+           // [32q, 32q + 32) from global memory, the four partials combine in a fixed order
+            const uint4* qr = reinterpret_cast<const uint4*>(a.q + ((size_t)plane * a.L + qrow) * kD + 32 * q);
+            float ss = 0.f;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const uint4 w4 = qr[c];
+                const uint32_t wv[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const float lo = __uint_as_float(wv[t] << 16), hi = __uint_as_float(wv[t] & 0xFFFF0000u);
+                    ss = fmaf(lo, lo, fmaf(hi, hi, ss));
+                }
+            }
+            const uint32_t xs = smem_u32(xch + 512);  // buffer 1: the first max exchange uses buffer 0
+            sts32(xs + 4 * (q * 128 + m), ss);
+            asm volatile("bar.sync %0, 128;" ::"r"(1 + wi) : "memory");  // the 4 warps sharing these rows
+            qn = sqrtf((lds32(xs + 4 * m) + lds32(xs + 4 * (128 + m))) +
+                       (lds32(xs + 4 * (256 + m)) + lds32(xs + 4 * (384 + m)))) * 1.0001f;  // rounding margin
+        }
+        const float* kmu = a.kmax + (size_t)unit * a.nT2;
+        float km = jmax >= 1 ? kmu[1] : 0.f;  // bound of tile j, loaded one iteration ahead
         for (int j = 0; j <= jmax; ++j) {
+            const float km_j = km;
+            if (j + 1 <= jmax) km = kmu[j + 1];
             mbar_wait(&bars.s_full, j & 1);
             tc_fence_after();
-            if (j == 0) {  // |q_row| from the (swizzled) smem tile: the norm is order-free
-                float ss = 0.f;
-#pragma unroll
-                for (int bx = 0; bx < 2; ++bx)
-#pragma unroll
-                    for (int ch = 0; ch < 8; ++ch) {
-                        const float4 w4 = lds128(smem_u32(sq + bx * 16384 + m * 128 + ch * 16));
-                        const uint32_t wv[4] = {__float_as_uint(w4.x), __float_as_uint(w4.y), __float_as_uint(w4.z),
-                                                __float_as_uint(w4.w)};
-#pragma unroll
-                        for (int t = 0; t < 4; ++t) {
-                            const float lo = __uint_as_float(wv[t] << 16), hi = __uint_as_float(wv[t] & 0xFFFF0000u);
-                            ss = fmaf(lo, lo, fmaf(hi, hi, ss));
-                        }
-                    }
-                qn = sqrtf(ss) * 1.0001f;  // rounding margin
-            }
             uint32_t r[2][32];
             tmem_ld32(sS, r[0]);
             tmem_ld32(sS + 32, r[1]);
@@ -246,7 +254,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT2, 1)
             // warp-uniform (the exchange below is a named barrier); the four warps sharing these rows
             // see the same rows, hence the same vote
             const bool skip =
-                __all_sync(0xffffffffu, j > 0 && qn * a.kmax[(size_t)unit * a.nT2 + j] * a.c <= m_ref + kSkip);
+                __all_sync(0xffffffffu, j > 0 && qn * km_j * a.c <= m_ref + kSkip);
             float corr = 1.f;
             bool warp_need = false;
             if (!skip) {
@@ -385,7 +393,7 @@ bool fwd2_tc_supported(int G, int nT) { return (G >= 2 && G % 2 == 0) || (G == 1
 
 cudaError_t launch_fwd2_tc(int L, int Hq, int Hkv, int G, int units, float c, void* out, float* nlse2,
                            float* lse_nat, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
-                           const void* k, float* kmax, cudaStream_t s) {
+                           const void* k, float* kmax, cudaStream_t s, const void* q) {
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(fwd2_tc_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem2);
@@ -416,6 +424,7 @@ cudaError_t launch_fwd2_tc(int L, int Hq, int Hkv, int G, int units, float c, vo
     a.debug = dbg;
     a.nT2 = (L + 255) / 256;
     a.kmax = kmax;
+    a.q = static_cast<const __nv_bfloat16*>(q);
     key_tile_norm_kernel<<<units * a.nT2, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(k), L, a.nT2, kmax);
     const int pairs = G >= 2 ? a.nT * units * (G / 2) : (a.nT / 2) * units;
     switch (poly) {

@@ -422,7 +422,7 @@ cudaError_t score_tc(const Dims& dm, const void* q, const void* k, const void* v
     if (p1 == 2 && fwd2_tc_supported(dm.G, fa.nT)) {
         float* kmax = reinterpret_cast<float*>(static_cast<char*>(ws) + nlse2_bytes(dm) + part_bytes(dm));
         cudaError_t e = launch_fwd2_tc(dm.L, dm.Hq, dm.Hkv, dm.G, dm.units, fa.c, o, nlse2, lse, tq, tk, tv, k,
-                                       kmax, s);
+                                       kmax, s, q);
         if (e != cudaSuccess) return e;
     } else
     switch (poly) {

@@ -52,7 +52,7 @@ bool fwd2_tc_supported(int G, int nT);
 size_t fwd2_workspace(int units, int L);
 cudaError_t launch_fwd2_tc(int L, int Hq, int Hkv, int G, int units, float c, void* out, float* nlse2,
                            float* lse_nat, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
-                           const void* k, float* kmax, cudaStream_t s);
+                           const void* k, float* kmax, cudaStream_t s, const void* q);
 cudaError_t launch_colsum2_tc(const sc::ColArgs& a, const CUtensorMap& tk, const CUtensorMap& tq,
                               cudaStream_t s);
 
