@@ -34,7 +34,8 @@ constexpr float kSkip = 64.0f;
 constexpr int kT2 = 576;  // w0 TMA, w1 MMA (leader), w2-17 softmax (warpgroup q = keys [64q, 64q+64))
 constexpr int kStages2 = 2;
 // Q 32 KB | K stages (this CTA's 128-key half) | V stages (256 keys x this CTA's 64 d cols)
-constexpr size_t kSmem2 = 1024 + kTileBytes + 2 * kStages2 * kTileBytes + 2 * 4 * 128 * 4;
+constexpr int kMaxT2 = 1024;  // 256-key tiles per sequence (L <= 262144) for the smem key bounds
+constexpr size_t kSmem2 = 1024 + kTileBytes + 2 * kStages2 * kTileBytes + 2 * 4 * 128 * 4 + kMaxT2 * 4;
 
 struct Fwd2Args {
     int L, Hq, Hkv, G, nT, units;
@@ -90,6 +91,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT2, 1)
     uint8_t* sk = sq + kTileBytes;                      // stages x 32 KB: 128 keys x 128 d
     uint8_t* sv = sk + kStages2 * kTileBytes;           // stages x 32 KB: 256 keys x 64 d
     float* xch = reinterpret_cast<float*>(sv + kStages2 * kTileBytes);  // [2 buf][4 quarters][128]
+    float* skm = xch + 2 * 4 * 128;  // [kMaxT2]: per-256-key-tile bounds of this unit
     __shared__ Bars2 bars;
 
     const int tid = threadIdx.x, warp = tid >> 5;
@@ -211,15 +213,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT2, 1)
             }
             const uint32_t xs = smem_u32(xch + 512);  // buffer 1: the first max exchange uses buffer 0
             sts32(xs + 4 * (q * 128 + m), ss);
+            for (int t = tid - 64; t <= jmax; t += kT2 - 64) skm[t] = a.kmax[(size_t)unit * a.nT2 + t];
+            asm volatile("bar.sync 5, %0;" ::"n"(kT2 - 64) : "memory");  // all softmax warps
             asm volatile("bar.sync %0, 128;" ::"r"(1 + wi) : "memory");  // the 4 warps sharing these rows
             qn = sqrtf((lds32(xs + 4 * m) + lds32(xs + 4 * (128 + m))) +
                        (lds32(xs + 4 * (256 + m)) + lds32(xs + 4 * (384 + m)))) * 1.0001f;  // rounding margin
         }
-        const float* kmu = a.kmax + (size_t)unit * a.nT2;
-        float km = jmax >= 1 ? kmu[1] : 0.f;  // bound of tile j, loaded one iteration ahead
+        const uint32_t skm_a = smem_u32(skm);
         for (int j = 0; j <= jmax; ++j) {
-            const float km_j = km;
-            if (j + 1 <= jmax) km = kmu[j + 1];
+            const float km_j = lds32(skm_a + 4 * j);
             mbar_wait(&bars.s_full, j & 1);
             tc_fence_after();
             uint32_t r[2][32];
@@ -389,7 +391,9 @@ __global__ void key_tile_norm_kernel(const __nv_bfloat16* __restrict__ k, int L,
 
 size_t fwd2_workspace(int units, int L) { return sizeof(float) * (size_t)units * ((L + 255) / 256); }
 
-bool fwd2_tc_supported(int G, int nT) { return (G >= 2 && G % 2 == 0) || (G == 1 && nT % 2 == 0); }
+bool fwd2_tc_supported(int G, int nT) {
+    return ((G >= 2 && G % 2 == 0) || (G == 1 && nT % 2 == 0)) && (nT + 1) / 2 <= kMaxT2;
+}
 
 cudaError_t launch_fwd2_tc(int L, int Hq, int Hkv, int G, int units, float c, void* out, float* nlse2,
                            float* lse_nat, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
