@@ -433,11 +433,15 @@ __global__ void __cluster_dims__(kClu, 1, 1) __launch_bounds__(kCThreads) select
 cudaError_t launch_select(const Dims& dm, int l_win, int n_imp, int n_tbm, int kernel,
                           const float* glo, const float* loc, const ems_stage& sg,
                           DevStatus* status, cudaStream_t s, int policy, int sink, int n_budget) {
-    static const int clustered = [] {
-        const char* e = getenv("EMS_SELECT_CLUSTER");  // A/B override
-        return e ? atoi(e) : 1;
+    static const int forced = [] {
+        const char* e = getenv("EMS_SELECT_CLUSTER");  // A/B override: 0 never, 1 always
+        return e ? atoi(e) : -1;
     }();
-    if (clustered && dm.L >= 8 * kClu) {
+    // The cluster kernel pays for its cross-CTA exchanges with 8x the parallelism per unit:
+    // worth it for long sequences when few units leave most SMs idle (config 3: 121 -> 35 us);
+    // with many units the one-CTA-per-unit grid already fills the GPU (config 2: 20 vs 109 us).
+    const bool auto_cluster = dm.L >= 8192 && (long long)dm.units * kClu <= 2 * 148;
+    if ((forced < 0 ? auto_cluster : forced != 0) && dm.L >= 8 * kClu) {
         select_cluster_kernel<<<dm.units * kClu, kCThreads, 0, s>>>(
             glo, loc, dm.L, l_win, n_imp, n_tbm, kernel, sg.pooled, sg.cls, sg.imp_idx, sg.tbm_idx, sg.part_counts,
             dm.cap_c, dm.cap_tbm, status, dm.unit_base, policy, sink, n_budget);

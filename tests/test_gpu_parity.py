@@ -203,3 +203,16 @@ def test_gpu_tc_merge_matches_simt_and_oracle(wname, L, key_only, budget, oracle
         check_unit(b, i, un, ref, ref.extra["glo"], ref.extra["loc"], w.dtype, cfg, oracle)
         if wname == "cfgM":
             assert rep["merged"] > 0
+
+
+@pytest.mark.parametrize("forced", ["0", "1"])
+def test_gpu_select_variants_forced(forced):
+    """Both select kernels (one CTA per unit / the 8-CTA cluster) against the oracle on every
+    config case; the launch picks one by shape, so each is forced once in a fresh process."""
+    import subprocess
+    import sys
+    env = dict(os.environ, EMS_SELECT_CLUSTER=forced)
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider", __file__,
+                        "-k", "configs_vs_oracle or golden_cache or reference_cases"],
+                       env=env, capture_output=True, text=True, cwd=os.path.dirname(os.path.dirname(__file__)))
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
