@@ -226,7 +226,9 @@ __global__ void __launch_bounds__(kTMax) decode_step_kernel(DecArgs a) {
         n_rows = base + count;
     }
     __syncthreads();
-    // 4. logits: one warp per row, lanes over RoPE pairs; all G heads share the key
+    // 4. logits: one warp per row, lanes over RoPE pairs; all G heads share the key.  The G
+    //    (<= 8) per-lane partial dot products are reduced together in 9 shuffles (each step
+    //    halves the values a lane carries), leaving head h's sum in lanes 4h' .. (fixed order).
     const float scale = rsqrtf((float)d);
     for (int r = warp; r < n_rows; r += kWarps) {
         const int o = rown[r];
@@ -238,19 +240,41 @@ __global__ void __launch_bounds__(kTMax) decode_step_kernel(DecArgs a) {
 #pragma unroll
         for (int h = 0; h < 8; ++h) part[h] = 0.f;
         for (int p = lane; p < pairs; p += 32) {
-            const float k0 = kb[2 * p] * kn, k1 = kb[2 * p + 1] * kn;
+            const float2 kk = reinterpret_cast<const float2*>(kb)[p];
+            const float k0 = kk.x * kn, k1 = kk.y * kn;
             const float2 cs = a.table[(size_t)rp * pairs + p];
             const float r0 = k0 * cs.x - k1 * cs.y, r1 = k0 * cs.y + k1 * cs.x;
 #pragma unroll
             for (int h = 0; h < 8; ++h)
-                if (h < G) part[h] += qrot[h * d + 2 * p] * r0 + qrot[h * d + 2 * p + 1] * r1;
+                if (h < G) {
+                    const float2 qq = reinterpret_cast<const float2*>(qrot + h * d)[p];
+                    part[h] += qq.x * r0 + qq.y * r1;
+                }
+        }
+        // transpose-reduce: after the xor-16/8/4 steps lane L holds head
+        // 4*bit4(L) + 2*bit3(L) + bit2(L), then xor-2/1 finish that head's sum
+        const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const float send = b4 ? part[i] : part[i + 4];
+            const float keep = b4 ? part[i + 4] : part[i];
+            part[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
         }
 #pragma unroll
-        for (int h = 0; h < 8; ++h)
-            if (h < G) {
-                const float s = warp_sum(part[h]);
-                if (lane == 0) prob[(size_t)h * a.R + r] = s * scale;
-            }
+        for (int i = 0; i < 2; ++i) {
+            const float send = b3 ? part[i] : part[i + 2];
+            const float keep = b3 ? part[i + 2] : part[i];
+            part[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+        }
+        {
+            const float send = b2 ? part[0] : part[1];
+            const float keep = b2 ? part[1] : part[0];
+            part[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+        }
+        part[0] += __shfl_xor_sync(0xffffffffu, part[0], 2);
+        part[0] += __shfl_xor_sync(0xffffffffu, part[0], 1);
+        const int h = (b4 ? 4 : 0) + (b3 ? 2 : 0) + (b2 ? 1 : 0);
+        if ((lane & 3) == 0 && h < G) prob[(size_t)h * a.R + r] = part[0] * scale;
     }
     __syncthreads();
     // 5. softmax per query head (softmax_in_place: max-subtracted exp, fp64 normaliser)
@@ -265,28 +289,40 @@ __global__ void __launch_bounds__(kTMax) decode_step_kernel(DecArgs a) {
         for (int r = tid; r < n_rows; r += kT) ph[r] = (float)((double)expf(ph[r] - m) / z);
         __syncthreads();
     }
-    // 6. outputs (weighted_value_sum in fp64): warp w sums a contiguous block of rows (in
-    //    order) for every head, lanes over d; the 8 warp partials combine in warp order.
+    // 6. outputs (weighted_value_sum): warp w sums a contiguous block of rows (in order) for all
+    //    G heads at once in fp32 (each value row is read once), lanes over d; the warp partials
+    //    combine in warp order in fp64, one head at a time.
     {
         const int per = (n_rows + kWarps - 1) / kWarps;
         const int r0 = min(n_rows, warp * per), r1 = min(n_rows, r0 + per);
         const int epl = (d + 31) / 32;  // elements per lane (d <= 128 -> <= 4)
         double* part = acc;              // [kWarps][d] for one head at a time (acc is free here)
-        for (int h = 0; h < G; ++h) {
-            const float* ph = prob + (size_t)h * a.R;
-            double o[4] = {0.0, 0.0, 0.0, 0.0};
-            for (int r = r0; r < r1; ++r) {
-                const int ow = rown[r];
-                const float* vr = ow < S ? sval + (size_t)ow * d : lval + (size_t)(ow - S) * d;
-                const double p = (double)ph[r];
+        float o[8][4];
 #pragma unroll
-                for (int e = 0; e < 4; ++e)
-                    if (e < epl && lane * epl + e < d) o[e] += p * (double)vr[lane * epl + e];
-            }
+        for (int h = 0; h < 8; ++h)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) o[h][e] = 0.f;
+        for (int r = r0; r < r1; ++r) {
+            const int ow = rown[r];
+            const float* vr = ow < S ? sval + (size_t)ow * d : lval + (size_t)(ow - S) * d;
+            float vv[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) vv[e] = (e < epl && lane * epl + e < d) ? vr[lane * epl + e] : 0.f;
+#pragma unroll
+            for (int h = 0; h < 8; ++h)
+                if (h < G) {
+                    const float p = prob[(size_t)h * a.R + r];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) o[h][e] = fmaf(p, vv[e], o[h][e]);
+                }
+        }
+#pragma unroll
+        for (int h = 0; h < 8; ++h) {
+            if (h >= G) break;
             __syncthreads();
 #pragma unroll
             for (int e = 0; e < 4; ++e)
-                if (e < epl && lane * epl + e < d) part[warp * d + lane * epl + e] = o[e];
+                if (e < epl && lane * epl + e < d) part[warp * d + lane * epl + e] = (double)o[h][e];
             __syncthreads();
             for (int i = tid; i < d; i += kT) {
                 double t = 0.0;
