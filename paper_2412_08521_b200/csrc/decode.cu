@@ -239,17 +239,29 @@ __global__ void __launch_bounds__(kTMax) decode_step_kernel(DecArgs a) {
         float part[8];
 #pragma unroll
         for (int h = 0; h < 8; ++h) part[h] = 0.f;
-        for (int p = lane; p < pairs; p += 32) {
-            const float2 kk = reinterpret_cast<const float2*>(kb)[p];
-            const float k0 = kk.x * kn, k1 = kk.y * kn;
-            const float2 cs = a.table[(size_t)rp * pairs + p];
-            const float r0 = k0 * cs.x - k1 * cs.y, r1 = k0 * cs.y + k1 * cs.x;
+        // d <= 128: at most two pairs per lane, both loaded before use (memory-level parallelism)
+        float2 kk[2], cs[2];
 #pragma unroll
-            for (int h = 0; h < 8; ++h)
-                if (h < G) {
-                    const float2 qq = reinterpret_cast<const float2*>(qrot + h * d)[p];
-                    part[h] += qq.x * r0 + qq.y * r1;
-                }
+        for (int t = 0; t < 2; ++t) {
+            const int p = lane + 32 * t;
+            if (p < pairs) {
+                kk[t] = reinterpret_cast<const float2*>(kb)[p];
+                cs[t] = a.table[(size_t)rp * pairs + p];
+            }
+        }
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+            const int p = lane + 32 * t;
+            if (p < pairs) {
+                const float k0 = kk[t].x * kn, k1 = kk[t].y * kn;
+                const float r0 = k0 * cs[t].x - k1 * cs[t].y, r1 = k0 * cs[t].y + k1 * cs[t].x;
+#pragma unroll
+                for (int h = 0; h < 8; ++h)
+                    if (h < G) {
+                        const float2 qq = reinterpret_cast<const float2*>(qrot + h * d)[p];
+                        part[h] += qq.x * r0 + qq.y * r1;
+                    }
+            }
         }
         // transpose-reduce: after the xor-16/8/4 steps lane L holds head
         // 4*bit4(L) + 2*bit3(L) + bit2(L), then xor-2/1 finish that head's sum
@@ -302,19 +314,30 @@ __global__ void __launch_bounds__(kTMax) decode_step_kernel(DecArgs a) {
         for (int h = 0; h < 8; ++h)
 #pragma unroll
             for (int e = 0; e < 4; ++e) o[h][e] = 0.f;
-        for (int r = r0; r < r1; ++r) {
-            const int ow = rown[r];
-            const float* vr = ow < S ? sval + (size_t)ow * d : lval + (size_t)(ow - S) * d;
-            float vv[4];
+        constexpr int kU = 4;  // rows in flight per warp (their value loads issued together)
+        for (int rb = r0; rb < r1; rb += kU) {
+            float vv[kU][4];
 #pragma unroll
-            for (int e = 0; e < 4; ++e) vv[e] = (e < epl && lane * epl + e < d) ? vr[lane * epl + e] : 0.f;
+            for (int t = 0; t < kU; ++t) {
+                const int r = rb + t;
+                const int ow = r < r1 ? rown[r] : 0;
+                const float* vr = ow < S ? sval + (size_t)ow * d : lval + (size_t)(ow - S) * d;
 #pragma unroll
-            for (int h = 0; h < 8; ++h)
-                if (h < G) {
-                    const float p = prob[(size_t)h * a.R + r];
+                for (int e = 0; e < 4; ++e)
+                    vv[t][e] = (r < r1 && e < epl && lane * epl + e < d) ? vr[lane * epl + e] : 0.f;
+            }
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) o[h][e] = fmaf(p, vv[e], o[h][e]);
-                }
+            for (int t = 0; t < kU; ++t) {
+                const int r = rb + t;
+                if (r >= r1) break;
+#pragma unroll
+                for (int h = 0; h < 8; ++h)
+                    if (h < G) {
+                        const float p = prob[(size_t)h * a.R + r];
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) o[h][e] = fmaf(p, vv[t][e], o[h][e]);
+                    }
+            }
         }
 #pragma unroll
         for (int h = 0; h < 8; ++h) {
