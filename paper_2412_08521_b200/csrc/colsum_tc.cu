@@ -220,16 +220,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int loc_start = a.L - a.lwin;
         const int last_interior = (loc_start / kTile) - 1;  // tiles <= this hold no window query
         double acc_g = 0.0, acc_l = 0.0;
-        for (int i = 0; i < n_items; ++i) {
-            const int I = J0 + i % span;
-            const int bb = i % kBufs;
-            const uint32_t ph = (i / kBufs) & 1;
-            mbar_wait(&bars.l_full[bb], ph);
-            mbar_wait(&bars.s_full[bb], ph);
+        // shared-window addresses hoisted out of the item loop (barriers of one kind are
+        // consecutive uint64_t, so buffer bb is +8 bb)
+        const uint32_t l_full0 = smem_u32(&bars.l_full[0]), s_full0 = smem_u32(&bars.s_full[0]);
+        const uint32_t s_empty0 = smem_u32(&bars.s_empty[0]);
+        const uint32_t sa0 = tmem + w * 128 + 64 * hc + ((uint32_t)(wi * 32) << 16);
+        const uint32_t lb0 = smem_u32(slse + 64 * hc);
+        static_assert(kBufs == 2, "item i uses buffer i & 1");
+        for (int i = 0, I = J0; i < n_items; ++i) {  // I = J0 + i % span, kept incrementally
+            const int bb = i & 1;
+            const uint32_t ph = (i >> 1) & 1;
+            mbar_wait_u(l_full0 + 8 * bb, ph);
+            mbar_wait_u(s_full0 + 8 * bb, ph);
             tc_fence_after();
             if (active && I >= Jw && a.debug != 1) {
-                const uint32_t sa = tmem + bb * 256 + w * 128 + 64 * hc + ((uint32_t)(wi * 32) << 16);
-                const uint32_t lb = smem_u32(slse + bb * 128 + 64 * hc);
+                const uint32_t sa = sa0 + bb * 256;
+                const uint32_t lb = lb0 + bb * 512;
                 if (I > Jw && I <= last_interior) {
                     acc_g += (double)cols_fast<kPoly>(sa, lb);
                 } else {
@@ -241,7 +247,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             tc_fence_before();
             __syncwarp();
-            if ((tid & 31) == 0) mbar_arrive(&bars.s_empty[bb]);
+            if ((tid & 31) == 0) mbar_arrive_u(s_empty0 + 8 * bb);
+            if (++I == a.nT) I = J0;
         }
         // combine the two column halves in a fixed order: (half 0 + half 1) / G
         double* sp = spart + w * 256;
