@@ -211,7 +211,8 @@ EMS_API int ems_prefill(const ems_desc* desc, double rope_base, const void* q, c
 /* engine::prefill from HOST memory -- the reference's own calling convention (per-head host
  * matrices, proj/src/engine.cpp:42-82), batched.  h_* are pinned host [B][H][L][d] tensors;
  * d_* are the caller's device staging buffers of the same shapes.  The units are split into
- * `chunks` contiguous groups: the host-to-device copy of group c+1 (on copy_stream, or a
+ * `chunks` contiguous groups of geometrically growing size (U/2^(chunks-1), ..., U/4, U/2 units,
+ * so compute starts after a small first copy): the host-to-device copy of group c+1 (on copy_stream, or a
  * library-owned per-thread stream when NULL) overlaps the compute of group c (on stream), and
  * each group's compressed cache is copied to h_cache (pinned host SoA with the device
  * cache's shapes; may be NULL) as soon as it is done.  rope_base > 0: h_q/h_k are raw and
