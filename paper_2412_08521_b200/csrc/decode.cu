@@ -142,7 +142,10 @@ __device__ __forceinline__ double combined(const double* sc, double align) {
     return fmax(sc[0] * align, sc[1] + sc[2]);
 }
 
-__global__ void __launch_bounds__(kTMax) decode_step_kernel(DecArgs a) {
+// kG: query heads per unit rounded up to a power of two (register arrays sized by it);
+// kTh / kMinB: launch width and residency hint (512 x 1 for few units, 256 x 3 for many).
+template <int kG, int kTh, int kMinB>
+__global__ void __launch_bounds__(kTh, kMinB) decode_step_kernel(DecArgs a) {
     extern __shared__ __align__(16) unsigned char dsm[];
     const int u = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int kT = blockDim.x, kWarps = kT >> 5;
@@ -236,9 +239,9 @@ __global__ void __launch_bounds__(kTMax) decode_step_kernel(DecArgs a) {
         const float* kb = center ? skey + (size_t)o * d : lkey + (size_t)(o - S) * d;
         const float kn = center ? snorm[o] : 1.f;
         const int rp = center && !a.with_pos ? spos[o] : rpos[r];
-        float part[8];
+        float part[kG];
 #pragma unroll
-        for (int h = 0; h < 8; ++h) part[h] = 0.f;
+        for (int h = 0; h < kG; ++h) part[h] = 0.f;
         // d <= 128: at most two pairs per lane, both loaded before use (memory-level parallelism)
         float2 kk[2], cs[2];
 #pragma unroll
@@ -256,37 +259,30 @@ __global__ void __launch_bounds__(kTMax) decode_step_kernel(DecArgs a) {
                 const float k0 = kk[t].x * kn, k1 = kk[t].y * kn;
                 const float r0 = k0 * cs[t].x - k1 * cs[t].y, r1 = k0 * cs[t].y + k1 * cs[t].x;
 #pragma unroll
-                for (int h = 0; h < 8; ++h)
+                for (int h = 0; h < kG; ++h)
                     if (h < G) {
                         const float2 qq = reinterpret_cast<const float2*>(qrot + h * d)[p];
                         part[h] += qq.x * r0 + qq.y * r1;
                     }
             }
         }
-        // transpose-reduce: after the xor-16/8/4 steps lane L holds head
-        // 4*bit4(L) + 2*bit3(L) + bit2(L), then xor-2/1 finish that head's sum
-        const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+        // transpose-reduce: each xor-16, 8, ... step halves the values a lane carries (the lane
+        // with the offset bit set keeps the upper half), so after log2(kG) steps lane L holds
+        // head = its offset bits read from the top; the remaining xor steps finish that sum
+        int h = 0, off = 16;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const float send = b4 ? part[i] : part[i + 4];
-            const float keep = b4 ? part[i + 4] : part[i];
-            part[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-        }
+        for (int n = kG; n > 1; n >>= 1, off >>= 1) {
+            const bool hi = lane & off;
 #pragma unroll
-        for (int i = 0; i < 2; ++i) {
-            const float send = b3 ? part[i] : part[i + 2];
-            const float keep = b3 ? part[i + 2] : part[i];
-            part[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+            for (int i = 0; i < n / 2; ++i) {
+                const float send = hi ? part[i] : part[i + n / 2];
+                const float keep = hi ? part[i + n / 2] : part[i];
+                part[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+            }
+            h = 2 * h + (hi ? 1 : 0);
         }
-        {
-            const float send = b2 ? part[0] : part[1];
-            const float keep = b2 ? part[1] : part[0];
-            part[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-        }
-        part[0] += __shfl_xor_sync(0xffffffffu, part[0], 2);
-        part[0] += __shfl_xor_sync(0xffffffffu, part[0], 1);
-        const int h = (b4 ? 4 : 0) + (b3 ? 2 : 0) + (b2 ? 1 : 0);
-        if ((lane & 3) == 0 && h < G) prob[(size_t)h * a.R + r] = part[0] * scale;
+        for (int o2 = off; o2 > 0; o2 >>= 1) part[0] += __shfl_xor_sync(0xffffffffu, part[0], o2);
+        if ((lane & (2 * off - 1)) == 0 && h < G) prob[(size_t)h * a.R + r] = part[0] * scale;
     }
     __syncthreads();
     // 5. softmax per query head (softmax_in_place: max-subtracted exp, fp64 normaliser)
@@ -309,9 +305,9 @@ __global__ void __launch_bounds__(kTMax) decode_step_kernel(DecArgs a) {
         const int r0 = min(n_rows, warp * per), r1 = min(n_rows, r0 + per);
         const int epl = (d + 31) / 32;  // elements per lane (d <= 128 -> <= 4)
         double* part = acc;              // [kWarps][d] for one head at a time (acc is free here)
-        float o[8][4];
+        float o[kG][4];
 #pragma unroll
-        for (int h = 0; h < 8; ++h)
+        for (int h = 0; h < kG; ++h)
 #pragma unroll
             for (int e = 0; e < 4; ++e) o[h][e] = 0.f;
         constexpr int kU = 4;  // rows in flight per warp (their value loads issued together)
@@ -331,7 +327,7 @@ __global__ void __launch_bounds__(kTMax) decode_step_kernel(DecArgs a) {
                 const int r = rb + t;
                 if (r >= r1) break;
 #pragma unroll
-                for (int h = 0; h < 8; ++h)
+                for (int h = 0; h < kG; ++h)
                     if (h < G) {
                         const float p = prob[(size_t)h * a.R + r];
 #pragma unroll
@@ -340,7 +336,7 @@ __global__ void __launch_bounds__(kTMax) decode_step_kernel(DecArgs a) {
             }
         }
 #pragma unroll
-        for (int h = 0; h < 8; ++h) {
+        for (int h = 0; h < kG; ++h) {
             if (h >= G) break;
             __syncthreads();
 #pragma unroll
@@ -751,14 +747,18 @@ cudaError_t launch_decode_step(const Dims& m, int dtype, int S, int W, int T, in
     a.row_pos = reinterpret_cast<int32_t*>(take(U * R * 4));
     a.probs = reinterpret_cast<float*>(take(U * m.G * R * 4));
     a.pmean = reinterpret_cast<float*>(take(U * R * 4));
-    const int threads = m.units >= 148 ? 256 : kTMax;
+    const bool wide = m.units < 148;  // few units: more warps per unit; many: more units per SM
+    const int threads = wide ? kTMax : 256;
     const size_t smem = (size_t)max(S + W, (threads / 32) * m.d) * 8 + (size_t)m.G * m.d * 4;
-    static size_t attr = 0;
-    if (smem > 48 * 1024 && smem > attr) {
-        cudaFuncSetAttribute(decode_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = smem;
-    }
-    decode_step_kernel<<<m.units, threads, smem, s>>>(a);
+    const int gb = m.G <= 1 ? 1 : m.G <= 2 ? 2 : m.G <= 4 ? 4 : 8;
+    void (*fn)(DecArgs) = nullptr;
+#define EMS_DEC_PICK(K)                                                                          \
+    if (gb == K) fn = wide ? decode_step_kernel<K, kTMax, 1> : decode_step_kernel<K, 256, 3>;
+    EMS_DEC_PICK(1) EMS_DEC_PICK(2) EMS_DEC_PICK(4) EMS_DEC_PICK(8)
+#undef EMS_DEC_PICK
+    if (!fn || m.G > 8) return cudaErrorInvalidValue;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    fn<<<m.units, threads, smem, s>>>(a);
     return cudaGetLastError();
 }
 
