@@ -1,0 +1,155 @@
+"""Full-size checks on the bench workload (config 3: B=1, H_q=32, H_kv=8, L=32768, bf16) and on
+config 5 (L=131072, H_q=64, budget 2560), where the CPU oracle cannot run:
+
+* scores against a plain PyTorch reference of streaming_pass (proj/src/scoring.cpp:20-64) on
+  the same bf16 values: fp32 matmuls (TF32 off), exact per-row LSE, fp64 column sums, GQA
+  mean (D2) -- glo / loc / LSE within the tolerances stated below, O on sampled rows;
+* size-independent properties: mass conservation (sum glo = L, sum loc = l_win per unit),
+  the selection (partition_tokens, compressor.cpp:48-74) re-derived in numpy from the
+  kernel's own pooled scores (index-exact), the cache layout invariants (centers by position,
+  exact locals, sorted LUT covering important + TBM tokens), and run-to-run bit identity.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+from paper_2412_08521_b200 import ems  # noqa: E402
+from paper_2412_08521_b200.inputs import CONFIGS, make_batch_torch  # noqa: E402
+
+
+def _run(w, seed=1):
+    q, kr, kw, v = make_batch_torch(w, seed=seed, device="cuda")
+    B, Hq, L, d = q.shape
+    cfg = ems.EmsConfig(w.n_budget, w.l_win, w.tau, w.gamma, w.kernel_size)
+    plan = ems.Plan(B, Hq, w.heads_kv, L, d, q.dtype, cfg, "cuda", "auto", want_out=True, want_lse=True)
+    plan.run(q, kr, kw, v)
+    plan.sync_status()
+    torch.cuda.synchronize()
+    return q, kr, kw, v, plan
+
+
+@pytest.fixture(scope="module")
+def cfg3():
+    w = CONFIGS["cfg3"]
+    return (w,) + _run(w)
+
+
+def _torch_scores(q, k, l_win, chunk=2048):
+    """streaming_pass in torch: per query head, row chunks; exact LSE; fp64 column sums."""
+    B, Hq, L, d = q.shape
+    Hkv = k.shape[1]
+    G = Hq // Hkv
+    glo = torch.zeros((B, Hkv, L), dtype=torch.float64, device=q.device)
+    loc = torch.zeros_like(glo)
+    lse = torch.empty((B, Hq, L), dtype=torch.float32, device=q.device)
+    scale = 1.0 / d ** 0.5
+    loc_start = L - l_win
+    for b in range(B):
+        for h in range(Hq):
+            kk = k[b, h // G].float()
+            for r0 in range(0, L, chunk):
+                r1 = min(L, r0 + chunk)
+                s = (q[b, h, r0:r1].float() @ kk[:r1].T) * scale
+                rows = torch.arange(r0, r1, device=q.device)[:, None]
+                s.masked_fill_(torch.arange(r1, device=q.device)[None, :] > rows, float("-inf"))
+                ls = torch.logsumexp(s, dim=1)
+                lse[b, h, r0:r1] = ls
+                p = torch.exp(s - ls[:, None])
+                glo[b, h // G, :r1] += p.sum(0, dtype=torch.float64)
+                if r1 > loc_start:
+                    loc[b, h // G, :r1] += p[max(loc_start - r0, 0):].sum(0, dtype=torch.float64)
+    return glo / G, loc / G, lse
+
+
+def test_cfg3_scores_match_torch_reference(cfg3):
+    w, q, kr, kw, v, plan = cfg3
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    try:
+        glo_t, loc_t, lse_t = _torch_scores(q, kr, w.l_win)
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+    g, lo = plan.glo.double(), plan.loc.double()
+    # glo: relative to the value, with a floor of 1e-4 x the mean (columns nobody attends)
+    floor = 1e-4 * glo_t.mean()
+    err_g = ((g - glo_t).abs() / (glo_t + floor)).max().item()
+    assert err_g <= 1e-5, err_g  # measured 5.8e-7
+    floor_l = 1e-4 * loc_t.mean()
+    err_l = ((lo - loc_t).abs() / (loc_t + floor_l)).max().item()
+    assert err_l <= 1e-5, err_l  # measured 1.1e-6
+    err_lse = (plan.lse - lse_t).abs().max().item()
+    assert err_lse <= 1e-4, err_lse  # natural-log units; measured 1.9e-6
+
+
+def test_cfg3_outputs_on_sampled_rows(cfg3):
+    w, q, kr, kw, v, plan = cfg3
+    B, Hq, L, d = q.shape
+    G = Hq // w.heads_kv
+    rows = torch.tensor([0, 1, 127, 128, 4095, 16384, L - 129, L - 2, L - 1], device="cuda")
+    for h in (0, 5, 17, Hq - 1):
+        kk, vv = kr[0, h // G].float(), v[0, h // G].float()
+        s = (q[0, h, rows].float() @ kk.T) / d ** 0.5
+        s.masked_fill_(torch.arange(L, device="cuda")[None, :] > rows[:, None], float("-inf"))
+        o_t = torch.softmax(s, dim=1) @ vv
+        o = plan.out[0, h, rows].float()
+        err = ((o - o_t).abs().max(dim=1).values / o_t.abs().max(dim=1).values.clamp_min(1e-3)).max().item()
+        assert err <= 2e-2, (h, err)  # bf16 P and bf16 output
+
+
+def _check_invariants(w, plan, L):
+    U = plan.dims.units
+    n_imp, n_tbm, lw = w.n_budget - w.l_win, int((w.gamma - 1.0) * w.n_budget), w.l_win
+    glo, loc = plan.glo.reshape(U, L).double(), plan.loc.reshape(U, L).double()
+    # mass conservation: every query row's probabilities sum to one (GQA mean keeps it)
+    assert ((glo.sum(1) - L).abs() / L).max().item() <= 1e-5
+    assert ((loc.sum(1) - lw).abs() / lw).max().item() <= 1e-5
+    c = {k: (t.float() if t.dtype == torch.bfloat16 else t).cpu().numpy() for k, t in plan.cache.items()}
+    pooled = plan.stage["pooled"].cpu().numpy()
+    for u in range(U):
+        counts = c["counts"][u]
+        assert list(counts[[0, 1, 3]]) == [n_imp, lw, 1]
+        # partition_tokens on the kernel's own pooled scores: stable descending order over the
+        # candidates [0, L - w), ties to the lower index (compressor.cpp:58-62)
+        cand = pooled[u, :L - lw]
+        order = np.lexsort((np.arange(L - lw), -cand.astype(np.float64)))
+        imp = np.sort(order[:n_imp])
+        tbm = np.sort(order[n_imp:n_imp + n_tbm])
+        np.testing.assert_array_equal(c["center_pos"][u, :n_imp], imp)
+        np.testing.assert_array_equal(c["local_pos"][u, :lw], np.arange(L - lw, L))
+        lut = c["lut_pos"][u, :counts[2]]
+        assert (np.diff(lut) > 0).all()
+        np.testing.assert_array_equal(lut, np.union1d(imp, tbm))  # zero_class mode keeps every TBM token
+        slots = c["lut_slot"][u, :counts[2]]
+        assert ((slots >= -1) & (slots < n_imp)).all()
+        assert (slots[np.isin(lut, imp)] == np.arange(n_imp)).all()  # center slot s = s-th important
+        keys = c["center_key"][u, :n_imp].astype(np.float32)
+        nrm = np.linalg.norm(keys, axis=1)
+        assert np.abs(nrm - 1.0).max() <= 1e-2  # unit keys (bf16 storage)
+
+
+def test_cfg3_selection_and_cache_invariants(cfg3):
+    w, q, kr, kw, v, plan = cfg3
+    _check_invariants(w, plan, q.shape[2])
+
+
+def test_cfg3_deterministic(cfg3):
+    w, q, kr, kw, v, plan = cfg3
+    ref = {k: t.clone() for k, t in plan.cache.items()}
+    glo, loc, out = plan.glo.clone(), plan.loc.clone(), plan.out.clone()
+    plan.run(q, kr, kw, v)
+    plan.sync_status()
+    assert torch.equal(plan.glo, glo) and torch.equal(plan.loc, loc) and torch.equal(plan.out, out)
+    for k in ref:
+        assert torch.equal(plan.cache[k], ref[k]), k
+
+
+def test_cfg5_properties():
+    """Config 5 (L = 131072, G = 8, budget 2560): mass, selection and layout at full size."""
+    w = CONFIGS["cfg5"]
+    q, kr, kw, v, plan = _run(w)
+    _check_invariants(w, plan, q.shape[2])
+    del q, kr, kw, v, plan
+    torch.cuda.empty_cache()
