@@ -124,4 +124,41 @@ void set_error(const char* fmt, ...);
         }                                                                             \
     } while (0)
 
+// ---- thread-block clusters: distributed shared memory reads, cluster barrier, rank --------
+__device__ __forceinline__ uint32_t dsm_addr(const void* p, int rank) {
+    uint32_t a;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"((uint32_t)__cvta_generic_to_shared(p)),
+                 "r"(rank));
+    return a;  // shared::cluster address, read with ld.shared::cluster
+}
+__device__ __forceinline__ int ld_dsm_i32(const void* p, int rank) {
+    int v;
+    asm volatile("ld.shared::cluster.s32 %0, [%1];" : "=r"(v) : "r"(dsm_addr(p, rank)) : "memory");
+    return v;
+}
+__device__ __forceinline__ long long ld_dsm_i64(const void* p, int rank) {
+    long long v;
+    asm volatile("ld.shared::cluster.s64 %0, [%1];" : "=l"(v) : "r"(dsm_addr(p, rank)) : "memory");
+    return v;
+}
+__device__ __forceinline__ float ld_dsm_f32(const void* p, int rank) {
+    float v;
+    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(dsm_addr(p, rank)) : "memory");
+    return v;
+}
+__device__ __forceinline__ double ld_dsm_f64(const void* p, int rank) {
+    double v;
+    asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(dsm_addr(p, rank)) : "memory");
+    return v;
+}
+// all threads of every CTA of the cluster; release/acquire at cluster scope (shared and global)
+__device__ __forceinline__ void cl_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ unsigned cl_rank() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+
 }  // namespace ems

@@ -32,6 +32,7 @@ namespace {
 // launched width, so results are a function of the problem shape only (deterministic)
 constexpr int kTMax = 512;
 constexpr int kWarpsMax = kTMax / 32;
+constexpr int kDecClu = 8;  // CTAs per unit in the cluster variant
 
 struct DecArgs {
     int G, d, S, W, T, R;          // query heads per unit; capacities: slots, locals, LUT, rows
@@ -144,14 +145,24 @@ __device__ __forceinline__ double combined(const double* sc, double align) {
 
 // kG: query heads per unit rounded up to a power of two (register arrays sized by it);
 // kTh / kMinB: launch width and residency hint (512 x 1 for few units, 256 x 3 for many).
-template <int kG, int kTh, int kMinB>
+// kClu > 1: a unit's expanded rows are split over a cluster of kClu CTAs (row list, logits,
+// softmax, value sums, argmax and the mass flow), with the cross-CTA maxima, normalisers,
+// partial sums and per-owner masses exchanged through distributed shared memory in rank
+// order; rank 0 then runs the sequential cache update alone.
+template <int kG, int kTh, int kMinB, int kClu>
 __global__ void __launch_bounds__(kTh, kMinB) decode_step_kernel(DecArgs a) {
     extern __shared__ __align__(16) unsigned char dsm[];
-    const int u = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int rank = kClu > 1 ? (int)cl_rank() : 0;
+    const int u = blockIdx.x / kClu, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int kT = blockDim.x, kWarps = kT >> 5;
     const int d = a.d, S = a.S, W = a.W, T = a.T, G = a.G, pairs = d / 2;
     double* acc = reinterpret_cast<double*>(dsm);                  // [max(S + W, 8 d)] owner mass / R / partials
     float* qrot = reinterpret_cast<float*>(acc + max(S + W, kWarps * d));  // [G][d]
+    double* vout = reinterpret_cast<double*>(qrot + ((G * d + 1) & ~1));   // [G][d] cluster partial outputs
+    __shared__ int s_cnt;
+    __shared__ float s_max[8];
+    __shared__ double s_z[8];
+    __shared__ Cand s_cand[8];
     __shared__ double shd[kWarpsMax];
     __shared__ float shf[kWarpsMax];
     __shared__ Cand shc[kWarpsMax];
@@ -184,7 +195,7 @@ __global__ void __launch_bounds__(kTh, kMinB) decode_step_kernel(DecArgs a) {
     int head = s_meta[0], count = s_meta[1], lut_n = s_meta[2];
 
     // 1. append the incoming token to the local window (engine.cpp:166-172)
-    {
+    if (rank == 0) {
         const int slot = (head + count) % W;
         for (int i = tid; i < d; i += kT) {
             lkey[(size_t)slot * d + i] = ldx(a.k, (size_t)u * d + i, a.dtype);
@@ -194,9 +205,10 @@ __global__ void __launch_bounds__(kTh, kMinB) decode_step_kernel(DecArgs a) {
             lpos[slot] = (int32_t)a.position;
             lscore[3 * slot] = lscore[3 * slot + 1] = lscore[3 * slot + 2] = 0.0;
         }
-        ++count;
     }
-    __syncthreads();  // the appended row's position is read by another warp in step 3
+    ++count;
+    if constexpr (kClu > 1) cl_sync();  // the appended row is read by other CTAs of the cluster
+    else __syncthreads();               // ... or by another warp in step 3
     // 2. RoPE'd queries (apply_rope at the new position, engine.cpp:175)
     for (int x = tid; x < G * pairs; x += kT) {
         const int h = x / pairs, p = x % pairs;
@@ -208,7 +220,39 @@ __global__ void __launch_bounds__(kTh, kMinB) decode_step_kernel(DecArgs a) {
     }
     // 3. expanded rows: non-zero LUT entries in LUT order, then the locals (expand_cache)
     int n_rows;
-    {
+    if constexpr (kClu > 1) {  // rank r lists LUT slice r (offset = rows of the lower ranks) and locals slice r
+        const int e0 = (int)((long long)rank * lut_n / kClu), e1 = (int)((long long)(rank + 1) * lut_n / kClu);
+        int cnt = 0;
+        for (int e = e0 + tid; e < e1; e += kT) cnt += tslot[e] >= 0;
+        int tot;
+        bscan(cnt, shi, &tot);
+        if (tid == 0) s_cnt = tot;
+        cl_sync();
+        int base = 0, lut_rows = 0;
+        for (int q = 0; q < kClu; ++q) {
+            const int c = ld_dsm_i32(&s_cnt, q);
+            base += q < rank ? c : 0;
+            lut_rows += c;
+        }
+        for (int c0 = e0; c0 < e1; c0 += kT) {
+            const int e = c0 + tid;
+            const int keep = e < e1 && tslot[e] >= 0;
+            const int off = bscan(keep, shi, &tot);
+            if (keep) {
+                rown[base + off] = tslot[e];
+                rpos[base + off] = tpos[e];
+            }
+            base += tot;
+        }
+        const int l0 = rank * count / kClu, l1 = (rank + 1) * count / kClu;
+        for (int li = l0 + tid; li < l1; li += kT) {
+            const int ring = (head + li) % W;
+            rown[lut_rows + li] = S + ring;
+            rpos[lut_rows + li] = lpos[ring];
+        }
+        n_rows = lut_rows + count;
+        cl_sync();  // the whole row list is visible to every CTA
+    } else {
         int base = 0;
         for (int c0 = 0; c0 < lut_n; c0 += kT) {
             const int e = c0 + tid;
@@ -227,13 +271,15 @@ __global__ void __launch_bounds__(kTh, kMinB) decode_step_kernel(DecArgs a) {
             rpos[base + li] = lpos[ring];
         }
         n_rows = base + count;
+        __syncthreads();
     }
-    __syncthreads();
+    // this CTA's rows: [R0, R1) (all of them without a cluster)
+    const int R0 = (int)((long long)rank * n_rows / kClu), R1 = (int)((long long)(rank + 1) * n_rows / kClu);
     // 4. logits: one warp per row, lanes over RoPE pairs; all G heads share the key.  The G
     //    (<= 8) per-lane partial dot products are reduced together in 9 shuffles (each step
     //    halves the values a lane carries), leaving head h's sum in lanes 4h' .. (fixed order).
     const float scale = rsqrtf((float)d);
-    for (int r = warp; r < n_rows; r += kWarps) {
+    for (int r = R0 + warp; r < R1; r += kWarps) {
         const int o = rown[r];
         const bool center = o < S;
         const float* kb = center ? skey + (size_t)o * d : lkey + (size_t)(o - S) * d;
@@ -286,23 +332,60 @@ __global__ void __launch_bounds__(kTh, kMinB) decode_step_kernel(DecArgs a) {
     }
     __syncthreads();
     // 5. softmax per query head (softmax_in_place: max-subtracted exp, fp64 normaliser)
-    for (int h = 0; h < G; ++h) {
-        float* ph = prob + (size_t)h * a.R;
-        float m = -FLT_MAX;
-        for (int r = tid; r < n_rows; r += kT) m = fmaxf(m, ph[r]);
-        m = bmax(m, shf);
-        double z = 0.0;
-        for (int r = tid; r < n_rows; r += kT) z += (double)expf(ph[r] - m);
-        z = bsum(z, shd);
-        for (int r = tid; r < n_rows; r += kT) ph[r] = (float)((double)expf(ph[r] - m) / z);
+    if constexpr (kClu > 1) {  // cluster-wide max, then the normaliser summed in rank order
+        for (int h = 0; h < G; ++h) {
+            const float* ph = prob + (size_t)h * a.R;
+            float m = -FLT_MAX;
+            for (int r = R0 + tid; r < R1; r += kT) m = fmaxf(m, ph[r]);
+            m = bmax(m, shf);
+            if (tid == 0) s_max[h] = m;
+        }
+        cl_sync();
+        float mh[kG];
+#pragma unroll
+        for (int h = 0; h < kG; ++h) {
+            mh[h] = -FLT_MAX;
+            if (h < G)
+                for (int q = 0; q < kClu; ++q) mh[h] = fmaxf(mh[h], ld_dsm_f32(&s_max[h], q));
+        }
+#pragma unroll
+        for (int h = 0; h < kG; ++h) {
+            if (h >= G) break;
+            const float* ph = prob + (size_t)h * a.R;
+            double z = 0.0;
+            for (int r = R0 + tid; r < R1; r += kT) z += (double)expf(ph[r] - mh[h]);
+            z = bsum(z, shd);
+            if (tid == 0) s_z[h] = z;
+        }
+        cl_sync();
+#pragma unroll
+        for (int h = 0; h < kG; ++h) {
+            if (h >= G) break;
+            double z = 0.0;
+            for (int q = 0; q < kClu; ++q) z += ld_dsm_f64(&s_z[h], q);
+            float* ph = prob + (size_t)h * a.R;
+            for (int r = R0 + tid; r < R1; r += kT) ph[r] = (float)((double)expf(ph[r] - mh[h]) / z);
+        }
         __syncthreads();
+    } else {
+        for (int h = 0; h < G; ++h) {
+            float* ph = prob + (size_t)h * a.R;
+            float m = -FLT_MAX;
+            for (int r = tid; r < n_rows; r += kT) m = fmaxf(m, ph[r]);
+            m = bmax(m, shf);
+            double z = 0.0;
+            for (int r = tid; r < n_rows; r += kT) z += (double)expf(ph[r] - m);
+            z = bsum(z, shd);
+            for (int r = tid; r < n_rows; r += kT) ph[r] = (float)((double)expf(ph[r] - m) / z);
+            __syncthreads();
+        }
     }
     // 6. outputs (weighted_value_sum): warp w sums a contiguous block of rows (in order) for all
     //    G heads at once in fp32 (each value row is read once), lanes over d; the warp partials
     //    combine in warp order in fp64, one head at a time.
     {
-        const int per = (n_rows + kWarps - 1) / kWarps;
-        const int r0 = min(n_rows, warp * per), r1 = min(n_rows, r0 + per);
+        const int per = (R1 - R0 + kWarps - 1) / kWarps;
+        const int r0 = min(R1, R0 + warp * per), r1 = min(R1, r0 + per);
         const int epl = (d + 31) / 32;  // elements per lane (d <= 128 -> <= 4)
         double* part = acc;              // [kWarps][d] for one head at a time (acc is free here)
         float o[kG][4];
@@ -346,26 +429,51 @@ __global__ void __launch_bounds__(kTh, kMinB) decode_step_kernel(DecArgs a) {
             for (int i = tid; i < d; i += kT) {
                 double t = 0.0;
                 for (int w2 = 0; w2 < kWarps; ++w2) t += part[w2 * d + i];
-                stx(a.out, ((size_t)u * G + h) * d + i, a.dtype, t);
+                if constexpr (kClu > 1) vout[h * d + i] = t;
+                else stx(a.out, ((size_t)u * G + h) * d + i, a.dtype, t);
             }
         }
         __syncthreads();
+        if constexpr (kClu > 1) {  // the CTAs' partial outputs, summed in rank order
+            cl_sync();
+            for (int x = rank * kT + tid; x < G * d; x += kClu * kT) {
+                double t = 0.0;
+                for (int q = 0; q < kClu; ++q) t += ld_dsm_f64(&vout[x], q);
+                stx(a.out, (size_t)u * G * d + x, a.dtype, t);
+            }
+        }
     }
+    auto better = [](const Cand& x, const Cand& y) {
+        if (y.idx < 0) return x.idx >= 0;
+        if (x.idx < 0) return false;
+        return x.key > y.key || (x.key == y.key && x.tie < y.tie);  // first max (engine.cpp:188-191)
+    };
     for (int h = 0; h < G; ++h) {
         const float* ph = prob + (size_t)h * a.R;
         Cand c{-1.0, 0, -1};
-        for (int r = tid; r < n_rows; r += kT)
+        for (int r = R0 + tid; r < R1; r += kT)
             if (c.idx < 0 || (double)ph[r] > c.key) c = Cand{(double)ph[r], r, r};
-        auto better = [](const Cand& x, const Cand& y) {
-            if (y.idx < 0) return x.idx >= 0;
-            if (x.idx < 0) return false;
-            return x.key > y.key || (x.key == y.key && x.tie < y.tie);  // first max (engine.cpp:188-191)
-        };
         c = bselect(c, better, shc);
-        if (tid == 0) a.argmax_pos[(size_t)u * G + h] = c.idx >= 0 ? rpos[c.idx] : -1;
+        if constexpr (kClu > 1) {
+            if (tid == 0) s_cand[h] = c;
+        } else if (tid == 0) {
+            a.argmax_pos[(size_t)u * G + h] = c.idx >= 0 ? rpos[c.idx] : -1;
+        }
+    }
+    if constexpr (kClu > 1) {  // candidates of the CTAs (global row indices: a total order)
+        cl_sync();
+        if (rank == 0 && tid < G) {
+            Cand c{-1.0, 0, -1};
+            for (int q = 0; q < kClu; ++q) {
+                const Cand x{ld_dsm_f64(&s_cand[tid].key, q), ld_dsm_i64(&s_cand[tid].tie, q),
+                             ld_dsm_i32(&s_cand[tid].idx, q)};
+                if (better(x, c)) c = x;
+            }
+            a.argmax_pos[(size_t)u * G + tid] = c.idx >= 0 ? rpos[c.idx] : -1;
+        }
     }
     // 8. attention mass flows back to the owners (engine.cpp:184-195), GQA mean
-    for (int r = tid; r < n_rows; r += kT) {
+    for (int r = R0 + tid; r < R1; r += kT) {
         double s = 0.0;
         for (int h = 0; h < G; ++h) s += (double)prob[(size_t)h * a.R + r];
         pm[r] = (float)(s / G);
@@ -373,24 +481,41 @@ __global__ void __launch_bounds__(kTh, kMinB) decode_step_kernel(DecArgs a) {
     for (int i = tid; i < S + W; i += kT) acc[i] = 0.0;
     __syncthreads();
     if (warp == 0) {  // ordered pass: rows in order, equal owners inside a 32-row chunk summed in lane order
-        for (int b = 0; b < n_rows; b += 32) {
+        for (int b = R0; b < R1; b += 32) {
             const int r = b + lane;
-            const int o = r < n_rows ? rown[r] : -1 - lane;
-            const double p = r < n_rows ? (G == 1 ? (double)prob[r] : (double)pm[r]) : 0.0;
+            const int o = r < R1 ? rown[r] : -1 - lane;
+            const double p = r < R1 ? (G == 1 ? (double)prob[r] : (double)pm[r]) : 0.0;
             const unsigned grp = __match_any_sync(0xffffffffu, o);
             double gs = 0.0;
             for (unsigned m = grp; m; m &= m - 1) gs += __shfl_sync(grp, p, __ffs(m) - 1);
-            if (r < n_rows && lane == __ffs(grp) - 1) acc[o] += gs;
+            if (r < R1 && lane == __ffs(grp) - 1) acc[o] += gs;
             __syncwarp();
         }
     }
     __syncthreads();
-    for (int s = tid; s < S; s += kT)
-        if (salive[s]) sscore[3 * s] += acc[s], sscore[3 * s + 2] += acc[s];
-    for (int li = tid; li < count; li += kT) {
-        const int ring = (head + li) % W;
-        lscore[3 * ring] += acc[S + ring];
-        lscore[3 * ring + 2] += acc[S + ring];
+    if constexpr (kClu > 1) {  // owners split over the CTAs; each owner's mass summed in rank order
+        cl_sync();
+        const int o0 = (int)((long long)rank * (S + W) / kClu), o1 = (int)((long long)(rank + 1) * (S + W) / kClu);
+        for (int o = o0 + tid; o < o1; o += kT) {
+            double t = 0.0;
+            for (int q = 0; q < kClu; ++q) t += ld_dsm_f64(&acc[o], q);
+            if (o < S) {
+                if (salive[o]) sscore[3 * o] += t, sscore[3 * o + 2] += t;
+            } else if ((o - S - head + W) % W < count) {  // a live local
+                lscore[3 * (o - S)] += t;
+                lscore[3 * (o - S) + 2] += t;
+            }
+        }
+        cl_sync();  // every score update visible, every remote read done
+        if (rank != 0) return;
+    } else {
+        for (int s = tid; s < S; s += kT)
+            if (salive[s]) sscore[3 * s] += acc[s], sscore[3 * s + 2] += acc[s];
+        for (int li = tid; li < count; li += kT) {
+            const int ring = (head + li) % W;
+            lscore[3 * ring] += acc[S + ring];
+            lscore[3 * ring + 2] += acc[S + ring];
+        }
     }
     // 9. score window rotation every l_win steps (engine.cpp:196-200)
     int wfill = s_meta[3] + 1;
@@ -748,18 +873,42 @@ cudaError_t launch_decode_step(const Dims& m, int dtype, int S, int W, int T, in
     a.probs = reinterpret_cast<float*>(take(U * m.G * R * 4));
     a.pmean = reinterpret_cast<float*>(take(U * R * 4));
     const bool wide = m.units < 148;  // few units: more warps per unit; many: more units per SM
-    const int threads = wide ? kTMax : 256;
-    const size_t smem = (size_t)max(S + W, (threads / 32) * m.d) * 8 + (size_t)m.G * m.d * 4;
+    // a unit split over a cluster of kDecClu CTAs when the grid is small and the rows many
+    static const int force_clu = [] {
+        const char* e = getenv("EMS_DECODE_CLUSTER");  // 0 never, 1 always (A/B, tests)
+        return e ? atoi(e) : -1;
+    }();
+    const bool clu = force_clu >= 0 ? force_clu == 1 : m.units * kDecClu <= 2 * 148;
+    const int threads = wide || clu ? kTMax : 256;
+    const size_t smem =
+        (size_t)max(S + W, (threads / 32) * m.d) * 8 + (size_t)((m.G * m.d + 1) & ~1) * 4 + (size_t)m.G * m.d * 8;
     const int gb = m.G <= 1 ? 1 : m.G <= 2 ? 2 : m.G <= 4 ? 4 : 8;
     void (*fn)(DecArgs) = nullptr;
-#define EMS_DEC_PICK(K)                                                                          \
-    if (gb == K) fn = wide ? decode_step_kernel<K, kTMax, 1> : decode_step_kernel<K, 256, 3>;
+#define EMS_DEC_PICK(K)                                                                                   \
+    if (gb == K)                                                                                          \
+        fn = clu ? decode_step_kernel<K, kTMax, 1, kDecClu>                                               \
+                 : (wide ? decode_step_kernel<K, kTMax, 1, 1> : decode_step_kernel<K, 256, 3, 1>);
     EMS_DEC_PICK(1) EMS_DEC_PICK(2) EMS_DEC_PICK(4) EMS_DEC_PICK(8)
 #undef EMS_DEC_PICK
     if (!fn || m.G > 8) return cudaErrorInvalidValue;
     if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    fn<<<m.units, threads, smem, s>>>(a);
-    return cudaGetLastError();
+    if (!clu) {
+        fn<<<m.units, threads, smem, s>>>(a);
+        return cudaGetLastError();
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(m.units * kDecClu);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = kDecClu;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, fn, a);
 }
 
 size_t decode_workspace_bytes(const Dims& m, int R) {
