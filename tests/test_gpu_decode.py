@@ -142,3 +142,16 @@ def test_decode_from_device_prefill_bf16_deterministic():
     meta = res[0][1]["meta"].cpu()
     assert (meta[:, 1] == cfg.l_win).all()            # locals back at the window size
     assert (meta[:, 5] == cfg.n_budget - cfg.l_win).all()  # centers at capacity
+
+
+def test_decode_single_cta_variant_forced():
+    """The launch splits a unit over a cluster when the grid is small; the one-CTA-per-unit
+    kernel (large batches) is forced once in a fresh process over the same parity cases."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, EMS_DECODE_CLUSTER="0")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider", __file__,
+                        "-k", "matches_reference or keep_all or window_rotation or gqa"],
+                       env=env, capture_output=True, text=True, cwd=os.path.dirname(os.path.dirname(__file__)))
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
