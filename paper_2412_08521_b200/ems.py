@@ -370,6 +370,24 @@ class Plan:
                     lut_slot=g("lut_slot")[:nu].numpy())
 
 
+def cache_dump_json(c: dict, head_dim: int) -> str:
+    """cache_dump_json (proj/src/cache.cpp:114-150) of a unit's cache as returned by
+    Plan.unit_cache / DecodeState.unit_cache: the reference's schema and key order (centers
+    by slot, locals oldest first, LUT in order), so its tooling reads GPU caches directly."""
+    import json
+    slots = c.get("slots", range(len(c["position"])))
+    trip = lambda t: {"glo": float(t[0]), "loc_past": float(t[1]), "loc_cur": float(t[2])}  # noqa: E731
+    centers = [{"slot": int(s), "position": int(c["position"][i]), "key_norm": float(c["key_norm"][i]),
+                "unit_key": [float(x) for x in c["unit_key"][i]], "value": [float(x) for x in c["value"][i]],
+                "score": trip(c["score"][i])} for i, s in enumerate(slots)]
+    locals_ = [{"position": int(c["local_position"][i]), "key": [float(x) for x in c["local_key"][i]],
+                "value": [float(x) for x in c["local_value"][i]], "score": trip(c["local_score"][i])}
+               for i in range(len(c["local_position"]))]
+    lut = [{"position": int(p), "slot": int(s)} for p, s in zip(c["lut_position"], c["lut_slot"])]
+    return json.dumps({"head_dim": int(head_dim), "compressed": bool(c["compressed"]), "centers": centers,
+                       "locals": locals_, "lut": lut}, indent=2)
+
+
 # -- reference-shaped conveniences ----------------------------------------------------
 def prefill_compress(q_rot, k_rot, k_raw, v, cfg: EmsConfig, want_out=True, score_impl="auto",
                      first_position=0) -> Plan:

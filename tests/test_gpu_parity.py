@@ -216,3 +216,23 @@ def test_gpu_select_variants_forced(forced):
                         "-k", "configs_vs_oracle or golden_cache or reference_cases"],
                        env=env, capture_output=True, text=True, cwd=os.path.dirname(os.path.dirname(__file__)))
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+def test_gpu_cache_dump_json_round_trips_through_reference_schema():
+    """ems.cache_dump_json writes the reference's cache_dump_json schema (cache.cpp:114-150):
+    read back with the parser of that schema, every field of the GPU cache is unchanged."""
+    w = CONFIGS["cfgM"]
+    un = make_unit_np(w, seed=21, seq_len=1024, unit=0)
+    cfg = _cfg_of(w)
+    plan = run_gpu([un], w.dtype, cfg)
+    c = plan.unit_cache(0)
+    back = Cache.from_dump_json(ems.cache_dump_json(c, un.q_rot.shape[2]))
+    np.testing.assert_array_equal(back.position, c["position"])
+    np.testing.assert_array_equal(back.lut_position, c["lut_position"])
+    np.testing.assert_array_equal(back.lut_slot, c["lut_slot"])
+    np.testing.assert_array_equal(back.local_position, c["local_position"])
+    np.testing.assert_array_equal(back.unit_key, c["unit_key"])
+    np.testing.assert_array_equal(back.score, c["score"])
+    np.testing.assert_array_equal(back.value, c["value"])
+    np.testing.assert_array_equal(back.local_key, c["local_key"])
+    assert back.compressed == c["compressed"] and back.extra["slots"] == list(range(len(c["position"])))
