@@ -9,7 +9,7 @@ Differences from the reference battery, each deliberate:
     reference's 1e-9 / 1e-12 thresholds become fp32-level ones (stated per criterion);
   * head_dim is restricted to the sizes the kernels support (8..128);
   * criterion 4 (identity policy, "errors exactly 0") becomes "errors at fp32 rounding level";
-  * criterion 11 (diagnostics rates) is out of scope.
+  * criterion 11 runs the GPU diagnostics (csrc/diag.cu) against the brute-force oracles.
 """
 import numpy as np
 import pytest
@@ -264,6 +264,37 @@ def test_c10_merge_beats_evict_only(reflib):
         lb = np.mean([l2(ob[s], ref_outs[s]) for s in range(32)])
         wins += int(la < lb)
     assert wins >= 8, f"merge beats evict-only in {wins}/10"
+
+
+# -- 11. sparsity / redundancy rates against brute force, monotone in zeta and tau -------------
+def test_c11_diagnostics_vs_brute_force():
+    from tests.test_oracle_diagnostics import brute_redundancy, brute_sparsity
+    rng = np.random.default_rng(23000)
+    worst = 0.0
+    for _ in range(10):
+        n = 32
+        k, v = _f32(rng.standard_normal((n, 8))), _f32(rng.standard_normal((n, 8)))
+        score = _f32(rng.uniform(0.0, 1.0, n) + 1e-6)
+        s = _t(score)[None]
+        prev = 1.0
+        for zi in range(1, 11):  # glo = loc = score: align 1, combined = score
+            p = ems.sparsity_rate(s, s, 0.1 * zi).item()
+            worst = max(worst, abs(p - brute_sparsity(score, 0.1 * zi)))
+            assert p <= prev + 1e-15
+            prev = p
+        prev = 1.0
+        for ti in range(10):
+            r = ems.redundancy_rate(_t(k)[None], _t(v)[None], 0.1 * ti).item()
+            want = brute_redundancy(k, v, 0.1 * ti)
+            # fp32 similarities: a token within 1e-5 of tau may land on either side
+            best = np.array([max(float(np.dot(k[t], k[j]) / np.linalg.norm(k[t]) / np.linalg.norm(k[j])) *
+                                 float(np.dot(v[t], v[j]) / np.linalg.norm(v[t]) / np.linalg.norm(v[j]))
+                                 for j in range(t)) for t in range(1, n)])
+            near = int(np.sum(np.abs(best - 0.1 * ti) < 1e-5))
+            assert abs(r - want) * n <= near + 1e-9, (ti, r, want)
+            assert r <= prev + 1e-15
+            prev = r
+    assert worst <= 1e-12, worst
 
 
 # -- 12. determinism: the whole run twice, byte-identical ----------------------------------
