@@ -240,11 +240,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
 cudaError_t launch_colsum2_tc(const ColArgs& a, const CUtensorMap& tk, const CUtensorMap& tq,
                               cudaStream_t s) {
-    static bool attr = false;
-    if (!attr) {
+    static const bool attr = [] {  // once per process, thread-safe (magic static)
         cudaFuncSetAttribute(colsum2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
-        attr = true;
-    }
+        return true;
+    }();
+    (void)attr;
     const dim3 grid(2 * ((a.nT + 1) / 2) * a.units);
     colsum2_kernel<<<grid, kThreads, kSmem, s>>>(tk, tq, a);
     return cudaGetLastError();

@@ -276,12 +276,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 template <int kPoly>
 cudaError_t launch_t(const ColArgs& a, const CUtensorMap& tk, const CUtensorMap& tq, cudaStream_t s) {
-    static bool attr = false;
-    if (!attr) {
+    static const bool attr = [] {  // once per process, thread-safe (magic static)
         cudaFuncSetAttribute(colsum_tc_kernel<kPoly>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)kSmem);
-        attr = true;
-    }
+        return true;
+    }();
+    (void)attr;
     const dim3 grid(((a.nT + 1) / 2) * a.units * a.hsplit);
     colsum_tc_kernel<kPoly><<<grid, kThreads, kSmem, s>>>(tk, tq, a);
     return cudaGetLastError();

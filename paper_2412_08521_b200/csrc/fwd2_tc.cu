@@ -398,14 +398,14 @@ bool fwd2_tc_supported(int G, int nT) {
 cudaError_t launch_fwd2_tc(int L, int Hq, int Hkv, int G, int units, float c, void* out, float* nlse2,
                            float* lse_nat, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                            const void* k, float* kmax, cudaStream_t s, const void* q) {
-    static bool attr = false;
-    if (!attr) {
+    static const bool attr = [] {  // once per process, thread-safe (magic static)
         cudaFuncSetAttribute(fwd2_tc_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem2);
         cudaFuncSetAttribute(fwd2_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem2);
         cudaFuncSetAttribute(fwd2_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem2);
         cudaFuncSetAttribute(fwd2_tc_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem2);
-        attr = true;
-    }
+        return true;
+    }();
+    (void)attr;
     static const int poly = [] {  // pairs (of every 8) whose exp2 runs on the FMA pipe
         const char* e = getenv("EMS_P1_POLY");
         return e ? atoi(e) : 2;

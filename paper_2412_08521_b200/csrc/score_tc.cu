@@ -348,12 +348,12 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 template <int kPoly>
 void fwd_launch(int grid, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                 const FwdArgs& fa, cudaStream_t s) {
-    static bool attr = false;
-    if (!attr) {
+    static const bool attr = [] {  // once per process, thread-safe (magic static)
         cudaFuncSetAttribute(fwd_tc_kernel<kPoly>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)kFwdSmem);
-        attr = true;
-    }
+        return true;
+    }();
+    (void)attr;
     fwd_tc_kernel<kPoly><<<grid, kFwdThreads, kFwdSmem, s>>>(tq, tk, tv, fa);
 }
 
