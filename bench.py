@@ -384,6 +384,25 @@ def main():
     achieved = flops / (score_ms / 1e3) / 1e12
     peak_tf = pk.get("bf16_tflops", FALLBACK_PEAKS["bf16_tflops"])
     roof_ms = max(flops / (peak_tf * 1e12), score_bytes(w) / (pk.get("hbm_gbs", 6650.0) * 1e9)) * 1e3
+    # the optional gather of every rank's fixed-size compressed caches, off the
+    # timed path and reported on its own: one NCCL all_gather per cache tensor
+    gather_ms = None
+    if ws > 1:
+        try:
+            from paper_2412_08521_b200.shard import gather_caches, unit_shard
+            shard = unit_shard(1, ws * plan.dims.units, ws, rank)
+            gather_caches(plan.cache, shard, ws * plan.dims.units)  # warm-up (NCCL communicators)
+            barrier()
+            g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            g0.record(stream)
+            gather_caches(plan.cache, shard, ws * plan.dims.units)
+            g1.record(stream)
+            barrier()
+            tg = torch.tensor([g0.elapsed_time(g1)], device=dev)
+            dist.all_reduce(tg, op=dist.ReduceOp.MAX)
+            gather_ms = tg.item()
+        except Exception as ex:  # noqa: BLE001 -- informational; never fails the bench line
+            gather_ms = f"unavailable: {str(ex)[:120]}"
     # our kernel launches per step, counted by the CUDA profiler on one extra (untimed) step:
     # every kernel of libems_b200.so lives in namespace ems
     from torch.profiler import ProfilerActivity, profile
@@ -412,6 +431,8 @@ def main():
             "energy_j_per_step": (clk.energy_j() / args.steps) if clk.energy_j() is not None else None,
             "e2e": e2e,
         }
+        if gather_ms is not None:
+            line["cache_allgather_ms"] = gather_ms  # outside the timed region
         if not args.no_cpu_baseline and ws == 1:
             try:
                 tok, desc, cores, _ = _cpu_sample(w, 2.5 * args.cpu_seconds)
