@@ -153,3 +153,12 @@ def test_cfg5_properties():
     _check_invariants(w, plan, q.shape[2])
     del q, kr, kw, v, plan
     torch.cuda.empty_cache()
+
+
+def test_cfg4_batch32_properties():
+    """Config 4 at B = 32 (256 units, L = 8192, rank-r keys): mass, selection and layout."""
+    w = CONFIGS["cfg4"].with_(batch=32)
+    q, kr, kw, v, plan = _run(w)
+    _check_invariants(w, plan, q.shape[2])
+    del q, kr, kw, v, plan
+    torch.cuda.empty_cache()
