@@ -268,7 +268,7 @@ def main():
                     help="CPU work budget per reference sample (ours arm uses 2.5x for cpu_baseline)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--e2e-chunks", type=int, default=4, help="unit groups of the host copy/compute pipeline")
+    ap.add_argument("--e2e-chunks", type=int, default=8, help="unit groups of the host copy/compute pipeline")
     args = ap.parse_args()
 
     from paper_2412_08521_b200.inputs import CONFIGS

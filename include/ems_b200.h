@@ -219,6 +219,10 @@ EMS_API int ems_prefill(const ems_desc* desc, double rope_base, const void* q, c
  * RoPE runs on the device into d_q_rot/d_k_rot (h_k_raw/d_k_raw unused); rope_base == 0:
  * h_q/h_k are pre-rotated and h_k_raw/d_k_raw carry the raw keys.  Asynchronous: on return
  * `stream` is ordered after every copy, so synchronising it completes the call. */
+/* Workspace that lets ems_prefill_host keep two unit groups in flight (odd groups on a second,
+ * library-owned stream with the second half of the workspace); with ems_workspace_bytes() the
+ * groups run one at a time on `stream`. */
+EMS_API size_t ems_prefill_host_workspace_bytes(const ems_desc* desc);
 EMS_API int ems_prefill_host(const ems_desc* desc, double rope_base, const void* h_q, const void* h_k,
                      const void* h_k_raw, const void* h_v, void* d_q, void* d_k, void* d_k_raw,
                      void* d_v, void* d_q_rot, void* d_k_rot, void* out_o, float* lse, float* glo,

@@ -378,6 +378,11 @@ size_t ems_workspace_bytes(const ems_desc* d) {
     return workspace_need(*d);
 }
 
+size_t ems_prefill_host_workspace_bytes(const ems_desc* d) {
+    if (ems_validate(d) != EMS_OK) return 0;
+    return 2 * ems::align_up(ems::workspace_need(*d));
+}
+
 int ems_score(const ems_desc* d, const void* q, const void* k, const void* v, void* out_o,
               float* lse, float* glo, float* loc, void* ws, size_t ws_bytes, cudaStream_t s) {
     if (int rc = ems_validate(d)) return rc;
@@ -599,8 +604,15 @@ namespace {
 struct HostPipeRes {
     int device = -1;
     cudaStream_t copy = nullptr;
+    cudaStream_t comp2 = nullptr;  // second compute stream (two unit groups in flight)
     std::vector<cudaEvent_t> ev;
 };
+
+// With two workspaces, odd groups run on a second stream with the second workspace; the
+// status word of that workspace is merged into the caller's at the end.
+__global__ void merge_status_kernel(DevStatus* dst, const DevStatus* src) {
+    if (dst->code == 0 && src->code != 0) *dst = *src;
+}
 thread_local HostPipeRes g_pipe[8];
 
 HostPipeRes* pipe_res(int nev) {
@@ -608,6 +620,8 @@ HostPipeRes* pipe_res(int nev) {
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 8) return nullptr;
     HostPipeRes& r = g_pipe[dev];
     if (r.copy == nullptr && cudaStreamCreateWithFlags(&r.copy, cudaStreamNonBlocking) != cudaSuccess)
+        return nullptr;
+    if (r.comp2 == nullptr && cudaStreamCreateWithFlags(&r.comp2, cudaStreamNonBlocking) != cudaSuccess)
         return nullptr;
     while ((int)r.ev.size() < nev) {
         cudaEvent_t e;
@@ -655,7 +669,7 @@ extern "C" int ems_prefill_host(const ems_desc* d, double rope_base, const void*
     const Dims m = make_dims(*d);
     const int U = m.units, G = m.G;
     int nc = chunks < 1 ? 1 : (chunks > U ? U : chunks);
-    HostPipeRes* res = pipe_res(2 * nc + 2);
+    HostPipeRes* res = pipe_res(2 * nc + 4);
     if (!res) {
         set_error("ems_prefill_host: could not create copy stream / events");
         return EMS_CUDA_ERROR;
@@ -678,10 +692,19 @@ extern "C" int ems_prefill_host(const ems_desc* d, double rope_base, const void*
         {(void* ems_cache::*)&ems_cache::lut_slot, (size_t)(m.cap_lut > 0 ? m.cap_lut : 1) * 4},
         {(void* ems_cache::*)&ems_cache::counts, 16},
     };
+    // two unit groups in flight (odd groups on a second stream and workspace) when the caller
+    // passed ems_prefill_host_workspace_bytes(); one at a time otherwise
+    const size_t one = align_up(workspace_need(*d));
+    const bool dual = nc >= 2 && ws_bytes >= 2 * one;
+    void* ws2 = dual ? off(ws, one) : nullptr;
+    cudaStream_t s2 = dual ? res->comp2 : s;
     EMS_CUDA_CHECK(cudaMemsetAsync(ws, 0, sizeof(DevStatus), s));
-    // the copy stream must not overwrite device inputs that earlier work on `s` still reads
+    if (dual) EMS_CUDA_CHECK(cudaMemsetAsync(ws2, 0, sizeof(DevStatus), s));
+    // the copy stream (and the second compute stream) must not overwrite device inputs that
+    // earlier work on `s` still reads
     EMS_CUDA_CHECK(cudaEventRecord(ev[2 * nc], s));
     EMS_CUDA_CHECK(cudaStreamWaitEvent(cs, ev[2 * nc], 0));
+    if (dual) EMS_CUDA_CHECK(cudaStreamWaitEvent(s2, ev[2 * nc], 0));
     // Geometric groups (U / 2^(nc-1), ..., U / 4, U / 2 units): the first group's inputs land
     // after a small copy, so compute starts early; later groups are large (efficient grids)
     // and their copies finish while earlier groups compute.
@@ -717,35 +740,43 @@ extern "C" int ems_prefill_host(const ems_desc* d, double rope_base, const void*
         sub.heads_kv = n;
         sub.heads_q = n * G;
         const size_t oq = (size_t)u0 * G * row, ok = (size_t)u0 * row;
-        EMS_CUDA_CHECK(cudaStreamWaitEvent(s, ev[c], 0));
+        cudaStream_t sc = (c & 1) ? s2 : s;
+        void* wsc = dual && (c & 1) ? ws2 : ws;
+        EMS_CUDA_CHECK(cudaStreamWaitEvent(sc, ev[c], 0));
         const void* qr = off(d_q, oq);
         const void* kr = off(d_k, ok);
         const void* kraw = rope ? kr : off(d_k_raw, ok);
         if (rope) {
             EMS_CUDA_CHECK(launch_rope(d->dtype, n * G, m.L, m.d, rope_base, d->first_position, qr,
-                                       off(d_q_rot, oq), s));
+                                       off(d_q_rot, oq), sc));
             EMS_CUDA_CHECK(launch_rope(d->dtype, n, m.L, m.d, rope_base, d->first_position, kr,
-                                       off(d_k_rot, ok), s));
+                                       off(d_k_rot, ok), sc));
             qr = off(d_q_rot, oq);
             kr = off(d_k_rot, ok);
         }
-        ems_cache sc = *d_cache;
-        for (const CacheField& f : fields) sc.*f.ptr = off(d_cache->*f.ptr, (size_t)u0 * f.per_unit);
+        ems_cache scache = *d_cache;
+        for (const CacheField& f : fields) scache.*f.ptr = off(d_cache->*f.ptr, (size_t)u0 * f.per_unit);
         const size_t ol = (size_t)u0 * m.L;
         if (int rc = run_path(&sub, qr, kr, kraw, off(d_v, ok), off(out_o, oq), off(lse, (size_t)u0 * G * m.L * 4),
-                              off(glo, ol * 4), off(loc, ol * 4), nullptr, sc, ws, s, u0))
+                              off(glo, ol * 4), off(loc, ol * 4), nullptr, scache, wsc, sc, u0))
             return rc;
-        EMS_CUDA_CHECK(cudaEventRecord(ev[nc + c], s));
+        EMS_CUDA_CHECK(cudaEventRecord(ev[nc + c], sc));
         if (h_cache) {
             EMS_CUDA_CHECK(cudaStreamWaitEvent(cs, ev[nc + c], 0));
             for (const CacheField& f : fields)
-                EMS_CUDA_CHECK(cudaMemcpyAsync(off(h_cache->*f.ptr, (size_t)u0 * f.per_unit), sc.*f.ptr,
+                EMS_CUDA_CHECK(cudaMemcpyAsync(off(h_cache->*f.ptr, (size_t)u0 * f.per_unit), scache.*f.ptr,
                                                (size_t)n * f.per_unit, cudaMemcpyDeviceToHost, cs));
         }
     }
-    // the caller synchronises `s`: make it cover the last cache copy
+    // the caller synchronises `s`: make it cover the last cache copy and the second stream
     EMS_CUDA_CHECK(cudaEventRecord(ev[2 * nc + 1], cs));
     EMS_CUDA_CHECK(cudaStreamWaitEvent(s, ev[2 * nc + 1], 0));
+    if (dual) {
+        EMS_CUDA_CHECK(cudaEventRecord(ev[2 * nc + 2], s2));
+        EMS_CUDA_CHECK(cudaStreamWaitEvent(s, ev[2 * nc + 2], 0));
+        merge_status_kernel<<<1, 1, 0, s>>>(static_cast<DevStatus*>(ws), static_cast<const DevStatus*>(ws2));
+        EMS_CUDA_CHECK(cudaGetLastError());
+    }
     return EMS_OK;
 }
 

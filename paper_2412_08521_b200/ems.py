@@ -107,6 +107,8 @@ def lib() -> C.CDLL:
         L.ems_status_string.restype = C.c_char_p
         L.ems_workspace_bytes.restype = C.c_size_t
         L.ems_workspace_bytes.argtypes = [C.POINTER(Desc)]
+        L.ems_prefill_host_workspace_bytes.restype = C.c_size_t
+        L.ems_prefill_host_workspace_bytes.argtypes = [C.POINTER(Desc)]
         L.ems_validate.argtypes = [C.POINTER(Desc)]
         L.ems_cache_dims_for.argtypes = [C.POINTER(Desc), C.POINTER(CacheDims)]
         vp, fp = C.c_void_p, C.c_void_p
@@ -260,6 +262,7 @@ class Plan:
     def run(self, q_rot, k_rot, k_raw, v, stream=None) -> None:
         """Whole path (ems_prefill_compress), asynchronous on the current stream."""
         self._check_inputs(q_rot, k_rot, k_raw, v)
+        self._status_ws = None
         _check(lib().ems_prefill_compress(C.byref(self.desc), _p(q_rot), _p(k_rot), _p(k_raw), _p(v),
                                           _p(self.out), _p(self.lse), _p(self.glo), _p(self.loc),
                                           C.byref(self._cstage), C.byref(self._ccache),
@@ -270,6 +273,7 @@ class Plan:
         """engine::prefill on RAW Q/K (ems_prefill): RoPE on the device into the plan's
         q_rot/k_rot scratch, then the whole path with k as the pre-RoPE keys."""
         self._check_inputs(q, k, k, v)
+        self._status_ws = None
         if rope_base > 0 and getattr(self, "q_rot", None) is None:
             D = self.desc
             self.q_rot = torch.empty((D.batch, D.heads_q, D.seq_len, D.head_dim), dtype=self.dtype,
@@ -290,7 +294,7 @@ class Plan:
             self._hcache = CCache(*[_p(self._host_cache[f]) for f, _ in CCache._fields_])
         return self._host_cache
 
-    def run_host(self, h_q, h_k, h_v, rope_base: float, h_k_raw=None, chunks: int = 4, stream=None) -> dict:
+    def run_host(self, h_q, h_k, h_v, rope_base: float, h_k_raw=None, chunks: int = 8, stream=None) -> dict:
         """engine::prefill from HOST (pinned) tensors (ems_prefill_host): the library stages the
         inputs in `chunks` groups of units and overlaps each group's host-to-device copy with
         the previous group's compute; every group's compressed cache is copied back to the
@@ -319,22 +323,28 @@ class Plan:
                 raise InvalidArgument("pre-rotated inputs (rope_base == 0) need h_k_raw")
             kraw_d = st.setdefault("k_raw", torch.empty(ks, dtype=self.dtype, device=self.device))
         hc = self.host_cache()
+        if getattr(self, "_ws_host", None) is None:  # room for two unit groups in flight
+            self._ws_host = torch.empty(lib().ems_prefill_host_workspace_bytes(C.byref(self.desc)), dtype=torch.uint8,
+                                        device=self.device)
+        self._status_ws = self._ws_host
         _check(lib().ems_prefill_host(
             C.byref(self.desc), float(rope_base), _p(h_q), _p(h_k), _p(h_k_raw), _p(h_v), _p(st["q"]), _p(st["k"]),
             _p(kraw_d), _p(st["v"]), _p(self.q_rot) if rope_base > 0 else None,
             _p(self.k_rot) if rope_base > 0 else None, _p(self.out), _p(self.lse), _p(self.glo), _p(self.loc),
-            C.byref(self._ccache), C.byref(self._hcache), int(chunks), _p(self.workspace), self.workspace.numel(),
+            C.byref(self._ccache), C.byref(self._hcache), int(chunks), _p(self._ws_host), self._ws_host.numel(),
             _stream(stream), None))
         return hc
 
     def score(self, q_rot, k_rot, v=None, stream=None) -> None:
         self._check_inputs(q_rot, k_rot, None, v)
+        self._status_ws = None
         _check(lib().ems_score(C.byref(self.desc), _p(q_rot), _p(k_rot), _p(v),
                                _p(self.out) if v is not None else None, _p(self.lse), _p(self.glo),
                                _p(self.loc), _p(self.workspace), self.workspace.numel(),
                                _stream(stream)))
 
     def select(self, stream=None) -> None:
+        self._status_ws = None
         _check(lib().ems_select(C.byref(self.desc), _p(self.glo), _p(self.loc), C.byref(self._cstage),
                                 _p(self.workspace), self.workspace.numel(), _stream(stream)))
 
@@ -348,8 +358,10 @@ class Plan:
                                  self.workspace.numel(), _stream(stream)))
 
     def sync_status(self, stream=None) -> None:
-        """Synchronise and raise the first data-dependent error the kernels recorded."""
-        _check(lib().ems_sync_status(C.byref(self.desc), _p(self.workspace), _stream(stream)))
+        """Synchronise and raise the first data-dependent error the kernels recorded (in the
+        workspace of the last run: the plan's, or run_host's larger one)."""
+        ws = getattr(self, "_status_ws", None)
+        _check(lib().ems_sync_status(C.byref(self.desc), _p(self.workspace if ws is None else ws), _stream(stream)))
 
     def unit_cache(self, u: int) -> dict:
         """Host copy of unit u's compressed cache, trimmed to its counts."""
@@ -427,7 +439,7 @@ def prefill(q, k, v, cfg: EmsConfig, rope_base: float, want_out=True, score_impl
     return plan
 
 
-def prefill_host(q, k, v, cfg: EmsConfig, rope_base: float, chunks: int = 4, want_out=True, score_impl="auto",
+def prefill_host(q, k, v, cfg: EmsConfig, rope_base: float, chunks: int = 8, want_out=True, score_impl="auto",
                  first_position=0) -> Plan:
     """engine::prefill (proj/src/engine.cpp:42-82) on pinned HOST [B][H][L][d] tensors, the
     reference's own calling convention: copies pipelined with compute (ems_prefill_host).
