@@ -294,12 +294,14 @@ class Plan:
             self._hcache = CCache(*[_p(self._host_cache[f]) for f, _ in CCache._fields_])
         return self._host_cache
 
-    def run_host(self, h_q, h_k, h_v, rope_base: float, h_k_raw=None, chunks: int = 8, stream=None) -> dict:
+    def run_host(self, h_q, h_k, h_v, rope_base: float, h_k_raw=None, chunks: int = 8, stream=None,
+                 concurrent: bool = True) -> dict:
         """engine::prefill from HOST (pinned) tensors (ems_prefill_host): the library stages the
         inputs in `chunks` groups of units and overlaps each group's host-to-device copy with
         the previous group's compute; every group's compressed cache is copied back to the
         pinned host cache as soon as it is done.  rope_base > 0: raw Q/K, RoPE on the device;
-        rope_base == 0: pre-rotated Q/K plus h_k_raw.  Asynchronous; returns the host cache."""
+        rope_base == 0: pre-rotated Q/K plus h_k_raw.  concurrent: two groups in flight (a
+        second workspace, ems_prefill_host_workspace_bytes).  Asynchronous; returns the host cache."""
         D = self.desc
         qs = (D.batch, D.heads_q, D.seq_len, D.head_dim)
         ks = (D.batch, D.heads_kv, D.seq_len, D.head_dim)
@@ -323,15 +325,16 @@ class Plan:
                 raise InvalidArgument("pre-rotated inputs (rope_base == 0) need h_k_raw")
             kraw_d = st.setdefault("k_raw", torch.empty(ks, dtype=self.dtype, device=self.device))
         hc = self.host_cache()
-        if getattr(self, "_ws_host", None) is None:  # room for two unit groups in flight
+        if concurrent and getattr(self, "_ws_host", None) is None:  # room for two unit groups in flight
             self._ws_host = torch.empty(lib().ems_prefill_host_workspace_bytes(C.byref(self.desc)), dtype=torch.uint8,
                                         device=self.device)
-        self._status_ws = self._ws_host
+        ws = self._ws_host if concurrent else self.workspace
+        self._status_ws = ws
         _check(lib().ems_prefill_host(
             C.byref(self.desc), float(rope_base), _p(h_q), _p(h_k), _p(h_k_raw), _p(h_v), _p(st["q"]), _p(st["k"]),
             _p(kraw_d), _p(st["v"]), _p(self.q_rot) if rope_base > 0 else None,
             _p(self.k_rot) if rope_base > 0 else None, _p(self.out), _p(self.lse), _p(self.glo), _p(self.loc),
-            C.byref(self._ccache), C.byref(self._hcache), int(chunks), _p(self._ws_host), self._ws_host.numel(),
+            C.byref(self._ccache), C.byref(self._hcache), int(chunks), _p(ws), ws.numel(),
             _stream(stream), None))
         return hc
 

@@ -99,3 +99,23 @@ def test_host_pipeline_rejects_pageable_and_missing_kraw():
         plan.run_host(x, kk.pin_memory(), kk.pin_memory(), 1e4)  # pageable q
     with pytest.raises(ems.InvalidArgument):
         plan.run_host(x.pin_memory(), kk.pin_memory(), kk.pin_memory(), 0.0)  # no k_raw
+
+
+def test_host_pipeline_concurrent_groups_equal_sequential():
+    """Two unit groups in flight (second stream + workspace) give the same bits as one at a time."""
+    w = CONFIGS["cfg3"]
+    rng = np.random.default_rng(4)
+    H, G, L = 6, 4, 1024
+    dt = torch.bfloat16
+    q, k, v = (torch.tensor(rng.standard_normal(s)).to(dt).pin_memory()
+               for s in ((1, H * G, L, 128), (1, H, L, 128), (1, H, L, 128)))
+    cfg = ems.EmsConfig(w.n_budget, w.l_win, w.tau, w.gamma, w.kernel_size)
+    plan = ems.Plan(1, H * G, H, L, 128, dt, cfg, "cuda")
+    res = []
+    for concurrent in (False, True):
+        hc = plan.run_host(q, k, v, w.rope_base, chunks=6, concurrent=concurrent)
+        plan.sync_status()
+        res.append(({n: t.clone() for n, t in hc.items()}, plan.glo.clone(), plan.out.clone()))
+    for n in res[0][0]:
+        assert torch.equal(res[0][0][n], res[1][0][n]), n
+    assert torch.equal(res[0][1], res[1][1]) and torch.equal(res[0][2], res[1][2])
