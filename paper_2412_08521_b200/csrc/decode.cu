@@ -1,4 +1,5 @@
-// decode.cu -- (f2) the EMS decode step on the device: one CTA per KV unit.
+// decode.cu -- (f2) the EMS decode step on the device: one CTA per KV unit,
+// or, for small grids, a cluster of 8 CTAs per unit (see decode_step_kernel).
 //
 // Restates, per head (unit), decode_step (proj/src/engine.cpp:150-210):
 //   append the raw (k, v) to the local window; expand the cache through its look-up table
@@ -17,8 +18,9 @@
 // GQA (contract D2): the G query heads of a unit attend the same cache; the mass flowing
 // back is the mean of their probabilities.
 // Numerics: keys/values fp32, logits fp32 dot products, softmax exp in fp32 with an fp64
-// normaliser, value sums and all score accumulators in fp64.  Every reduction runs in a
-// fixed order (no float atomics) -> deterministic.
+// normaliser, value sums in fp32 per warp slice combined in fp64, all score accumulators in
+// fp64.  Every reduction runs in a fixed order (no float atomics) -> deterministic for a
+// given launch shape.
 #include <float.h>
 
 #include "common.cuh"
