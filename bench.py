@@ -249,9 +249,10 @@ def config_dict(w, n):
                         f"d={w.head_dim} L={w.seq_len} {w.dtype} budget={w.n_budget} w={w.l_win} "
                         f"gamma={w.gamma} tau={w.tau} kernel={w.kernel_size}"
             if w.name.startswith("cfg3") else f"{w.name}",
-            "global_batch": w.batch * n, "seq_len": w.seq_len, "units_per_gpu": w.units,
+            "global_batch": w.batch * n, "seq_len": w.seq_len, "layers": w.layers, "units_per_gpu": w.units,
             "parallelism": f"kv-unit sharding x{n} (weak, no collective)",
-            "l2": "inputs > L2 (Q alone 268 MB), no flush"}
+            "l2": (f"inputs > L2 (Q alone {w.batch * w.heads_q * w.seq_len * w.head_dim * (2 if w.dtype == 'bf16' else 4) / 1e6:.0f} MB"
+                   f" per layer), no flush")}
 
 
 def main():
@@ -294,20 +295,28 @@ def main():
     if ws > 1:
         dist.init_process_group("nccl", device_id=dev)
     cfg = ems.EmsConfig(w.n_budget, w.l_win, w.tau, w.gamma, w.kernel_size)
-    q, kr, kw, v = make_batch_torch(w, seed=1 + rank, device=dev)
+    # a step runs every layer of the workload (config 4: 32); layers alternate between two
+    # distinct input sets (each layer's inputs are far larger than L2, so nothing is reused)
+    n_layers = w.layers
+    sets = [make_batch_torch(w, seed=1 + rank, device=dev, layer=l) for l in range(min(n_layers, 2))]
+    q, kr, kw, v = sets[0]
     B, Hq, L, d = q.shape
     plan = ems.Plan(B, Hq, w.heads_kv, L, d, q.dtype, cfg, dev, args.score_impl, want_out=True)
     stream = torch.cuda.current_stream()
 
-    def step(mid_event=None):
-        """One step through the staged C-ABI entry points (same kernels as ems_prefill_compress);
-        mid_event brackets the score pass for the roofline."""
-        plan.score(q, kr, v)
-        if mid_event is not None:
-            mid_event.record(stream)
-        plan.select()
-        plan.merge(kw, v)
-        plan.compact(kw, v)
+    def step(score_events=None):
+        """One step through the staged C-ABI entry points (same kernels as ems_prefill_compress),
+        all layers; score_events[l] = (start, end) bracket layer l's score pass for the roofline."""
+        for li in range(n_layers):
+            ql, krl, kwl, vl = sets[li % len(sets)]
+            if score_events is not None:
+                score_events[li][0].record(stream)
+            plan.score(ql, krl, vl)
+            if score_events is not None:
+                score_events[li][1].record(stream)
+            plan.select()
+            plan.merge(kwl, vl)
+            plan.compact(kwl, vl)
 
     def barrier():
         if ws > 1:
@@ -321,8 +330,9 @@ def main():
     barrier()
     # timed region: per-step events bracket the score pass and the whole step
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    mids = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    sev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n_layers)]
+           for _ in range(args.steps)]
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
     barrier()
@@ -330,15 +340,15 @@ def main():
     t_start.record(stream)
     for i in range(args.steps):
         starts[i].record(stream)
-        step(mids[i])
+        step(sev[i])
         ends[i].record(stream)
     t_end.record(stream)
     barrier()
     clk.end()
     plan.sync_status()
     total_ms = t_start.elapsed_time(t_end)
-    score_ms = sum(starts[i].elapsed_time(mids[i]) for i in range(args.steps)) / args.steps
-    tail_ms = sum(mids[i].elapsed_time(ends[i]) for i in range(args.steps)) / args.steps
+    score_ms = sum(a.elapsed_time(b) for i in range(args.steps) for a, b in sev[i]) / args.steps
+    tail_ms = sum(starts[i].elapsed_time(ends[i]) for i in range(args.steps)) / args.steps - score_ms
     t = torch.tensor([total_ms], device=dev)
     if ws > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -352,15 +362,19 @@ def main():
     e2e = None
     if not args.no_e2e:
         base = w.rope_base or 0.0
-        q_raw = unrope(q, base) if base else q
-        hq, hk, hv = (x.cpu().pin_memory() for x in (q_raw, kw, v))
-        del q_raw
+        hsets = []
+        for ql, _, kwl, vl in sets:
+            q_raw = unrope(ql, base) if base else ql
+            hsets.append(tuple(x.cpu().pin_memory() for x in (q_raw, kwl, vl)))
+            del q_raw
         host_cache = plan.host_cache()
-        h2d = sum(x.numel() * x.element_size() for x in (hq, hk, hv))
-        d2h = sum(x.numel() * x.element_size() for x in host_cache.values())
+        h2d = n_layers * sum(x.numel() * x.element_size() for x in hsets[0])
+        d2h = n_layers * sum(x.numel() * x.element_size() for x in host_cache.values())
 
-        def e2e_step():
-            plan.run_host(hq, hk, hv, base, h_k_raw=None if base else hk, chunks=args.e2e_chunks)
+        def e2e_step():  # every layer: its host inputs in, its compressed cache out
+            for li in range(n_layers):
+                hq, hk, hv = hsets[li % len(hsets)]
+                plan.run_host(hq, hk, hv, base, h_k_raw=None if base else hk, chunks=args.e2e_chunks)
 
         for _ in range(2):
             e2e_step()
@@ -380,10 +394,10 @@ def main():
                "api": f"ems.Plan.run_host (ems_prefill_host, raw Q/K + device RoPE, {args.e2e_chunks} chunks)"}
 
     pk = peaks()
-    flops = f_alg(w)
+    flops = f_alg(w) * n_layers  # every layer's score pass
     achieved = flops / (score_ms / 1e3) / 1e12
     peak_tf = pk.get("bf16_tflops", FALLBACK_PEAKS["bf16_tflops"])
-    roof_ms = max(flops / (peak_tf * 1e12), score_bytes(w) / (pk.get("hbm_gbs", 6650.0) * 1e9)) * 1e3
+    roof_ms = max(flops / (peak_tf * 1e12), n_layers * score_bytes(w) / (pk.get("hbm_gbs", 6650.0) * 1e9)) * 1e3
     # the optional gather of every rank's fixed-size compressed caches, off the
     # timed path and reported on its own: one NCCL all_gather per cache tensor
     gather_ms = None
@@ -407,7 +421,7 @@ def main():
     # every kernel of libems_b200.so lives in namespace ems
     from torch.profiler import ProfilerActivity, profile
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
-        step(mids[0])
+        step()
         torch.cuda.synchronize()
     kernels_per_step = sum(e.count for e in prof.key_averages() if e.device_time_total > 0 and "ems::" in e.key)
     if rank == 0:
@@ -424,7 +438,7 @@ def main():
                          "frac_of_sustained_peak": achieved / pk.get("bf16_tflops_sustained", peak_tf),
                          "kernel": "score pass (O+LSE and glo/loc column sums)",
                          "peak_source": f"{pk['source']} bf16_tflops (burst)",
-                         "algorithmic_flops_per_launch": flops},
+                         "algorithmic_flops_per_launch": f_alg(w)},
             "gpu_launches": kernels_per_step * args.steps,
             "clocks": clk.summary(),
             "step_ms": [round(starts[i].elapsed_time(ends[i]), 3) for i in range(args.steps)],
