@@ -612,22 +612,40 @@ __global__ void __launch_bounds__(kTh, kMinB) decode_step_kernel(DecArgs a) {
         };
         tb = bselect(tb, least, shc);
         const int ts = tb.idx;
-        // R(tbm, c) for every other alive center: one warp per center
+        // R(tbm, c) for every other alive center: one warp per center; lane owns elements
+        // [4 lane, 4 lane + 4) (d <= 128, d % 4 == 0), the retiring center stays in registers
         double vv = 0.0;
         for (int i = tid; i < d; i += kT) vv += (double)sval[(size_t)ts * d + i] * sval[(size_t)ts * d + i];
         const double nv1 = sqrt(bsum(vv, shd));
         const float tnorm = snorm[ts];
+        const bool act = 4 * lane < d;
+        const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 kt4 = act ? reinterpret_cast<const float4*>(skey + (size_t)ts * d)[lane] : z4;
+        const float4 vt4 = act ? reinterpret_cast<const float4*>(sval + (size_t)ts * d)[lane] : z4;
         for (int c = warp; c < S; c += kWarps) {
             if (!salive[c] || c == ts) continue;
-            double kd = 0.0, vd = 0.0, v2 = 0.0;
-            for (int i = lane; i < d; i += 32) {
-                kd += (double)skey[(size_t)ts * d + i] * skey[(size_t)c * d + i];
-                vd += (double)sval[(size_t)ts * d + i] * sval[(size_t)c * d + i];
-                v2 += (double)sval[(size_t)c * d + i] * sval[(size_t)c * d + i];
+            const float4 kc = act ? reinterpret_cast<const float4*>(skey + (size_t)c * d)[lane] : z4;
+            const float4 vc = act ? reinterpret_cast<const float4*>(sval + (size_t)c * d)[lane] : z4;
+            double p0 = (double)kt4.x * kc.x + (double)kt4.y * kc.y + (double)kt4.z * kc.z + (double)kt4.w * kc.w;
+            double p1 = (double)vt4.x * vc.x + (double)vt4.y * vc.y + (double)vt4.z * vc.z + (double)vt4.w * vc.w;
+            double p2 = (double)vc.x * vc.x + (double)vc.y * vc.y + (double)vc.z * vc.z + (double)vc.w * vc.w;
+            // transpose-reduce {kd, vd, v2, 0}: xor-16 and xor-8 halve the values a lane carries
+            // (lanes 0-7 end with kd, 8-15 vd, 16-23 v2), xor-4/2/1 finish each sum
+            {
+                const bool h16 = lane & 16, h8 = lane & 8;
+                const double k0 = h16 ? p2 : p0, k1 = h16 ? 0.0 : p1;
+                const double s0 = h16 ? p0 : p2, s1 = h16 ? p1 : 0.0;
+                const double b0 = k0 + __shfl_xor_sync(0xffffffffu, s0, 16);
+                const double b1 = k1 + __shfl_xor_sync(0xffffffffu, s1, 16);
+                double cacc = (h8 ? b1 : b0) + __shfl_xor_sync(0xffffffffu, h8 ? b0 : b1, 8);
+                cacc += __shfl_xor_sync(0xffffffffu, cacc, 4);
+                cacc += __shfl_xor_sync(0xffffffffu, cacc, 2);
+                cacc += __shfl_xor_sync(0xffffffffu, cacc, 1);
+                p0 = __shfl_sync(0xffffffffu, cacc, 0);
+                p1 = __shfl_sync(0xffffffffu, cacc, 8);
+                p2 = __shfl_sync(0xffffffffu, cacc, 16);
             }
-            kd = warp_sum(kd);
-            vd = warp_sum(vd);
-            v2 = warp_sum(v2);
+            const double kd = p0, vd = p1, v2 = p2;
             if (lane == 0) {
                 double r = 0.0;
                 if (tnorm > 0.f && snorm[c] > 0.f) {
