@@ -450,16 +450,49 @@ __global__ void __launch_bounds__(kTh, kMinB) decode_step_kernel(DecArgs a) {
         if (x.idx < 0) return false;
         return x.key > y.key || (x.key == y.key && x.tie < y.tie);  // first max (engine.cpp:188-191)
     };
-    for (int h = 0; h < G; ++h) {
-        const float* ph = prob + (size_t)h * a.R;
-        Cand c{-1.0, 0, -1};
-        for (int r = R0 + tid; r < R1; r += kT)
-            if (c.idx < 0 || (double)ph[r] > c.key) c = Cand{(double)ph[r], r, r};
-        c = bselect(c, better, shc);
-        if constexpr (kClu > 1) {
-            if (tid == 0) s_cand[h] = c;
-        } else if (tid == 0) {
-            a.argmax_pos[(size_t)u * G + h] = c.idx >= 0 ? rpos[c.idx] : -1;
+    // 7. argmax per head (first max) and 8a. the GQA-mean probability per row, one pass over
+    //    the rows for all heads; per-head candidates reduced by warp shuffles, then across warps
+    //    in warp order by warp 0
+    {
+        float ck[kG];
+        int ci[kG];
+#pragma unroll
+        for (int h = 0; h < kG; ++h) ck[h] = -1.f, ci[h] = -1;
+        for (int r = R0 + tid; r < R1; r += kT) {
+            double sum = 0.0;
+#pragma unroll
+            for (int h = 0; h < kG; ++h)
+                if (h < G) {
+                    const float p = prob[(size_t)h * a.R + r];
+                    sum += (double)p;
+                    if (ci[h] < 0 || p > ck[h]) ck[h] = p, ci[h] = r;
+                }
+            pm[r] = (float)(sum / G);
+        }
+#pragma unroll
+        for (int h = 0; h < kG; ++h)
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const float ok = __shfl_xor_sync(0xffffffffu, ck[h], o);
+                const int oi = __shfl_xor_sync(0xffffffffu, ci[h], o);
+                if (oi >= 0 && (ci[h] < 0 || ok > ck[h] || (ok == ck[h] && oi < ci[h]))) ck[h] = ok, ci[h] = oi;
+            }
+        __shared__ float s_ak[kWarpsMax][8];
+        __shared__ int s_ai[kWarpsMax][8];
+        if (lane == 0)
+#pragma unroll
+            for (int h = 0; h < kG; ++h) s_ak[warp][h] = ck[h], s_ai[warp][h] = ci[h];
+        __syncthreads();
+        if (warp == 0 && lane < G) {
+            float bk = -1.f;
+            int bi = -1;
+            for (int w2 = 0; w2 < kWarps; ++w2) {
+                const float ok = s_ak[w2][lane];
+                const int oi = s_ai[w2][lane];
+                if (oi >= 0 && (bi < 0 || ok > bk || (ok == bk && oi < bi))) bk = ok, bi = oi;
+            }
+            if constexpr (kClu > 1) s_cand[lane] = Cand{(double)bk, bi, bi};
+            else a.argmax_pos[(size_t)u * G + lane] = bi >= 0 ? rpos[bi] : -1;
         }
     }
     if constexpr (kClu > 1) {  // candidates of the CTAs (global row indices: a total order)
@@ -473,12 +506,6 @@ __global__ void __launch_bounds__(kTh, kMinB) decode_step_kernel(DecArgs a) {
             }
             a.argmax_pos[(size_t)u * G + tid] = c.idx >= 0 ? rpos[c.idx] : -1;
         }
-    }
-    // 8. attention mass flows back to the owners (engine.cpp:184-195), GQA mean
-    for (int r = R0 + tid; r < R1; r += kT) {
-        double s = 0.0;
-        for (int h = 0; h < G; ++h) s += (double)prob[(size_t)h * a.R + r];
-        pm[r] = (float)(s / G);
     }
     for (int i = tid; i < S + W; i += kT) acc[i] = 0.0;
     __syncthreads();
