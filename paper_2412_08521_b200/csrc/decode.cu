@@ -333,54 +333,80 @@ __global__ void __launch_bounds__(kTh, kMinB) decode_step_kernel(DecArgs a) {
         if ((lane & (2 * off - 1)) == 0 && h < G) prob[(size_t)h * a.R + r] = part[0] * scale;
     }
     __syncthreads();
-    // 5. softmax per query head (softmax_in_place: max-subtracted exp, fp64 normaliser)
-    if constexpr (kClu > 1) {  // cluster-wide max, then the normaliser summed in rank order
-        for (int h = 0; h < G; ++h) {
-            const float* ph = prob + (size_t)h * a.R;
-            float m = -FLT_MAX;
-            for (int r = R0 + tid; r < R1; r += kT) m = fmaxf(m, ph[r]);
-            m = bmax(m, shf);
-            if (tid == 0) s_max[h] = m;
-        }
-        cl_sync();
+    // 5. softmax per query head (softmax_in_place: max-subtracted exp, fp64 normaliser), all
+    //    heads per pass over this CTA's rows: per-head maxima, then fp64 normalisers (warp
+    //    shuffles, warp partials combined in warp order; across a cluster in rank order)
+    {
+        __shared__ float s_wm[kWarpsMax][8];
+        __shared__ double s_wz[kWarpsMax][8];
         float mh[kG];
 #pragma unroll
-        for (int h = 0; h < kG; ++h) {
-            mh[h] = -FLT_MAX;
-            if (h < G)
-                for (int q = 0; q < kClu; ++q) mh[h] = fmaxf(mh[h], ld_dsm_f32(&s_max[h], q));
-        }
+        for (int h = 0; h < kG; ++h) mh[h] = -FLT_MAX;
+        for (int r = R0 + tid; r < R1; r += kT)
+#pragma unroll
+            for (int h = 0; h < kG; ++h)
+                if (h < G) mh[h] = fmaxf(mh[h], prob[(size_t)h * a.R + r]);
 #pragma unroll
         for (int h = 0; h < kG; ++h) {
-            if (h >= G) break;
-            const float* ph = prob + (size_t)h * a.R;
-            double z = 0.0;
-            for (int r = R0 + tid; r < R1; r += kT) z += (double)expf(ph[r] - mh[h]);
-            z = bsum(z, shd);
-            if (tid == 0) s_z[h] = z;
-        }
-        cl_sync();
-#pragma unroll
-        for (int h = 0; h < kG; ++h) {
-            if (h >= G) break;
-            double z = 0.0;
-            for (int q = 0; q < kClu; ++q) z += ld_dsm_f64(&s_z[h], q);
-            float* ph = prob + (size_t)h * a.R;
-            for (int r = R0 + tid; r < R1; r += kT) ph[r] = (float)((double)expf(ph[r] - mh[h]) / z);
+            mh[h] = warp_max(mh[h]);
+            if (lane == 0) s_wm[warp][h] = mh[h];
         }
         __syncthreads();
-    } else {
-        for (int h = 0; h < G; ++h) {
-            float* ph = prob + (size_t)h * a.R;
+#pragma unroll
+        for (int h = 0; h < kG; ++h) {
             float m = -FLT_MAX;
-            for (int r = tid; r < n_rows; r += kT) m = fmaxf(m, ph[r]);
-            m = bmax(m, shf);
-            double z = 0.0;
-            for (int r = tid; r < n_rows; r += kT) z += (double)expf(ph[r] - m);
-            z = bsum(z, shd);
-            for (int r = tid; r < n_rows; r += kT) ph[r] = (float)((double)expf(ph[r] - m) / z);
-            __syncthreads();
+            for (int w2 = 0; w2 < kWarps; ++w2) m = fmaxf(m, s_wm[w2][h]);
+            mh[h] = m;
         }
+        if constexpr (kClu > 1) {  // cluster-wide max
+            if (tid < G) s_max[tid] = mh[tid];
+            cl_sync();
+#pragma unroll
+            for (int h = 0; h < kG; ++h) {
+                float m = -FLT_MAX;
+                if (h < G)
+                    for (int q = 0; q < kClu; ++q) m = fmaxf(m, ld_dsm_f32(&s_max[h], q));
+                mh[h] = m;
+            }
+        }
+        double zh[kG];
+#pragma unroll
+        for (int h = 0; h < kG; ++h) zh[h] = 0.0;
+        for (int r = R0 + tid; r < R1; r += kT)
+#pragma unroll
+            for (int h = 0; h < kG; ++h)
+                if (h < G) zh[h] += (double)expf(prob[(size_t)h * a.R + r] - mh[h]);
+#pragma unroll
+        for (int h = 0; h < kG; ++h) {
+            zh[h] = warp_sum(zh[h]);
+            if (lane == 0) s_wz[warp][h] = zh[h];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int h = 0; h < kG; ++h) {
+            double z = 0.0;
+            for (int w2 = 0; w2 < kWarps; ++w2) z += s_wz[w2][h];
+            zh[h] = z;
+        }
+        if constexpr (kClu > 1) {  // normalisers summed in rank order
+            if (tid < G) s_z[tid] = zh[tid];
+            cl_sync();
+#pragma unroll
+            for (int h = 0; h < kG; ++h) {
+                double z = 0.0;
+                if (h < G)
+                    for (int q = 0; q < kClu; ++q) z += ld_dsm_f64(&s_z[h], q);
+                zh[h] = z;
+            }
+        }
+        for (int r = R0 + tid; r < R1; r += kT)
+#pragma unroll
+            for (int h = 0; h < kG; ++h)
+                if (h < G) {
+                    float* ph = prob + (size_t)h * a.R;
+                    ph[r] = (float)((double)expf(ph[r] - mh[h]) / zh[h]);
+                }
+        __syncthreads();
     }
     // 6. outputs (weighted_value_sum): warp w sums a contiguous block of rows (in order) for all
     //    G heads at once in fp32 (each value row is read once), lanes over d; the warp partials
