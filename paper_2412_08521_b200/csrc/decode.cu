@@ -281,56 +281,77 @@ __global__ void __launch_bounds__(kTh, kMinB) decode_step_kernel(DecArgs a) {
     //    (<= 8) per-lane partial dot products are reduced together in 9 shuffles (each step
     //    halves the values a lane carries), leaving head h's sum in lanes 4h' .. (fixed order).
     const float scale = rsqrtf((float)d);
-    for (int r = R0 + warp; r < R1; r += kWarps) {
-        const int o = rown[r];
-        const bool center = o < S;
-        const float* kb = center ? skey + (size_t)o * d : lkey + (size_t)(o - S) * d;
-        const float kn = center ? snorm[o] : 1.f;
-        const int rp = center && !a.with_pos ? spos[o] : rpos[r];
-        float part[kG];
+    //    Few units (512-thread CTAs): two rows per warp pass, both rows' owners, norms, keys and
+    //    RoPE factors loaded before either is used (the pass is latency-bound on L2); many
+    //    units per SM (256 x 3) already overlap their loads and have no registers to spare.
+    constexpr int kLR = kMinB > 1 ? 1 : 2;
+    for (int r00 = R0 + warp; r00 < R1; r00 += kLR * kWarps) {
+        int oo[kLR], rr[kLR];
 #pragma unroll
-        for (int h = 0; h < kG; ++h) part[h] = 0.f;
-        // d <= 128: at most two pairs per lane, both loaded before use (memory-level parallelism)
-        float2 kk[2], cs[2];
+        for (int t2 = 0; t2 < kLR; ++t2) {
+            rr[t2] = r00 + t2 * kWarps;
+            oo[t2] = rr[t2] < R1 ? rown[rr[t2]] : -1;
+        }
+        // d <= 128: at most two pairs per lane, all loaded before use (memory-level parallelism)
+        float2 kk[kLR][2], cs[kLR][2];
+        float kns[kLR];
 #pragma unroll
-        for (int t = 0; t < 2; ++t) {
-            const int p = lane + 32 * t;
-            if (p < pairs) {
-                kk[t] = reinterpret_cast<const float2*>(kb)[p];
-                cs[t] = a.table[(size_t)rp * pairs + p];
+        for (int t2 = 0; t2 < kLR; ++t2) {
+            const int o = oo[t2], r = rr[t2];
+            if (o < 0) continue;
+            const bool center = o < S;
+            const float* kb = center ? skey + (size_t)o * d : lkey + (size_t)(o - S) * d;
+            kns[t2] = center ? snorm[o] : 1.f;
+            const int rp = center && !a.with_pos ? spos[o] : rpos[r];
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+                const int p = lane + 32 * t;
+                if (p < pairs) {
+                    kk[t2][t] = reinterpret_cast<const float2*>(kb)[p];
+                    cs[t2][t] = a.table[(size_t)rp * pairs + p];
+                }
             }
         }
 #pragma unroll
-        for (int t = 0; t < 2; ++t) {
-            const int p = lane + 32 * t;
-            if (p < pairs) {
-                const float k0 = kk[t].x * kn, k1 = kk[t].y * kn;
-                const float r0 = k0 * cs[t].x - k1 * cs[t].y, r1 = k0 * cs[t].y + k1 * cs[t].x;
+        for (int t2 = 0; t2 < kLR; ++t2) {
+            const int r = rr[t2];
+            if (oo[t2] < 0) continue;
+            const float kn = kns[t2];
+            float part[kG];
 #pragma unroll
-                for (int h = 0; h < kG; ++h)
-                    if (h < G) {
-                        const float2 qq = reinterpret_cast<const float2*>(qrot + h * d)[p];
-                        part[h] += qq.x * r0 + qq.y * r1;
-                    }
+            for (int h = 0; h < kG; ++h) part[h] = 0.f;
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+                const int p = lane + 32 * t;
+                if (p < pairs) {
+                    const float k0 = kk[t2][t].x * kn, k1 = kk[t2][t].y * kn;
+                    const float r0 = k0 * cs[t2][t].x - k1 * cs[t2][t].y, r1 = k0 * cs[t2][t].y + k1 * cs[t2][t].x;
+#pragma unroll
+                    for (int h = 0; h < kG; ++h)
+                        if (h < G) {
+                            const float2 qq = reinterpret_cast<const float2*>(qrot + h * d)[p];
+                            part[h] += qq.x * r0 + qq.y * r1;
+                        }
+                }
             }
-        }
-        // transpose-reduce: each xor-16, 8, ... step halves the values a lane carries (the lane
-        // with the offset bit set keeps the upper half), so after log2(kG) steps lane L holds
-        // head = its offset bits read from the top; the remaining xor steps finish that sum
-        int h = 0, off = 16;
+            // transpose-reduce: each xor-16, 8, ... step halves the values a lane carries (the lane
+            // with the offset bit set keeps the upper half), so after log2(kG) steps lane L holds
+            // head = its offset bits read from the top; the remaining xor steps finish that sum
+            int h = 0, off = 16;
 #pragma unroll
-        for (int n = kG; n > 1; n >>= 1, off >>= 1) {
-            const bool hi = lane & off;
+            for (int n = kG; n > 1; n >>= 1, off >>= 1) {
+                const bool hi = lane & off;
 #pragma unroll
-            for (int i = 0; i < n / 2; ++i) {
-                const float send = hi ? part[i] : part[i + n / 2];
-                const float keep = hi ? part[i + n / 2] : part[i];
-                part[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+                for (int i = 0; i < n / 2; ++i) {
+                    const float send = hi ? part[i] : part[i + n / 2];
+                    const float keep = hi ? part[i + n / 2] : part[i];
+                    part[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+                }
+                h = 2 * h + (hi ? 1 : 0);
             }
-            h = 2 * h + (hi ? 1 : 0);
+            for (int o2 = off; o2 > 0; o2 >>= 1) part[0] += __shfl_xor_sync(0xffffffffu, part[0], o2);
+            if ((lane & (2 * off - 1)) == 0 && h < G) prob[(size_t)h * a.R + r] = part[0] * scale;
         }
-        for (int o2 = off; o2 > 0; o2 >>= 1) part[0] += __shfl_xor_sync(0xffffffffu, part[0], o2);
-        if ((lane & (2 * off - 1)) == 0 && h < G) prob[(size_t)h * a.R + r] = part[0] * scale;
     }
     __syncthreads();
     // 5. softmax per query head (softmax_in_place: max-subtracted exp, fp64 normaliser), all
@@ -666,7 +687,10 @@ __global__ void __launch_bounds__(kTh, kMinB) decode_step_kernel(DecArgs a) {
         tb = bselect(tb, least, shc);
         const int ts = tb.idx;
         // R(tbm, c) for every other alive center: one warp per center; lane owns elements
-        // [4 lane, 4 lane + 4) (d <= 128, d % 4 == 0), the retiring center stays in registers
+        // [4 lane, 4 lane + 4) (d <= 128, d % 4 == 0), the retiring center stays in registers.
+        // kRU centers per warp pass: their alive flags, norms, keys and values are all loaded
+        // before the first is used (the pass is latency-bound on L2, one CTA per unit)
+        constexpr int kRU = kMinB > 1 ? 1 : 4;
         double vv = 0.0;
         for (int i = tid; i < d; i += kT) vv += (double)sval[(size_t)ts * d + i] * sval[(size_t)ts * d + i];
         const double nv1 = sqrt(bsum(vv, shd));
@@ -675,39 +699,54 @@ __global__ void __launch_bounds__(kTh, kMinB) decode_step_kernel(DecArgs a) {
         const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
         const float4 kt4 = act ? reinterpret_cast<const float4*>(skey + (size_t)ts * d)[lane] : z4;
         const float4 vt4 = act ? reinterpret_cast<const float4*>(sval + (size_t)ts * d)[lane] : z4;
-        for (int c = warp; c < S; c += kWarps) {
-            if (!salive[c] || c == ts) continue;
-            const float4 kc = act ? reinterpret_cast<const float4*>(skey + (size_t)c * d)[lane] : z4;
-            const float4 vc = act ? reinterpret_cast<const float4*>(sval + (size_t)c * d)[lane] : z4;
-            double p0 = (double)kt4.x * kc.x + (double)kt4.y * kc.y + (double)kt4.z * kc.z + (double)kt4.w * kc.w;
-            double p1 = (double)vt4.x * vc.x + (double)vt4.y * vc.y + (double)vt4.z * vc.z + (double)vt4.w * vc.w;
-            double p2 = (double)vc.x * vc.x + (double)vc.y * vc.y + (double)vc.z * vc.z + (double)vc.w * vc.w;
-            // transpose-reduce {kd, vd, v2, 0}: xor-16 and xor-8 halve the values a lane carries
-            // (lanes 0-7 end with kd, 8-15 vd, 16-23 v2), xor-4/2/1 finish each sum
-            {
-                const bool h16 = lane & 16, h8 = lane & 8;
-                const double k0 = h16 ? p2 : p0, k1 = h16 ? 0.0 : p1;
-                const double s0 = h16 ? p0 : p2, s1 = h16 ? p1 : 0.0;
-                const double b0 = k0 + __shfl_xor_sync(0xffffffffu, s0, 16);
-                const double b1 = k1 + __shfl_xor_sync(0xffffffffu, s1, 16);
-                double cacc = (h8 ? b1 : b0) + __shfl_xor_sync(0xffffffffu, h8 ? b0 : b1, 8);
-                cacc += __shfl_xor_sync(0xffffffffu, cacc, 4);
-                cacc += __shfl_xor_sync(0xffffffffu, cacc, 2);
-                cacc += __shfl_xor_sync(0xffffffffu, cacc, 1);
-                p0 = __shfl_sync(0xffffffffu, cacc, 0);
-                p1 = __shfl_sync(0xffffffffu, cacc, 8);
-                p2 = __shfl_sync(0xffffffffu, cacc, 16);
+        for (int c0 = warp; c0 < S; c0 += kRU * kWarps) {
+            float4 kcs[kRU], vcs[kRU];
+            int alv[kRU];
+            float cns[kRU];
+#pragma unroll
+            for (int t = 0; t < kRU; ++t) {
+                const int c = c0 + t * kWarps;
+                const bool in = c < S;
+                alv[t] = in ? salive[c] : 0;
+                cns[t] = in ? snorm[c] : 0.f;
+                kcs[t] = in && act ? reinterpret_cast<const float4*>(skey + (size_t)c * d)[lane] : z4;
+                vcs[t] = in && act ? reinterpret_cast<const float4*>(sval + (size_t)c * d)[lane] : z4;
             }
-            const double kd = p0, vd = p1, v2 = p2;
-            if (lane == 0) {
-                double r = 0.0;
-                if (tnorm > 0.f && snorm[c] > 0.f) {
-                    const double ck = fmin(fmax(kd, -1.0), 1.0);
-                    const double nv2 = sqrt(v2);
-                    const double cv = (nv1 > 0.0 && nv2 > 0.0) ? fmin(fmax(vd / (nv1 * nv2), -1.0), 1.0) : 0.0;
-                    r = ck * cv;
+#pragma unroll
+            for (int t = 0; t < kRU; ++t) {
+                const int c = c0 + t * kWarps;
+                if (!alv[t] || c == ts) continue;
+                const float4 kc = kcs[t], vc = vcs[t];
+                double p0 = (double)kt4.x * kc.x + (double)kt4.y * kc.y + (double)kt4.z * kc.z + (double)kt4.w * kc.w;
+                double p1 = (double)vt4.x * vc.x + (double)vt4.y * vc.y + (double)vt4.z * vc.z + (double)vt4.w * vc.w;
+                double p2 = (double)vc.x * vc.x + (double)vc.y * vc.y + (double)vc.z * vc.z + (double)vc.w * vc.w;
+                // transpose-reduce {kd, vd, v2, 0}: xor-16 and xor-8 halve the values a lane carries
+                // (lanes 0-7 end with kd, 8-15 vd, 16-23 v2), xor-4/2/1 finish each sum
+                {
+                    const bool h16 = lane & 16, h8 = lane & 8;
+                    const double k0 = h16 ? p2 : p0, k1 = h16 ? 0.0 : p1;
+                    const double s0 = h16 ? p0 : p2, s1 = h16 ? p1 : 0.0;
+                    const double b0 = k0 + __shfl_xor_sync(0xffffffffu, s0, 16);
+                    const double b1 = k1 + __shfl_xor_sync(0xffffffffu, s1, 16);
+                    double cacc = (h8 ? b1 : b0) + __shfl_xor_sync(0xffffffffu, h8 ? b0 : b1, 8);
+                    cacc += __shfl_xor_sync(0xffffffffu, cacc, 4);
+                    cacc += __shfl_xor_sync(0xffffffffu, cacc, 2);
+                    cacc += __shfl_xor_sync(0xffffffffu, cacc, 1);
+                    p0 = __shfl_sync(0xffffffffu, cacc, 0);
+                    p1 = __shfl_sync(0xffffffffu, cacc, 8);
+                    p2 = __shfl_sync(0xffffffffu, cacc, 16);
                 }
-                acc[c] = r;
+                const double kd = p0, vd = p1, v2 = p2;
+                if (lane == 0) {
+                    double r = 0.0;
+                    if (tnorm > 0.f && cns[t] > 0.f) {
+                        const double ck = fmin(fmax(kd, -1.0), 1.0);
+                        const double nv2 = sqrt(v2);
+                        const double cv = (nv1 > 0.0 && nv2 > 0.0) ? fmin(fmax(vd / (nv1 * nv2), -1.0), 1.0) : 0.0;
+                        r = ck * cv;
+                    }
+                    acc[c] = r;
+                }
             }
         }
         __syncthreads();
