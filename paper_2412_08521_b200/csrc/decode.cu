@@ -557,15 +557,26 @@ __global__ void __launch_bounds__(kTh, kMinB) decode_step_kernel(DecArgs a) {
     for (int i = tid; i < S + W; i += kT) acc[i] = 0.0;
     __syncthreads();
     if (warp == 0) {  // ordered pass: rows in order, equal owners inside a 32-row chunk summed in lane order
-        for (int b = R0; b < R1; b += 32) {
-            const int r = b + lane;
-            const int o = r < R1 ? rown[r] : -1 - lane;
-            const double p = r < R1 ? (G == 1 ? (double)prob[r] : (double)pm[r]) : 0.0;
-            const unsigned grp = __match_any_sync(0xffffffffu, o);
-            double gs = 0.0;
-            for (unsigned m = grp; m; m &= m - 1) gs += __shfl_sync(grp, p, __ffs(m) - 1);
-            if (r < R1 && lane == __ffs(grp) - 1) acc[o] += gs;
-            __syncwarp();
+        constexpr int kOP = 4;  // chunks whose owners and masses are loaded before the first is summed
+        for (int b0 = R0; b0 < R1; b0 += kOP * 32) {
+            int oc[kOP];
+            double pc[kOP];
+#pragma unroll
+            for (int t = 0; t < kOP; ++t) {
+                const int r = b0 + 32 * t + lane;
+                oc[t] = r < R1 ? rown[r] : -1 - lane;
+                pc[t] = r < R1 ? (G == 1 ? (double)prob[r] : (double)pm[r]) : 0.0;
+            }
+#pragma unroll
+            for (int t = 0; t < kOP; ++t) {
+                if (b0 + 32 * t >= R1) break;
+                const int r = b0 + 32 * t + lane, o = oc[t];
+                const unsigned grp = __match_any_sync(0xffffffffu, o);
+                double gs = 0.0;
+                for (unsigned m = grp; m; m &= m - 1) gs += __shfl_sync(grp, pc[t], __ffs(m) - 1);
+                if (r < R1 && lane == __ffs(grp) - 1) acc[o] += gs;
+                __syncwarp();
+            }
         }
     }
     __syncthreads();
