@@ -151,6 +151,16 @@ __device__ __forceinline__ double ld_dsm_f64(const void* p, int rank) {
     asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(dsm_addr(p, rank)) : "memory");
     return v;
 }
+// remote stores into another CTA's shared memory (visible to it after the next cl_sync)
+__device__ __forceinline__ void st_dsm_i32(void* p, int rank, int v) {
+    asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(dsm_addr(p, rank)), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_dsm_i64(void* p, int rank, long long v) {
+    asm volatile("st.shared::cluster.s64 [%0], %1;" ::"r"(dsm_addr(p, rank)), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_dsm_f64(void* p, int rank, double v) {
+    asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(dsm_addr(p, rank)), "d"(v) : "memory");
+}
 // all threads of every CTA of the cluster; release/acquire at cluster scope (shared and global)
 __device__ __forceinline__ void cl_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");

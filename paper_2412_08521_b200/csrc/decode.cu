@@ -594,7 +594,6 @@ __global__ void __launch_bounds__(kTh, kMinB) decode_step_kernel(DecArgs a) {
             }
         }
         cl_sync();  // every score update visible, every remote read done
-        if (rank != 0) return;
     } else {
         for (int s = tid; s < S; s += kT)
             if (salive[s]) sscore[3 * s] += acc[s], sscore[3 * s + 2] += acc[s];
@@ -607,24 +606,28 @@ __global__ void __launch_bounds__(kTh, kMinB) decode_step_kernel(DecArgs a) {
     // 9. score window rotation every l_win steps (engine.cpp:196-200)
     int wfill = s_meta[3] + 1;
     if (wfill >= a.l_win) {
-        for (int s = tid; s < S; s += kT)
-            if (salive[s]) sscore[3 * s + 1] = sscore[3 * s + 2], sscore[3 * s + 2] = 0.0;
-        for (int li = tid; li < count; li += kT) {
-            const int ring = (head + li) % W;
-            lscore[3 * ring + 1] = lscore[3 * ring + 2];
-            lscore[3 * ring + 2] = 0.0;
+        if (rank == 0) {
+            for (int s = tid; s < S; s += kT)
+                if (salive[s]) sscore[3 * s + 1] = sscore[3 * s + 2], sscore[3 * s + 2] = 0.0;
+            for (int li = tid; li < count; li += kT) {
+                const int ring = (head + li) % W;
+                lscore[3 * ring + 1] = lscore[3 * ring + 2];
+                lscore[3 * ring + 2] = 0.0;
+            }
         }
         wfill = 0;
     }
     __syncthreads();
     // 10. policy_decode_compress (policies.cpp:182-242): EMS decode_update (compressor.cpp:376-398);
-    //     SnapKV / H2O / StreamingLLM graduate_locals (policies.cpp:88-98) then drop; full: identity
+    //     SnapKV / H2O / StreamingLLM graduate_locals (policies.cpp:88-98) then drop; full: identity.
+    //     With a cluster, rank 0 alone writes the cache; every rank takes part in the retire
+    //     step's redundancy pass (its slice of the centers, candidates gathered in rank order).
     int n_alive = s_meta[5], compressed = s_meta[4];
     const bool ems = a.policy == EMS_POLICY_EMS;
     while (a.policy != EMS_POLICY_FULL && count > a.l_win) {
         const int g = head;  // graduating local (front of the window)
         // 10a. oldest zero-mapped (else oldest) LUT entry leaves at capacity (:272-284)
-        if (ems && lut_n >= a.lut_cap) {
+        if (rank == 0 && ems && lut_n >= a.lut_cap) {
             Cand c{0.0, 0, -1};
             for (int e = tid; e < lut_n; e += kT)
                 if (tslot[e] < 0 && (c.idx < 0 || e < c.idx)) c = Cand{0.0, e, e};
@@ -644,27 +647,29 @@ __global__ void __launch_bounds__(kTh, kMinB) decode_step_kernel(DecArgs a) {
             --lut_n;
         }
         // 10b. insert_center: lowest free slot (cache.cpp:48-57)
-        Cand fs{0.0, 0, -1};
-        for (int s = tid; s < S; s += kT)
-            if (!salive[s] && (fs.idx < 0 || s < fs.idx)) fs = Cand{0.0, s, s};
-        auto lower = [](const Cand& x, const Cand& y) { return x.idx >= 0 && (y.idx < 0 || x.idx < y.idx); };
-        fs = bselect(fs, lower, shc);
-        const int slot = fs.idx;
-        double kk = 0.0;
-        for (int i = tid; i < d; i += kT) kk += (double)lkey[(size_t)g * d + i] * lkey[(size_t)g * d + i];
-        const double kn = sqrt(bsum(kk, shd));  // normalized_or_zero, :16-25
-        for (int i = tid; i < d; i += kT) {
-            const float x = lkey[(size_t)g * d + i];
-            skey[(size_t)slot * d + i] = kn > 0.0 ? (float)((double)x / kn) : x;
-            sval[(size_t)slot * d + i] = lval[(size_t)g * d + i];
-        }
-        if (tid == 0) {
-            snorm[slot] = (float)kn;
-            spos[slot] = lpos[g];
-            for (int t = 0; t < 3; ++t) sscore[3 * slot + t] = lscore[3 * g + t];
-            salive[slot] = 1;
-            tpos[lut_n] = lpos[g];
-            tslot[lut_n] = slot;
+        if (rank == 0) {
+            Cand fs{0.0, 0, -1};
+            for (int s = tid; s < S; s += kT)
+                if (!salive[s] && (fs.idx < 0 || s < fs.idx)) fs = Cand{0.0, s, s};
+            auto lower = [](const Cand& x, const Cand& y) { return x.idx >= 0 && (y.idx < 0 || x.idx < y.idx); };
+            fs = bselect(fs, lower, shc);
+            const int slot = fs.idx;
+            double kk = 0.0;
+            for (int i = tid; i < d; i += kT) kk += (double)lkey[(size_t)g * d + i] * lkey[(size_t)g * d + i];
+            const double kn = sqrt(bsum(kk, shd));  // normalized_or_zero, :16-25
+            for (int i = tid; i < d; i += kT) {
+                const float x = lkey[(size_t)g * d + i];
+                skey[(size_t)slot * d + i] = kn > 0.0 ? (float)((double)x / kn) : x;
+                sval[(size_t)slot * d + i] = lval[(size_t)g * d + i];
+            }
+            if (tid == 0) {
+                snorm[slot] = (float)kn;
+                spos[slot] = lpos[g];
+                for (int t = 0; t < 3; ++t) sscore[3 * slot + t] = lscore[3 * g + t];
+                salive[slot] = 1;
+                tpos[lut_n] = lpos[g];
+                tslot[lut_n] = slot;
+            }
         }
         ++lut_n;
         ++n_alive;
@@ -672,6 +677,7 @@ __global__ void __launch_bounds__(kTh, kMinB) decode_step_kernel(DecArgs a) {
         --count;
         __syncthreads();
         if (!ems || n_alive <= a.cap_c) continue;
+        if constexpr (kClu > 1) cl_sync();  // rank 0's insert and window rotation visible to every rank
         // 10c. retire_least_important_center (:286-372)
         double sg = 0.0, sl = 0.0;
         for (int s = tid; s < S; s += kT)
@@ -710,14 +716,15 @@ __global__ void __launch_bounds__(kTh, kMinB) decode_step_kernel(DecArgs a) {
         const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
         const float4 kt4 = act ? reinterpret_cast<const float4*>(skey + (size_t)ts * d)[lane] : z4;
         const float4 vt4 = act ? reinterpret_cast<const float4*>(sval + (size_t)ts * d)[lane] : z4;
-        for (int c0 = warp; c0 < S; c0 += kRU * kWarps) {
+        const int c_lo = (int)((long long)rank * S / kClu), c_hi = (int)((long long)(rank + 1) * S / kClu);
+        for (int c0 = c_lo + warp; c0 < c_hi; c0 += kRU * kWarps) {
             float4 kcs[kRU], vcs[kRU];
             int alv[kRU];
             float cns[kRU];
 #pragma unroll
             for (int t = 0; t < kRU; ++t) {
                 const int c = c0 + t * kWarps;
-                const bool in = c < S;
+                const bool in = c < c_hi;
                 alv[t] = in ? salive[c] : 0;
                 cns[t] = in ? snorm[c] : 0.f;
                 kcs[t] = in && act ? reinterpret_cast<const float4*>(skey + (size_t)c * d)[lane] : z4;
@@ -762,7 +769,7 @@ __global__ void __launch_bounds__(kTh, kMinB) decode_step_kernel(DecArgs a) {
         }
         __syncthreads();
         Cand bs{0.0, 0, -1};
-        for (int c = tid; c < S; c += kT)
+        for (int c = c_lo + tid; c < c_hi; c += kT)
             if (salive[c] && c != ts) {
                 const Cand x{acc[c], spos[c], c};
                 if (bs.idx < 0 || x.key > bs.key || (x.key == bs.key && x.tie < bs.tie)) bs = x;
@@ -773,8 +780,23 @@ __global__ void __launch_bounds__(kTh, kMinB) decode_step_kernel(DecArgs a) {
             return x.key > y.key || (x.key == y.key && x.tie < y.tie);
         };
         bs = bselect(bs, most, shc);
+        if constexpr (kClu > 1) {  // the ranks' candidates into rank 0, reduced in rank order
+            __shared__ Cand s_rc[kClu];
+            if (tid == 0) {
+                st_dsm_f64(&s_rc[rank].key, 0, bs.key);
+                st_dsm_i64(&s_rc[rank].tie, 0, bs.tie);
+                st_dsm_i32(&s_rc[rank].idx, 0, bs.idx);
+            }
+            cl_sync();
+            if (rank == 0) {
+                bs = Cand{0.0, 0, -1};
+                for (int q = 0; q < kClu; ++q)
+                    if (most(s_rc[q], bs)) bs = s_rc[q];
+            }
+        }
         const int best = bs.idx;
-        if (best >= 0 && bs.key >= a.tau) {  // merge into the most redundant center
+        // only rank 0 writes the cache
+        if (rank == 0 && best >= 0 && bs.key >= a.tau) {  // merge into the most redundant center
             if (tid == 0) {
                 double wd = combined(sscore + 3 * best, align), wt = combined(sscore + 3 * ts, align);
                 double ws = wd + wt;
@@ -800,10 +822,10 @@ __global__ void __launch_bounds__(kTh, kMinB) decode_step_kernel(DecArgs a) {
                 for (int t = 0; t < 3; ++t) sscore[3 * best + t] += sscore[3 * ts + t];
             for (int e = tid; e < lut_n; e += kT)
                 if (tslot[e] == ts) tslot[e] = best;
-        } else if (a.zero_class) {
+        } else if (rank == 0 && a.zero_class) {
             for (int e = tid; e < lut_n; e += kT)
                 if (tslot[e] == ts) tslot[e] = -1;
-        } else {  // explicit removal: stable in-place compaction of the LUT
+        } else if (rank == 0) {  // explicit removal: stable in-place compaction of the LUT
             int base = 0;
             for (int c0 = 0; c0 < lut_n; c0 += kT) {
                 const int e = c0 + tid;
@@ -819,11 +841,12 @@ __global__ void __launch_bounds__(kTh, kMinB) decode_step_kernel(DecArgs a) {
             lut_n = base;
         }
         __syncthreads();
-        if (tid == 0) salive[ts] = 0;
+        if (tid == 0 && rank == 0) salive[ts] = 0;
         --n_alive;
         compressed = 1;
         __syncthreads();
     }
+    if (rank != 0) return;
     // 10d. H2O: drop the lowest-glo centers beyond capacity (ties -> lower position);
     //      StreamingLLM: drop the oldest non-sink center while over budget (policies.cpp:200-241)
     while ((a.policy == EMS_POLICY_H2O && n_alive > a.cap_c) ||
