@@ -79,17 +79,6 @@ __device__ double bsum(double v, double* sh) {
     __syncthreads();
     return t;
 }
-__device__ float bmax(float v, float* sh) {
-    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-    v = warp_max(v);
-    __syncthreads();
-    if (l == 0) sh[w] = v;
-    __syncthreads();
-    float t = -FLT_MAX;
-    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t = fmaxf(t, sh[i]);
-    __syncthreads();
-    return t;
-}
 // (key, tie, idx) lexicographic "better" selection; better(a, b) decides.  Keys/ties are
 // a total order on the candidates, so the result does not depend on reduction order.
 struct Cand {
@@ -150,7 +139,8 @@ __device__ __forceinline__ double combined(const double* sc, double align) {
 // kClu > 1: a unit's expanded rows are split over a cluster of kClu CTAs (row list, logits,
 // softmax, value sums, argmax and the mass flow), with the cross-CTA maxima, normalisers,
 // partial sums and per-owner masses exchanged through distributed shared memory in rank
-// order; rank 0 then runs the sequential cache update alone.
+// order; rank 0 then writes the cache alone, every rank scoring its slice of the centers in
+// the retire step's redundancy pass.
 template <int kG, int kTh, int kMinB, int kClu>
 __global__ void __launch_bounds__(kTh, kMinB) decode_step_kernel(DecArgs a) {
     extern __shared__ __align__(16) unsigned char dsm[];
@@ -166,7 +156,6 @@ __global__ void __launch_bounds__(kTh, kMinB) decode_step_kernel(DecArgs a) {
     __shared__ double s_z[8];
     __shared__ Cand s_cand[8];
     __shared__ double shd[kWarpsMax];
-    __shared__ float shf[kWarpsMax];
     __shared__ Cand shc[kWarpsMax];
     __shared__ int shi[kWarpsMax];
     __shared__ int s_meta[8];
