@@ -545,27 +545,56 @@ __global__ void __launch_bounds__(kTh, kMinB) decode_step_kernel(DecArgs a) {
     }
     for (int i = tid; i < S + W; i += kT) acc[i] = 0.0;
     __syncthreads();
-    if (warp == 0) {  // ordered pass: rows in order, equal owners inside a 32-row chunk summed in lane order
-        constexpr int kOP = 4;  // chunks whose owners and masses are loaded before the first is summed
-        for (int b0 = R0; b0 < R1; b0 += kOP * 32) {
-            int oc[kOP];
-            double pc[kOP];
+    // ordered pass: rows in order, equal owners inside a 32-row chunk summed in lane order
+    if constexpr (kClu > 1) {
+        // a few hundred rows per CTA: warp 0 alone, four chunks' owners and masses loaded
+        // before the first is summed (fewer block barriers than the round scheme below)
+        constexpr int kOP = 4;
+        if (warp == 0)
+            for (int b0 = R0; b0 < R1; b0 += kOP * 32) {
+                int oc[kOP];
+                double pc[kOP];
 #pragma unroll
-            for (int t = 0; t < kOP; ++t) {
-                const int r = b0 + 32 * t + lane;
-                oc[t] = r < R1 ? rown[r] : -1 - lane;
-                pc[t] = r < R1 ? (G == 1 ? (double)prob[r] : (double)pm[r]) : 0.0;
-            }
+                for (int t = 0; t < kOP; ++t) {
+                    const int r = b0 + 32 * t + lane;
+                    oc[t] = r < R1 ? rown[r] : -1 - lane;
+                    pc[t] = r < R1 ? (G == 1 ? (double)prob[r] : (double)pm[r]) : 0.0;
+                }
 #pragma unroll
-            for (int t = 0; t < kOP; ++t) {
-                if (b0 + 32 * t >= R1) break;
-                const int r = b0 + 32 * t + lane, o = oc[t];
-                const unsigned grp = __match_any_sync(0xffffffffu, o);
-                double gs = 0.0;
-                for (unsigned m = grp; m; m &= m - 1) gs += __shfl_sync(grp, pc[t], __ffs(m) - 1);
-                if (r < R1 && lane == __ffs(grp) - 1) acc[o] += gs;
-                __syncwarp();
+                for (int t = 0; t < kOP; ++t) {
+                    if (b0 + 32 * t >= R1) break;
+                    const int r = b0 + 32 * t + lane, o = oc[t];
+                    const unsigned grp = __match_any_sync(0xffffffffu, o);
+                    double gs = 0.0;
+                    for (unsigned m = grp; m; m &= m - 1) gs += __shfl_sync(grp, pc[t], __ffs(m) - 1);
+                    if (r < R1 && lane == __ffs(grp) - 1) acc[o] += gs;
+                    __syncwarp();
+                }
             }
+    } else {
+        // all of a unit's rows in one CTA: each round, warp w forms the group sums of chunk
+        // (round, w) (match + lane-order shuffles, every warp in parallel); warp 0 then adds
+        // the round's chunks into acc in chunk order (a chunk's group leaders have distinct
+        // owners, so its lanes add at once) -- the same sums in the same order as above
+        __shared__ int s_go[kWarpsMax][32];
+        __shared__ double s_gs[kWarpsMax][32];
+        for (int b0 = R0; b0 < R1; b0 += kWarps * 32) {
+            const int r = b0 + 32 * warp + lane;
+            const int o = r < R1 ? rown[r] : -1 - lane;
+            const double p = r < R1 ? (G == 1 ? (double)prob[r] : (double)pm[r]) : 0.0;
+            const unsigned grp = __match_any_sync(0xffffffffu, o);
+            double gs = 0.0;
+            for (unsigned m = grp; m; m &= m - 1) gs += __shfl_sync(grp, p, __ffs(m) - 1);
+            s_go[warp][lane] = r < R1 && lane == __ffs(grp) - 1 ? o : -1;
+            s_gs[warp][lane] = gs;
+            __syncthreads();
+            if (warp == 0)
+                for (int w2 = 0; w2 < kWarps && b0 + 32 * w2 < R1; ++w2) {
+                    const int ow = s_go[w2][lane];
+                    if (ow >= 0) acc[ow] += s_gs[w2][lane];
+                    __syncwarp();
+                }
+            __syncthreads();
         }
     }
     __syncthreads();
