@@ -394,6 +394,9 @@ class RefLib:
         L.ems_ref_prefill_unit.argtypes = [_dp, _dp, _dp, _dp, C.c_int64, C.c_int64, C.c_int64,
                                            C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_int64,
                                            C.c_int32, _dp, _dp, C.c_int32]
+        L.ems_ref_prefill_units.argtypes = [_dp, _dp, _dp, _dp, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
+                                            C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_int64,
+                                            C.c_int32, C.c_int32, _dp, _dp, C.c_int32]
         L.ems_ref_engine_prefill.argtypes = [_dp, _dp, _dp, C.c_int64, C.c_int64, C.c_int64,
                                              C.c_int64, C.c_int64, C.c_double, C.c_double,
                                              C.c_int64, C.c_int32, C.c_double, C.c_int64]
@@ -484,6 +487,23 @@ class RefLib:
                   "prefill_unit")
         cache = Cache.from_dump_json(self.lib.ems_ref_last_json().decode()) if dump else None
         return cache, glo, loc
+
+    def prefill_units(self, q_rot, k_rot, k_raw, v, c: Config, with_out=True, dump=True):
+        """U units at once (ems_ref_prefill_units): q_rot [U,G,n,d], k_rot/k_raw/v [U,n,d].
+        Every (unit, query head) score pass in one OpenMP region as engine.cpp:65 does.
+        Returns (caches or None, glo [U,n], loc [U,n])."""
+        q, kr, kw, vv = map(_f64, (q_rot, k_rot, k_raw, v))
+        U, G, n, d = q.shape
+        glo, loc = np.zeros((U, n)), np.zeros((U, n))
+        self._chk(self.lib.ems_ref_prefill_units(_ptr(q), _ptr(kr), _ptr(kw), _ptr(vv), U, G, n, d,
+                                                 c.n_budget, c.l_win, c.tau, c.gamma, c.kernel_size,
+                                                 int(c.zero_class), int(with_out), _ptr(glo), _ptr(loc),
+                                                 int(dump)), "prefill_units")
+        caches = None
+        if dump:
+            texts = self.lib.ems_ref_last_json().decode().split("\x1e")[:U]
+            caches = [Cache.from_dump_json(t) for t in texts]
+        return caches, glo, loc
 
     def engine_prefill_dump(self, q, k, v, c: Config, rope_base=10000.0, head=0) -> str:
         q, k, v = map(_f64, (q, k, v))

@@ -12,6 +12,7 @@
 //   make_engine / prefill  proj/src/engine.cpp:26-82
 //   gen_synthetic          proj/src/trace.cpp:414-429
 // No reference code is copied here; everything is a call into it.
+#include <algorithm>
 #include <cstdint>
 #include <cstring>
 #include <stdexcept>
@@ -252,6 +253,82 @@ int ems_ref_prefill_unit(const double* q_rot, const double* k_rot, const double*
         const ems::HeadCacheState cache = ems::policy_prefill_compress(
             ems::PolicyHandle{ems::PolicyKind::ems}, to_matrix(k_raw, n, d), V, s, cfg);
         if (dump) g_json = ems::cache_dump_json(cache);
+    });
+}
+
+// The same composition over U units at once, the way engine::prefill spreads work
+// (engine.cpp:65: one parallel loop over every head): the U*G (unit, query head) score passes
+// share one OpenMP region; when there are fewer of them than threads, each takes
+// threads / (U*G) threads for streaming_pass's own row loop (scoring.cpp:41, nested).  Then
+// GQA mean, init_score_state and policy_prefill_compress per unit, parallel over units.
+//   q_rot [U][G][n][d], k_rot / k_raw / v [U][n][d]; glo_out / loc_out [U][n] (may be NULL).
+//   with_out = 1: prefill_attention (O computed and discarded, as engine::prefill's result);
+//   0: prefill_scores (same glo/loc, scoring.hpp:48-54).  dump = 1: the caches'
+//   cache_dump_json texts, '\x1e'-terminated in unit order (ems_ref_last_json).
+int ems_ref_prefill_units(const double* q_rot, const double* k_rot, const double* k_raw, const double* v,
+                          int64_t U, int64_t G, int64_t n, int64_t d, int64_t n_budget, int64_t l_win,
+                          double tau, double gamma, int64_t kernel, int32_t zero_class, int32_t with_out,
+                          double* glo_out, double* loc_out, int32_t dump) {
+    return guarded([&] {
+        const auto cfg = make_config(n_budget, l_win, tau, gamma, kernel, zero_class);
+        const std::size_t l_win_eff = std::min<std::size_t>(l_win, n);
+        const int64_t items = U * G;
+        const int T = omp_get_max_threads();
+        const int outer = (int)std::min<int64_t>(items, T);
+        const int inner = std::max(1, T / std::max(outer, 1));
+        const int levels = omp_get_max_active_levels();
+        omp_set_max_active_levels(inner > 1 ? 2 : 1);
+        std::vector<ems::Vector> glo(items), loc(items);
+        std::vector<std::string> errs(items);
+#pragma omp parallel for num_threads(outer) schedule(dynamic, 1)
+        for (int64_t it = 0; it < items; ++it) {
+            omp_set_num_threads(inner);
+            const int64_t u = it / G;
+            try {
+                const auto Q = to_matrix(q_rot + it * n * d, n, d), K = to_matrix(k_rot + u * n * d, n, d);
+                if (with_out) {
+                    ems::PrefillAttention pa =
+                        ems::prefill_attention(Q, K, to_matrix(v + u * n * d, n, d), l_win_eff);
+                    glo[it] = std::move(pa.glo);
+                    loc[it] = std::move(pa.loc);
+                } else {
+                    ems::PrefillScores ps = ems::prefill_scores(Q, K, l_win_eff);
+                    glo[it] = std::move(ps.glo);
+                    loc[it] = std::move(ps.loc);
+                }
+            } catch (const std::exception& e) {
+                errs[it] = e.what();
+            }
+        }
+        omp_set_max_active_levels(levels);
+        for (auto& e : errs)
+            if (!e.empty()) throw std::invalid_argument(e);
+        std::vector<std::string> dumps(U);
+#pragma omp parallel for schedule(dynamic, 1)
+        for (int64_t u = 0; u < U; ++u) {
+            ems::Vector g(n, 0.0), l(n, 0.0);
+            for (int64_t h = 0; h < G; ++h)
+                for (int64_t j = 0; j < n; ++j) g[j] += glo[u * G + h][j], l[j] += loc[u * G + h][j];
+            for (int64_t j = 0; j < n; ++j) g[j] /= double(G), l[j] /= double(G);
+            if (glo_out) std::memcpy(glo_out + u * n, g.data(), sizeof(double) * n);
+            if (loc_out) std::memcpy(loc_out + u * n, l.data(), sizeof(double) * n);
+            try {
+                const ems::ScoreState s = ems::init_score_state(g, l, l_win);
+                const ems::HeadCacheState cache =
+                    ems::policy_prefill_compress(ems::PolicyHandle{ems::PolicyKind::ems},
+                                                 to_matrix(k_raw + u * n * d, n, d),
+                                                 to_matrix(v + u * n * d, n, d), s, cfg);
+                if (dump) dumps[u] = ems::cache_dump_json(cache);
+            } catch (const std::exception& e) {
+                dumps[u] = std::string("\x1f") + e.what();
+            }
+        }
+        g_json.clear();
+        for (auto& s : dumps) {
+            if (!s.empty() && s[0] == '\x1f') throw std::invalid_argument(s.substr(1));
+            g_json += s;
+            g_json += '\x1e';
+        }
     });
 }
 

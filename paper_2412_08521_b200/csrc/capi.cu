@@ -4,6 +4,9 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
+#include <set>
+#include <utility>
 #include <vector>
 
 #include "common.cuh"
@@ -65,6 +68,19 @@ void set_error(const char* fmt, ...) {
     va_start(ap, fmt);
     vsnprintf(g_err, sizeof(g_err), fmt, ap);
     va_end(ap);
+}
+
+cudaError_t smem_optin(const void* kernel, int bytes) {
+    static std::mutex mu;
+    static std::set<std::pair<const void*, int>> done;  // (kernel, device) pairs already opted in
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lock(mu);
+    if (done.count({kernel, dev})) return cudaSuccess;
+    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) done.insert({kernel, dev});
+    return e;
 }
 
 Dims make_dims(const ems_desc& d) {
@@ -196,8 +212,13 @@ int run_score(const ems_desc* desc, const void* q, const void* k, const void* v,
     if (use_tc(*desc)) {
         e = score_tc(m, q, k, v, o, lse_buf, glo, loc, at<void>(ws, l.tc), s);
     } else {
-        if (desc->score_impl == EMS_SCORE_TCGEN05) {
-            set_error("tcgen05 score pass unsupported for this shape/dtype");
+        // The SIMT kernels serve fp32 (no tcgen05 kind keeps the 1e-4 contract) and head_dim
+        // != 128; bf16 at d = 128 always takes the tensor cores (any L up to 2^20) unless the
+        // caller asks for the SIMT twin explicitly -- never a silent ~700x slower path.
+        const bool tc_shape = desc->dtype == EMS_BF16 && desc->head_dim == 128;
+        if (desc->score_impl == EMS_SCORE_TCGEN05 || (tc_shape && desc->score_impl == EMS_SCORE_AUTO)) {
+            set_error("tcgen05 score pass unavailable (needs an sm_100 device and seq_len <= 1048576; "
+                      "got seq_len %d)", desc->seq_len);
             return EMS_UNSUPPORTED;
         }
         e = score_simt(m, desc->dtype, q, k, v, o, lse_buf, glo, loc, s);

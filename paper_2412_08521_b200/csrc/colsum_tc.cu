@@ -6,6 +6,9 @@
 // Reference semantics: streaming_pass column scatter, proj/src/scoring.cpp:52-62;
 // GQA mean per contract D2.
 //
+// Any L: the last query / key tile is TMA zero fill past L; queries >= L are masked in the
+// (always masked-path) last query tile and keys >= L are never stored.
+//
 // One CTA owns TWO 128-key tiles (J0 = 2*jp, J1 = J0 + 1) of one unit, both resident
 // in smem, and streams every (query head h, query tile I >= J0) through a 4-stage
 // TMA ring.  Each streamed Q tile feeds two SS MMAs  S^T_w = K_Jw Q_I^T  (keys on
@@ -17,8 +20,6 @@
 // the FMA pipe (ex2_poly2) and the rest on MUFU.  Per-item fp32 sums are accumulated
 // in fp64 in item order and the two column halves are combined in a fixed order ->
 // deterministic.
-#include <stdlib.h>
-
 #include "score_tc.cuh"
 
 namespace ems {
@@ -42,7 +43,7 @@ struct Bars {
 
 // 64 query columns of the thread's key row, general path (causal mask + window).
 __device__ __forceinline__ void cols_masked(uint32_t sa, uint32_t lb, float c, int q0, int key,
-                                            int loc_start, float& sg, float& sl) {
+                                            int loc_start, int L, float& sg, float& sl) {
     sg = 0.f;
     sl = 0.f;
     uint32_t r[2][32];
@@ -55,7 +56,7 @@ __device__ __forceinline__ void cols_masked(uint32_t sa, uint32_t lb, float c, i
         for (int x = 0; x < 32; ++x) {
             const int n = cc * 32 + x, qi = q0 + n;
             float p = ex2(fmaf(__uint_as_float(r[cc][x]), c, lds32(lb + 4 * n)));
-            if (qi < key) p = 0.f;  // query before key: masked
+            if (qi < key || qi >= L) p = 0.f;  // query before key, or padding row past L: masked
             sg += p;
             if (qi >= loc_start) sl += p;
         }
@@ -65,7 +66,7 @@ __device__ __forceinline__ void cols_masked(uint32_t sa, uint32_t lb, float c, i
 // tensor-core path is d = 128 only); groups of 4 pairs are tree-summed before entering
 // one of 4 independent accumulators, keeping the FADD dependency chains short.
 constexpr float kC128 = 0.12751743f;
-template <int kPoly>
+constexpr int kPoly = 2;  // exp2 pairs (of every 8) computed on the FMA pipe (ex2_poly2)
 __device__ __forceinline__ float cols_fast(uint32_t sa, uint32_t lb) {
     const float2 c2 = make_float2(kC128, kC128);
     uint32_t r[2][32];
@@ -98,7 +99,6 @@ __device__ __forceinline__ float cols_fast(uint32_t sa, uint32_t lb) {
     return s.x + s.y;
 }
 
-template <int kPoly>
 __global__ void __launch_bounds__(kThreads, 1)
     colsum_tc_kernel(const __grid_constant__ CUtensorMap tk, const __grid_constant__ CUtensorMap tq,
                      const ColArgs a) {
@@ -112,19 +112,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     __shared__ Bars bars;
 
     const int tid = threadIdx.x, warp = tid >> 5;
-    int jp, unit, hg;                                  // key-tile pair (heaviest first), unit, head group
-    if (a.unit_major) {                                // unit by unit: the unit's Q stays in L2
-        const int per_unit = ((a.nT + 1) / 2) * a.hsplit;
-        unit = blockIdx.x / per_unit;
-        const int r = blockIdx.x % per_unit;
-        jp = r / a.hsplit;
-        hg = r % a.hsplit;
-    } else {
-        const int per_jp = a.units * a.hsplit;
-        jp = blockIdx.x / per_jp;
-        unit = blockIdx.x % a.units;
-        hg = (blockIdx.x % per_jp) / a.units;
-    }
+    // key-tile pair (heaviest first over all units: unit by unit would leave the last unit's
+    // longest CTAs to the end of the grid), unit, head group
+    const int per_jp = a.units * a.hsplit;
+    const int jp = blockIdx.x / per_jp;
+    const int unit = blockIdx.x % a.units;
+    const int hg = (blockIdx.x % per_jp) / a.units;
+    const size_t Lp = (size_t)a.nT * kTile;
     const int gh = a.G / a.hsplit;                     // query heads of this CTA
     const int b = unit / a.Hkv, hk = unit % a.Hkv;
     const int J0 = 2 * jp;
@@ -175,7 +169,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tma_load_3d(dq + 16384, &tq, &bars.q_full[s], 64, I * kTile, plane);
                 if (i >= kBufs) mbar_wait(&bars.s_empty[bb], ((i / kBufs) - 1) & 1);
                 mbar_expect_tx(&bars.l_full[bb], 512);
-                bulk_load(slse + bb * 128, a.nlse2 + (size_t)plane * a.L + (size_t)I * kTile, 512,
+                bulk_load(slse + bb * 128, a.nlse2 + (size_t)plane * Lp + (size_t)I * kTile, 512,
                           &bars.l_full[bb]);
             }
         }
@@ -195,10 +189,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t d0 = tmem + bb * 256;
 #pragma unroll
                 for (int k = 0; k < 8; ++k)
-                    if (a.debug != 2)
-                        mma_ss(d0, sdesc(kmajor_addr(ka0, k), 16, 1024),
+                    mma_ss(d0, sdesc(kmajor_addr(ka0, k), 16, 1024),
                                sdesc(kmajor_addr(qa, k), 16, 1024), id_s, k > 0);
-                if (has1 && I >= J0 + 1 && a.debug != 2) {  // key tile J1 is fully masked vs query tile J0
+                if (has1 && I >= J0 + 1) {  // key tile J1 is fully masked vs query tile J0
 #pragma unroll
                     for (int k = 0; k < 8; ++k)
                         mma_ss(d0 + 128, sdesc(kmajor_addr(ka1, k), 16, 1024),
@@ -233,14 +226,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait_u(l_full0 + 8 * bb, ph);
             mbar_wait_u(s_full0 + 8 * bb, ph);
             tc_fence_after();
-            if (active && I >= Jw && a.debug != 1) {
+            if (active && I >= Jw) {
                 const uint32_t sa = sa0 + bb * 256;
                 const uint32_t lb = lb0 + bb * 512;
                 if (I > Jw && I <= last_interior) {
-                    acc_g += (double)cols_fast<kPoly>(sa, lb);
+                    acc_g += (double)cols_fast(sa, lb);
                 } else {
                     float sg, sl;
-                    cols_masked(sa, lb, a.c, I * kTile + 64 * hc, key, loc_start, sg, sl);
+                    cols_masked(sa, lb, a.c, I * kTile + 64 * hc, key, loc_start, a.L, sg, sl);
                     acc_g += (double)sg;
                     acc_l += (double)sl;
                 }
@@ -257,7 +250,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             sp[128 + mrow] = acc_l;
         }
         asm volatile("bar.sync %0, 256;" ::"r"(1 + w) : "memory");
-        if (hc == 0 && active) {
+        if (hc == 0 && active && key < a.L) {
             if (a.hsplit == 1) {
                 const size_t o = (size_t)unit * a.L + (size_t)Jw * kTile + mrow;
                 a.glo[o] = (float)((acc_g + sp[mrow]) / a.G);
@@ -272,19 +265,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_before();
     __syncthreads();
     if (warp == 0) tmem_dealloc<512>(tmem);
-}
-
-template <int kPoly>
-cudaError_t launch_t(const ColArgs& a, const CUtensorMap& tk, const CUtensorMap& tq, cudaStream_t s) {
-    static const bool attr = [] {  // once per process, thread-safe (magic static)
-        cudaFuncSetAttribute(colsum_tc_kernel<kPoly>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)kSmem);
-        return true;
-    }();
-    (void)attr;
-    const dim3 grid(((a.nT + 1) / 2) * a.units * a.hsplit);
-    colsum_tc_kernel<kPoly><<<grid, kThreads, kSmem, s>>>(tk, tq, a);
-    return cudaGetLastError();
 }
 
 // glo/loc = (sum over head groups, in order) / G  -- deterministic
@@ -308,18 +288,11 @@ __global__ void colsum_reduce_kernel(const double* __restrict__ pg, const double
 
 cudaError_t launch_colsum_tc(const ColArgs& a, const CUtensorMap& tk, const CUtensorMap& tq,
                              cudaStream_t s) {
-    // pairs (of every 8) whose exp2 runs on the FMA pipe; EMS_P2_POLY overrides (tuning)
-    static const int poly = [] {
-        const char* e = getenv("EMS_P2_POLY");
-        return e ? atoi(e) : 2;
-    }();
-    cudaError_t e;
-    switch (poly) {
-        case 0: e = launch_t<0>(a, tk, tq, s); break;
-        case 2: e = launch_t<2>(a, tk, tq, s); break;
-        case 4: e = launch_t<4>(a, tk, tq, s); break;
-        default: e = launch_t<3>(a, tk, tq, s); break;
-    }
+    cudaError_t e = smem_optin(reinterpret_cast<const void*>(colsum_tc_kernel), (int)kSmem);
+    if (e != cudaSuccess) return e;
+    const dim3 grid(((a.nT + 1) / 2) * a.units * a.hsplit);
+    colsum_tc_kernel<<<grid, kThreads, kSmem, s>>>(tk, tq, a);
+    e = cudaGetLastError();
     if (e != cudaSuccess || a.hsplit == 1) return e;
     colsum_reduce_kernel<<<4 * 148, 256, 0, s>>>(a.part_g, a.part_l, a.glo, a.loc, a.units, a.L, a.hsplit, a.G);
     return cudaGetLastError();
@@ -329,11 +302,6 @@ cudaError_t launch_colsum_tc(const ColArgs& a, const CUtensorMap& tk, const CUte
 // ~4 CTAs per SM (the heaviest key-tile pair otherwise dominates small unit counts).
 int colsum_hsplit(int G, int nT, int units) {
     const int pairs = (nT + 1) / 2;
-    static const int forced = [] {
-        const char* e = getenv("EMS_P2_HSPLIT");  // tuning override (power of two dividing G)
-        return e ? atoi(e) : 0;
-    }();
-    if (forced > 0 && G % forced == 0) return forced;
     int hs = 1;
     while (hs < G && G % (2 * hs) == 0 && (long long)pairs * units * hs < 4LL * 148) hs *= 2;
     return hs;

@@ -104,6 +104,11 @@ Dims make_dims(const ems_desc& d);
 
 void set_error(const char* fmt, ...);
 
+// Dynamic shared memory above 48 KB is a function attribute of the CURRENT DEVICE's context:
+// set it once per (kernel, device), so one process can drive several GPUs (one host thread
+// per device).  Thread-safe; returns the cudaFuncSetAttribute status.
+cudaError_t smem_optin(const void* kernel, int bytes);
+
 #define EMS_CUDA_CHECK(expr)                                                          \
     do {                                                                              \
         cudaError_t _e = (expr);                                                      \

@@ -1055,7 +1055,10 @@ cudaError_t launch_decode_step(const Dims& m, int dtype, int S, int W, int T, in
     EMS_DEC_PICK(1) EMS_DEC_PICK(2) EMS_DEC_PICK(4) EMS_DEC_PICK(8)
 #undef EMS_DEC_PICK
     if (!fn || m.G > 8) return cudaErrorInvalidValue;
-    if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (smem > 48 * 1024) {
+        const cudaError_t e = smem_optin(reinterpret_cast<const void*>(fn), (int)smem);
+        if (e != cudaSuccess) return e;
+    }
     if (!clu) {
         fn<<<m.units, threads, smem, s>>>(a);
         return cudaGetLastError();

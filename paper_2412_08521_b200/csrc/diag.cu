@@ -389,11 +389,8 @@ cudaError_t launch_redundancy(int units, int L, int d, int dtype, const void* k,
     const bool tc = dtype == EMS_BF16 && d == kD && L >= 128 && encode_fn() != nullptr && getenv("EMS_DIAG_SIMT") == nullptr &&
                     make_tmap_bf16_3d(&tk, k, kD, L, units, 128) && make_tmap_bf16_3d(&tv, v, kD, L, units, 128);
     if (tc) {
-        static const bool attr = [] {  // once per process, thread-safe (magic static)
-            cudaFuncSetAttribute(redundancy_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
-            return true;
-        }();
-        (void)attr;
+        const cudaError_t e = smem_optin(reinterpret_cast<const void*>(redundancy_tc_kernel), (int)kSmem);
+        if (e != cudaSuccess) return e;
         redundancy_tc_kernel<<<dim3(Lpad / 128, units), kThreads, kSmem, s>>>(tk, tv, L, Lpad, inv, tau, count);
     } else {
         dim3 g((L + 7) / 8, units);

@@ -1,8 +1,14 @@
 // fwd2_tc.cu -- (P1, CTA-pair variant) causal FlashAttention forward on cta_group::2 with
-// 256-key tiles: O, row LSE.  Reference semantics: streaming_pass, proj/src/scoring.cpp:20-64.
+// 256-key tiles: O, row LSE.  Reference semantics: streaming_pass, proj/src/scoring.cpp:20-64,
+// for any prompt length L (the reference accepts any n) and any GQA group size G.
 //
-// A cluster of two CTAs owns 256 query rows: the same query tile of two heads of a GQA
-// group (G >= 2) or query tiles 2p, 2p+1 of one head (G == 1); CTA r holds its 128 rows.
+// A cluster of two CTAs owns two 128-row (query head, query tile) items of one unit: a unit's
+// G * ceil(L/128) items are walked heaviest tile first, heads inner, and paired consecutively
+// (the same query tile of two heads when G is even; tiles t, t-1 of one head when G == 1).
+// An odd item count gets a dummy partner that recomputes rank 0's item and stores nothing.
+// Rows >= L of the last query tile and keys >= L of the last key tile arrive as TMA zero fill;
+// the causal mask (key > row) removes every key >= L from every real row, and no row >= L is
+// stored.  CTA r holds its item's 128 rows.
 // The leader issues, per 256-key tile j,
 //   S_j  = Q K_j^T        tcgen05.mma.cta_group::2, M = 256, N = 256, K = 128 (SS): each CTA
 //                          supplies its 128 query rows (A) and one 128-key half of K_j (B)
@@ -34,16 +40,17 @@ constexpr float kSkip = 64.0f;
 constexpr int kT2 = 576;  // w0 TMA, w1 MMA (leader), w2-17 softmax (warpgroup q = keys [64q, 64q+64))
 constexpr int kStages2 = 2;
 // Q 32 KB | K stages (this CTA's 128-key half) | V stages (256 keys x this CTA's 64 d cols)
-constexpr int kMaxT2 = 1024;  // 256-key tiles per sequence (L <= 262144) for the smem key bounds
+constexpr int kMaxT2 = 4096;  // 256-key tiles per sequence (L <= 1048576) for the smem key bounds
 constexpr size_t kSmem2 = 1024 + kTileBytes + 2 * kStages2 * kTileBytes + 2 * 4 * 128 * 4 + kMaxT2 * 4;
 
+constexpr int kPoly = 2;  // exp2 pairs (of every 8) computed on the FMA pipe (ex2_poly2)
+
 struct Fwd2Args {
-    int L, Hq, Hkv, G, nT, units;
+    int L, Lp, Hq, Hkv, G, nT, units;  // Lp = nT * 128: row stride of nlse2
     float c;
-    __nv_bfloat16* out;
-    float* nlse2;
-    float* lse_nat;
-    int debug;  // profiling only: 1 = no softmax math (P = 0), 2 = no MMAs
+    __nv_bfloat16* out;  // [planes][L][128] (may be null)
+    float* nlse2;        // [planes][Lp] negated log2-domain LSE (P2's input)
+    float* lse_nat;      // [planes][L] natural-log LSE (may be null)
     const float* kmax;  // [units][nT2] max ||k|| over each 256-key tile (Cauchy-Schwarz bound)
     int nT2;
     const __nv_bfloat16* q;  // [planes][L][128]: |q_row| for the bound, read before the first S
@@ -58,30 +65,23 @@ struct Bars2 {
     uint32_t tmem_base;
 };
 
+// Unit by unit; within a unit item k = (tile nT-1 - k/G, head k%G), pairs (2p, 2p+1).
 __device__ __forceinline__ void pair_item(const Fwd2Args& a, int pair, int rank, int& plane, int& tile,
-                                          int& unit, int& jmax) {
-    if (a.G >= 2) {  // unit by unit, heaviest query tiles first; CTA r takes head 2 hp + r
-        const int hps = a.G / 2;
-        const int per_unit = a.nT * hps;
-        unit = pair / per_unit;
-        const int r = pair % per_unit;
-        tile = a.nT - 1 - r / hps;
-        const int hp = r % hps;
-        const int b = unit / a.Hkv, hk = unit % a.Hkv;
-        plane = b * a.Hq + hk * a.G + 2 * hp + rank;
-    } else {  // query tiles 2p, 2p+1 of one head
-        const int np = a.nT / 2;
-        unit = pair / np;
-        const int p = np - 1 - pair % np;
-        const int b = unit / a.Hkv, hk = unit % a.Hkv;
-        plane = b * a.Hq + hk;
-        tile = 2 * p + rank;
-    }
-    // 256-key tiles 0 .. jmax cover every key <= the last query row of both CTAs
-    jmax = (a.G >= 2 ? tile : (tile | 1)) / 2;
+                                          int& unit, int& jmax, bool& real) {
+    const int items = a.G * a.nT, per_unit = (items + 1) / 2;
+    unit = pair / per_unit;
+    const int k0 = 2 * (pair % per_unit);
+    int k = k0 + rank;
+    real = k < items;
+    if (!real) k = k0;  // dummy partner: rank 0's item again, nothing stored
+    tile = a.nT - 1 - k / a.G;
+    const int b = unit / a.Hkv, hk = unit % a.Hkv;
+    plane = b * a.Hq + hk * a.G + k % a.G;
+    // 256-key tiles 0 .. jmax cover every key <= the last query row of both CTAs (rank 0's
+    // item has the larger or equal tile)
+    jmax = (a.nT - 1 - k0 / a.G) / 2;
 }
 
-template <int kPoly>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT2, 1)
     fwd2_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                    const __grid_constant__ CUtensorMap tv, const Fwd2Args a) {
@@ -97,7 +97,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT2, 1)
     const int tid = threadIdx.x, warp = tid >> 5;
     const uint32_t rank = cluster_ctarank();
     int plane, tile, unit, jmax;
-    pair_item(a, blockIdx.x >> 1, (int)rank, plane, tile, unit, jmax);
+    bool real;
+    pair_item(a, blockIdx.x >> 1, (int)rank, plane, tile, unit, jmax, real);
 
     if (warp == 0) {
         tmem_alloc_2sm<512>(&bars.tmem_base);
@@ -156,7 +157,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT2, 1)
                 const uint32_t ka = smem_u32(sk + (j % kStages2) * kTileBytes);
 #pragma unroll
                 for (int k = 0; k < 8; ++k)
-                    if (a.debug != 2) mma_ss_2sm(tS, sdesc(kmajor_addr(qa, k), 16, 1024), sdesc(kmajor_addr(ka, k), 16, 1024), id_s,
+                    mma_ss_2sm(tS, sdesc(kmajor_addr(qa, k), 16, 1024), sdesc(kmajor_addr(ka, k), 16, 1024), id_s,
                                k > 0);
                 mma_commit_2sm(&bars.s_full, 0x3);
                 mma_commit_2sm(&bars.k_empty[j % kStages2], 0x3);
@@ -178,7 +179,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT2, 1)
                 const uint32_t va = smem_u32(sv + (j % kStages2) * kTileBytes);
 #pragma unroll
                 for (int k = 0; k < 16; ++k)
-                    if (a.debug != 2) mma_ts_2sm(tO, tP + k * 8, sdesc(va + k * 2048, 16384, 1024), id_o, (j > 0 || k > 0) ? 1u : 0u);
+                    mma_ts_2sm(tO, tP + k * 8, sdesc(va + k * 2048, 16384, 1024), id_o, (j > 0 || k > 0) ? 1u : 0u);
                 mma_commit_2sm(&bars.o_full, 0x3);
                 mma_commit_2sm(&bars.v_empty[j % kStages2], 0x3);
             }
@@ -189,6 +190,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT2, 1)
         const int wi = warp & 3;
         const int m = wi * 32 + (tid & 31);     // row within the CTA's tile
         const int qrow = tile * kTile + m;       // query position
+        const bool store = real && qrow < a.L;   // rows >= L (TMA zero fill) are computed, never stored
         const uint32_t lane_off = (uint32_t)(wi * 32) << 16;
         const uint32_t sS = tS + lane_off + 64 * q;
         const uint32_t sP = tP + lane_off + 32 * q;
@@ -203,7 +205,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT2, 1)
             float ss = 0.f;
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
-                const uint4 w4 = qr[c];
+                const uint4 w4 = qrow < a.L ? qr[c] : make_uint4(0, 0, 0, 0);
                 const uint32_t wv[4] = {w4.x, w4.y, w4.z, w4.w};
 #pragma unroll
                 for (int t = 0; t < 4; ++t) {
@@ -231,20 +233,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT2, 1)
             tc_fence_before();
             __syncwarp();
             if ((tid & 31) == 0) mbar_arrive_cluster(s_free_l);  // S_j may be overwritten
-            if (a.debug == 1) {  // profiling: skip the softmax math
-                uint32_t z[16] = {};
-                if (j > 0) mbar_wait(&bars.o_full, (j - 1) & 1);
-                tc_fence_after();
-                tmem_st16(sP, z);
-                tmem_st16(sP + 16, z);
-                tmem_st_wait();
-                tc_fence_before();
-                __syncwarp();
-                if ((tid & 31) == 0) mbar_arrive_cluster(p_full_l);
-                l = 1.f;
-                m_ref = 0.f;
-                continue;
-            }
             const int key0 = 2 * j * kTile + 64 * q;
             if (key0 + 63 > qrow) {  // causal mask near the diagonal
 #pragma unroll
@@ -331,13 +319,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT2, 1)
         tc_fence_after();
         const size_t row = (size_t)plane * a.L + qrow;
         const float inv = 1.f / lt;
-        if (a.out) {
-            uint32_t o[32];
+        if (a.out && __any_sync(0xffffffffu, store)) {  // tcgen05.ld is warp-collective: load
+            uint32_t o[32];                               // warp-uniformly, store per row
             tmem_ld32(sO, o);
             tmem_ld_wait();
             uint4* dst = reinterpret_cast<uint4*>(a.out + row * kD + 32 * q);
 #pragma unroll
-            for (int x = 0; x < 4; ++x) {
+            for (int x = 0; x < 4 && store; ++x) {
                 uint4 v;
                 v.x = pack_bf16(__uint_as_float(o[8 * x + 0]) * inv, __uint_as_float(o[8 * x + 1]) * inv);
                 v.y = pack_bf16(__uint_as_float(o[8 * x + 2]) * inv, __uint_as_float(o[8 * x + 3]) * inv);
@@ -346,9 +334,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT2, 1)
                 dst[x] = v;
             }
         }
-        if (q == 0) {
+        if (q == 0 && store) {
             const float lse2 = m_ref + __log2f(lt);
-            a.nlse2[row] = -lse2;
+            a.nlse2[(size_t)plane * a.Lp + qrow] = -lse2;
             if (a.lse_nat) a.lse_nat[row] = lse2 * kLn2;
         }
     }
@@ -391,52 +379,31 @@ __global__ void key_tile_norm_kernel(const __nv_bfloat16* __restrict__ k, int L,
 
 size_t fwd2_workspace(int units, int L) { return sizeof(float) * (size_t)units * ((L + 255) / 256); }
 
-bool fwd2_tc_supported(int G, int nT) {
-    return ((G >= 2 && G % 2 == 0) || (G == 1 && nT % 2 == 0)) && (nT + 1) / 2 <= kMaxT2;
-}
+bool fwd2_tc_supported(int L) { return (L + 255) / 256 <= kMaxT2; }
 
 cudaError_t launch_fwd2_tc(int L, int Hq, int Hkv, int G, int units, float c, void* out, float* nlse2,
                            float* lse_nat, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                            const void* k, float* kmax, cudaStream_t s, const void* q) {
-    static const bool attr = [] {  // once per process, thread-safe (magic static)
-        cudaFuncSetAttribute(fwd2_tc_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem2);
-        cudaFuncSetAttribute(fwd2_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem2);
-        cudaFuncSetAttribute(fwd2_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem2);
-        cudaFuncSetAttribute(fwd2_tc_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem2);
-        return true;
-    }();
-    (void)attr;
-    static const int poly = [] {  // pairs (of every 8) whose exp2 runs on the FMA pipe
-        const char* e = getenv("EMS_P1_POLY");
-        return e ? atoi(e) : 2;
-    }();
+    cudaError_t e = smem_optin(reinterpret_cast<const void*>(fwd2_tc_kernel), (int)kSmem2);
+    if (e != cudaSuccess) return e;
     Fwd2Args a;
     a.L = L;
+    a.nT = (L + kTile - 1) / kTile;
+    a.Lp = a.nT * kTile;
     a.Hq = Hq;
     a.Hkv = Hkv;
     a.G = G;
-    a.nT = L / kTile;
     a.units = units;
     a.c = c;
     a.out = static_cast<__nv_bfloat16*>(out);
     a.nlse2 = nlse2;
     a.lse_nat = lse_nat;
-    static const int dbg = [] {
-        const char* e = getenv("EMS_P1_DEBUG");
-        return e ? atoi(e) : 0;
-    }();
-    a.debug = dbg;
     a.nT2 = (L + 255) / 256;
     a.kmax = kmax;
     a.q = static_cast<const __nv_bfloat16*>(q);
     key_tile_norm_kernel<<<units * a.nT2, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(k), L, a.nT2, kmax);
-    const int pairs = G >= 2 ? a.nT * units * (G / 2) : (a.nT / 2) * units;
-    switch (poly) {
-        case 1: fwd2_tc_kernel<1><<<2 * pairs, kT2, kSmem2, s>>>(tq, tk, tv, a); break;
-        case 2: fwd2_tc_kernel<2><<<2 * pairs, kT2, kSmem2, s>>>(tq, tk, tv, a); break;
-        case 3: fwd2_tc_kernel<3><<<2 * pairs, kT2, kSmem2, s>>>(tq, tk, tv, a); break;
-        default: fwd2_tc_kernel<0><<<2 * pairs, kT2, kSmem2, s>>>(tq, tk, tv, a); break;
-    }
+    const long long pairs = (long long)units * ((G * a.nT + 1) / 2);
+    fwd2_tc_kernel<<<(unsigned)(2 * pairs), kT2, kSmem2, s>>>(tq, tk, tv, a);
     return cudaGetLastError();
 }
 

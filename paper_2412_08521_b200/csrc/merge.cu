@@ -288,8 +288,8 @@ cudaError_t launch_merge_assign_t(const Dims& dm, const void* k, const void* v,
                                          sg.part_counts, dm.cap_c, dm.cap_tbm, inv_kc, inv_vc,
                                          inv_kt, inv_vt);
     const size_t smem = sizeof(float) * 4 * 32 * (D + 1);
-    cudaFuncSetAttribute(assign_simt_kernel<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
+    cudaError_t e = smem_optin(reinterpret_cast<const void*>(assign_simt_kernel<T, D>), (int)smem);
+    if (e != cudaSuccess) return e;
     dim3 ga((dm.cap_tbm + 31) / 32, dm.units);
     if (dm.cap_tbm > 0)
         assign_simt_kernel<T, D><<<ga, 256, smem, s>>>(

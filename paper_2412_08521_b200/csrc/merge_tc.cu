@@ -297,11 +297,8 @@ cudaError_t launch_merge_tc(const Dims& dm, const void* k, const void* v, const 
     a.counts = sg.part_counts;
     a.inv = inv;
     a.dest = sg.dest;
-    static const bool attr = [] {  // once per process, thread-safe (magic static)
-        cudaFuncSetAttribute(assign_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
-        return true;
-    }();
-    (void)attr;
+    cudaError_t e = smem_optin(reinterpret_cast<const void*>(assign_tc_kernel), (int)kSmem);
+    if (e != cudaSuccess) return e;
     dim3 ga(pad_t / 128, dm.units);
     assign_tc_kernel<<<ga, kThreads, kSmem, s>>>(tkc, tvc, tkt, tvt, a);
     return cudaGetLastError();

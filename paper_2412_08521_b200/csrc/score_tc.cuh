@@ -30,15 +30,13 @@ __device__ __forceinline__ uint32_t tmem_lane_addr(uint32_t base, int warp_in_wg
 struct ColArgs {
     int L, Hq, Hkv, G, nT, units, lwin;
     float c;               // log2(e) / sqrt(d)
-    const float* nlse2;    // [B*Hq][L] negated log2-domain LSE from P1
+    const float* nlse2;    // [B*Hq][nT*128] negated log2-domain LSE from P1 (rows >= L unset)
     float* glo;            // [units][L]
     float* loc;
-    int debug = 0;         // profiling only: 1 = skip the exp epilogue, 2 = skip the MMAs
     // Head split (load balance when few units): each CTA takes G / hsplit query heads of its
     // key-tile pair and writes fp64 partial sums part_{g,l}[unit][hsplit][L]; a reduce kernel
     // sums them in head-group order.  hsplit == 1 writes glo/loc directly.
     int hsplit = 1;
-    int unit_major = 1;    // CTA order: unit by unit (Q of one unit stays in L2) or pair-major
     double* part_g = nullptr;
     double* part_l = nullptr;
 };
@@ -48,12 +46,10 @@ struct ColArgs {
 cudaError_t launch_colsum_tc(const sc::ColArgs& a, const CUtensorMap& tk, const CUtensorMap& tq,
                              cudaStream_t s);
 int colsum_hsplit(int G, int nT, int units);
-bool fwd2_tc_supported(int G, int nT);
+bool fwd2_tc_supported(int L);
 size_t fwd2_workspace(int units, int L);
 cudaError_t launch_fwd2_tc(int L, int Hq, int Hkv, int G, int units, float c, void* out, float* nlse2,
                            float* lse_nat, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                            const void* k, float* kmax, cudaStream_t s, const void* q);
-cudaError_t launch_colsum2_tc(const sc::ColArgs& a, const CUtensorMap& tk, const CUtensorMap& tq,
-                              cudaStream_t s);
 
 }  // namespace ems

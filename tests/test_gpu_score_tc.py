@@ -20,6 +20,13 @@ SHAPES = [  # B, Hq, Hkv, L, lwin
     (2, 8, 2, 1024, 32),
     (1, 8, 1, 2048, 64),
     (1, 2, 2, 768, 32),     # G == 1, 6 tiles
+    # any L (reference streaming_pass accepts any n, scoring.cpp:20-64): partial last tiles
+    (1, 4, 1, 1000, 32),    # L % 128 != 0, G = 4
+    (1, 1, 1, 4097, 32),    # G == 1, 33 tiles (odd item count: a dummy pair partner)
+    (1, 3, 1, 1000, 32),    # odd G: pairs straddle query tiles
+    (2, 6, 2, 777, 20),     # G = 3, two batches
+    (1, 2, 1, 100, 8),      # L < one tile
+    (1, 5, 1, 257, 32),     # G = 5, one key past a 256-key tile
 ]
 
 
@@ -98,3 +105,54 @@ def test_tc_large_logits_rescale_path(oracle):
         # |logit| reaches ~64 here: fp32 accumulation of q.k carries ~1e-5 absolute error
         lse = tcp.lse[0, h].double().cpu().numpy()
         assert np.all(np.abs(lse - lse_ref) <= 1e-5 + 1e-6 * np.abs(lse_ref))
+
+
+def _torch_scores(q, k, l_win):
+    """streaming_pass in torch (fp32 matmul, TF32 off, exact LSE, fp64 column sums), GQA mean."""
+    B, Hq, L, d = q.shape
+    G = Hq // k.shape[1]
+    glo = torch.zeros((B, k.shape[1], L), dtype=torch.float64, device=q.device)
+    loc = torch.zeros_like(glo)
+    for b in range(B):
+        for h in range(Hq):
+            kk = k[b, h // G].float()
+            for r0 in range(0, L, 4096):
+                r1 = min(L, r0 + 4096)
+                s = (q[b, h, r0:r1].float() @ kk[:r1].T) / d ** 0.5
+                rows = torch.arange(r0, r1, device=q.device)[:, None]
+                s.masked_fill_(torch.arange(r1, device=q.device)[None, :] > rows, float("-inf"))
+                p = torch.exp(s - torch.logsumexp(s, dim=1, keepdim=True))
+                glo[b, h // G, :r1] += p.sum(0, dtype=torch.float64)
+                lo = max(L - l_win - r0, 0)
+                if lo < r1 - r0:
+                    loc[b, h // G, :r1] += p[lo:].sum(0, dtype=torch.float64)
+    return glo / G, loc / G
+
+
+@pytest.mark.parametrize("L,G", [(32767, 4), (8191, 1)])
+def test_tc_score_long_odd_lengths(L, G):
+    """Long prompts that are not a multiple of the tile: tcgen05 (forced) against torch."""
+    dev = torch.device("cuda")
+    g = torch.Generator(device=dev)
+    g.manual_seed(L)
+    q = torch.randn((1, G, L, 128), generator=g, device=dev).to(torch.bfloat16)
+    k = torch.randn((1, 1, L, 128), generator=g, device=dev).to(torch.bfloat16)
+    v = torch.randn((1, 1, L, 128), generator=g, device=dev).to(torch.bfloat16)
+    cfg = ems.EmsConfig(n_budget=33, l_win=32, gamma=1.0, kernel_size=1)
+    plan = ems.Plan(1, G, 1, L, 128, torch.bfloat16, cfg, dev, "tcgen05", want_out=True, want_lse=True)
+    plan.score(q, k, v)
+    torch.cuda.synchronize()
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    try:
+        glo_t, loc_t = _torch_scores(q, k, 32)
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+    floor = 1e-4 * glo_t.mean()
+    eg = ((plan.glo.double() - glo_t).abs() / (glo_t + floor)).max().item()
+    m = loc_t > 1e-6
+    el = ((plan.loc.double() - loc_t).abs()[m] / loc_t[m]).max().item()
+    assert eg <= 1e-5, eg
+    assert el <= 2e-4, el
+    assert abs(plan.glo.double().sum().item() - L) <= 1e-5 * L
+    assert torch.isfinite(plan.out.float()).all()
