@@ -8,19 +8,23 @@ score pass (O, LSE, GQA-mean glo/loc) -> select -> merge -> compact, for every
 KV unit of the batch.  Default workload: BASELINE config 3 (B=1, H_q=32,
 H_kv=8, d=128, L=32768, bf16, budget 256) -- the config the metric is quoted on.
 
-* value: device-timed tokens/s with inputs resident in HBM (CUDA events,
-  barrier + synchronize on both sides, max over ranks); inputs (>= 268 MB of Q)
-  exceed the 126 MB L2, so no explicit flush is needed.
-* e2e: the same metric through the public API (ems.Plan.run) from pinned HOST
-  buffers: H2D of Q_rot/K_rot/K_raw/V and D2H of the compressed cache inside
-  the timed region.
+* value: device-timed tokens/s of the WHOLE workload with inputs resident in HBM
+  (CUDA events, barrier + synchronize on both sides, max over ranks); inputs
+  (>= 268 MB of Q) exceed the 126 MB L2, so no explicit flush is needed.
+* e2e: the same metric through the public API (ems_prefill_host): pinned HOST raw
+  Q/K/V in, RoPE on the device, compressed cache AND attention output O back to
+  pinned host memory, all inside the timed region.
 * roofline: the score pass (the dominant kernel pair) against the measured
   bf16 tensor peak; algorithmic FLOPs F_alg = 4*d*G*L(L+1)/2 per unit.
-* cpu_baseline: the reference's own code (oracle/_ref) on a bounded sample,
-  extrapolated (see _cpu_sample).
-Multi-GPU (torchrun): weak scaling, each rank runs its own batch of units, no
-collective on the data path.  --impl reference times the reference CPU path
-(rank 0 only).
+* cpu_baseline: the reference's own code (oracle/_ref) on all units of one layer at a
+  fixed sample length L' (the same L' in both arms), every (unit, head) score pass in
+  one OpenMP region over all host cores as engine.cpp:65 does; extrapolated to L
+  (score pass x L(L+1)/L'(L'+1), compress x L/L') and to every layer / batch element,
+  with the extrapolation stated in the line.
+Multi-GPU: `--gpus N` (or torchrun with N ranks) shards the workload's units across the
+ranks (shard.unit_shard: one KV head per GPU for configs 3 and 5 at N = 8), no
+collective on the data path -> strong scaling.  --impl reference times the reference
+CPU path (rank 0 only).
 """
 from __future__ import annotations
 
@@ -119,25 +123,11 @@ class ClockSampler:
         self._ready.wait(timeout=5.0)
         return self
 
-    def _energy_mj(self):
-        try:
-            import pynvml
-            return pynvml.nvmlDeviceGetTotalEnergyConsumption(pynvml.nvmlDeviceGetHandleByIndex(self.index))
-        except Exception:  # noqa: BLE001
-            return None
-
     def begin(self):
-        self.e0 = self._energy_mj()
         self.t0 = time.perf_counter()
 
     def end(self):
         self.t1 = time.perf_counter()
-        self.e1 = self._energy_mj()
-
-    def energy_j(self):
-        """Board energy over the timed window (NVML counter, J), or None."""
-        e0, e1 = getattr(self, "e0", None), getattr(self, "e1", None)
-        return None if e0 is None or e1 is None else (e1 - e0) / 1e3
 
     def stop(self):
         if self._thread is not None:
@@ -153,7 +143,8 @@ class ClockSampler:
         watts = [s[3] for s in win if s[3] is not None]
         return {"sm_mhz": statistics.median(s[1] for s in win), "sm_max_mhz": self.max_mhz,
                 "reasons": reasons, "samples": len(win), "sm_mhz_min": min(s[1] for s in win),
-                "power_w_max": max(watts) if watts else None}
+                "power_w_max": max(watts) if watts else None,
+                "power_w_median": statistics.median(watts) if watts else None}
 
 
 def unrope(x, base: float):
@@ -180,14 +171,25 @@ def dist_env():
     return ws, rank, local
 
 
-def _cpu_sample(w, seconds_budget: float = 20.0, fixed_lp: int | None = None):
-    """Reference CPU path (oracle/_ref = the reference's own sources) on a bounded sample.
+# Reference sample lengths L' per workload: the same L' in both arms (the ours arm's
+# cpu_baseline and --impl reference), sized so one sample (every unit of one layer of batch
+# element 0, with O, all host cores) is a few seconds of CPU work.
+SAMPLE_LEN = {"cfg1": 1024, "cfg2": 4096, "cfg3": 4096, "cfg3b": 4096, "cfg4": 2048, "cfg5": 2048,
+              "cfgM": 4096}
 
-    Sample: unit 0's G query heads through prefill_attention (parallel over heads as
-    engine.cpp:65 does) + GQA mean + compress_prefill, on the first L' tokens of the
-    workload's recipe, L' chosen so the sample runs ~10-30 s.  Extrapolation to the
-    full step: score cost scales as (L/L')^2 (causal L^2 d), compress as L/L'; both
-    scale linearly in the number of units.  Returns (tokens/s, description, cores)."""
+
+def _cpu_sample(w, sample_len: int | None = None):
+    """The reference CPU path (oracle/_ref = the reference's own sources) on a bounded sample.
+
+    Sample: every KV unit of one layer of batch element 0 (config 3: all 8 units = 32 query
+    heads) at the first L' tokens of the workload's recipe, through ems_ref_prefill_units:
+    prefill_attention for every (unit, query head) in ONE OpenMP region over all host
+    threads (engine.cpp:65 spreads heads the same way), GQA mean (D2), init_score_state,
+    policy_prefill_compress -> compress_prefill per unit (parallel over units).  The library
+    times the two phases separately; the full step is extrapolated as
+        t = t_score * L(L+1) / L'(L'+1) + t_compress * L / L'     (causal pairs / tokens)
+    times batch elements x layers (identical work per unit).  L' = L means no length
+    extrapolation.  Returns (tokens/s, description, cores, extrapolation dict)."""
     import numpy as np
 
     from oracle.oracle import Config, RefLib
@@ -196,24 +198,25 @@ def _cpu_sample(w, seconds_budget: float = 20.0, fixed_lp: int | None = None):
     ref = RefLib()
     cores = ref.max_threads()
     cfg = Config(n_budget=w.n_budget, l_win=w.l_win, tau=w.tau, gamma=w.gamma, kernel_size=w.kernel_size)
-    Lp = fixed_lp or min(w.seq_len, 1024)
-    un = make_unit_np(w, seed=1, seq_len=Lp, unit=0)
-    t0 = time.perf_counter()
-    ref.prefill_unit(un.q_rot, un.k_rot, un.k_raw, un.v, cfg, dump=False)
-    t_small = time.perf_counter() - t0
-    # grow L' while the projected sample stays inside the budget
-    while fixed_lp is None and Lp * 2 <= w.seq_len and t_small * 4 <= seconds_budget:
-        Lp *= 2
-        un = make_unit_np(w, seed=1, seq_len=Lp, unit=0)
-        t0 = time.perf_counter()
-        ref.prefill_unit(un.q_rot, un.k_rot, un.k_raw, un.v, cfg, dump=False)
-        t_small = time.perf_counter() - t0
-    scale = (w.seq_len / Lp) ** 2
-    t_full = t_small * scale * w.units
-    tok = w.batch * w.seq_len / t_full
-    desc = (f"reference prefill_attention x{w.group} heads + GQA mean + compress_prefill on 1 unit at "
-            f"L'={Lp} ({t_small:.2f}s, {cores} threads); extrapolated x(L/L')^2={scale:.0f} and x{w.units} units")
-    return tok, desc, cores, Lp
+    Lp = min(w.seq_len, sample_len or SAMPLE_LEN.get(w.name, 1024))
+    units = [make_unit_np(w, seed=1, seq_len=Lp, unit=u) for u in range(w.heads_kv)]
+    stack = lambda f: np.stack([getattr(u, f) for u in units])  # noqa: E731
+    ref.prefill_units(stack("q_rot"), stack("k_rot"), stack("k_raw"), stack("v"), cfg, with_out=True, dump=False)
+    t_score, t_comp = ref.last_seconds
+    L = w.seq_len
+    s_score = L * (L + 1) / (Lp * (Lp + 1))
+    s_comp = L / Lp
+    reps = w.batch * w.layers
+    t_full = (t_score * s_score + t_comp * s_comp) * reps
+    tok = w.batch * L / t_full
+    ex = {"sample_len": Lp, "seq_len": L, "score_s": round(t_score, 3), "compress_s": round(t_comp, 3),
+          "score_scale": round(s_score, 2), "compress_scale": round(s_comp, 2), "unit_scale": reps,
+          "extrapolated": Lp != L or reps != 1}
+    desc = (f"reference prefill_attention for all {w.heads_kv} units x {w.group} heads of one layer in one OpenMP "
+            f"region + GQA mean + compress_prefill, at L'={Lp} ({t_score:.2f}s + {t_comp:.2f}s, {cores} threads)"
+            + (f"; extrapolated: score x{s_score:.1f}, compress x{s_comp:.1f}, x{reps} (batch x layers)"
+               if ex["extrapolated"] else "; no extrapolation"))
+    return tok, desc, cores, ex
 
 
 def run_reference(args, w):
@@ -222,21 +225,22 @@ def run_reference(args, w):
         return
     os.environ.setdefault("OMP_WAIT_POLICY", "passive")
     times = []
-    desc, cores, lp = "", 0, None
+    desc, cores, ex = "", 0, {}
     for i in range(args.warmup + args.steps):
-        # the first call sizes the sample (~cpu_seconds of work); later steps reuse L'
-        tok, desc, cores, lp = _cpu_sample(w, seconds_budget=args.cpu_seconds, fixed_lp=lp)
+        # warm-up samples are short (thread pools, page faults); timed steps use the fixed L'
+        lp = args.sample_len or SAMPLE_LEN.get(w.name, 1024)
+        tok, desc, cores, ex = _cpu_sample(w, max(128, lp // 4) if i < args.warmup else lp)
         if i >= args.warmup:
             times.append(tok)
     import statistics
     v = statistics.median(times)
     line = {"metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * w.batch * w.seq_len / v,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
-            "config": config_dict(w, ws),
+            "config": config_dict(w, 1),
             "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": cores, "kind": "reference",
-                             "sample": desc},
+                             "sample": desc, "extrapolation": ex},
             "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -249,8 +253,9 @@ def config_dict(w, n):
                         f"d={w.head_dim} L={w.seq_len} {w.dtype} budget={w.n_budget} w={w.l_win} "
                         f"gamma={w.gamma} tau={w.tau} kernel={w.kernel_size}"
             if w.name.startswith("cfg3") else f"{w.name}",
-            "global_batch": w.batch * n, "seq_len": w.seq_len, "layers": w.layers, "units_per_gpu": w.units,
-            "parallelism": f"kv-unit sharding x{n} (weak, no collective)",
+            "global_batch": w.batch, "seq_len": w.seq_len, "layers": w.layers,
+            "units": w.batch * w.heads_kv * w.layers,
+            "parallelism": f"kv-unit sharding over {n} GPU(s) (shard.unit_shard; strong scaling, no collective)",
             "l2": _l2_note(w)}
 
 
@@ -263,6 +268,19 @@ def _l2_note(w) -> str:
     return f"inputs fit in L2 ({total / 1e6:.0f} MB); not flushed (informational config, not the headline)"
 
 
+def _relaunch(args) -> int:
+    """`python bench.py --gpus N` outside torchrun: start N ranks the way the driver does
+    (torch.distributed.run, one process per GPU, rendezvous on 127.0.0.1)."""
+    import socket
+    import subprocess
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd).returncode
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -273,12 +291,17 @@ def main():
     ap.add_argument("--batch", type=int, default=0, help="override B (config 4 uses 1/8/32)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--score-impl", default="auto", choices=["auto", "simt", "tcgen05"])
-    ap.add_argument("--cpu-seconds", type=float, default=8.0,
-                    help="CPU work budget per reference sample (ours arm uses 2.5x for cpu_baseline)")
+    ap.add_argument("--sample-len", type=int, default=0, help="reference sample length L' (default: SAMPLE_LEN)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-chunks", type=int, default=8, help="unit groups of the host copy/compute pipeline")
+    ap.add_argument("--oversubscribe", action="store_true",
+                    help="testing only: every rank on cuda:0 with gloo plumbing (ranks never wait on each "
+                         "other's kernels); numbers from such a run are not scaling results")
     args = ap.parse_args()
+
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(_relaunch(args))
 
     from paper_2412_08521_b200.inputs import CONFIGS
 
@@ -296,20 +319,34 @@ def main():
 
     from paper_2412_08521_b200 import ems
     from paper_2412_08521_b200.inputs import make_batch_torch
+    from paper_2412_08521_b200.shard import slice_inputs, unit_shard
 
     ws, rank, local = dist_env()
+    if ws > 1 and not args.oversubscribe and torch.cuda.device_count() < ws:
+        raise SystemExit(f"bench.py: {ws} ranks but {torch.cuda.device_count()} visible GPU(s)")
+    local = 0 if args.oversubscribe else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if ws > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.oversubscribe:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     cfg = ems.EmsConfig(w.n_budget, w.l_win, w.tau, w.gamma, w.kernel_size)
+    # this rank's units of every layer (strong scaling: the workload is fixed, the units are split)
+    shard = unit_shard(w.batch, w.heads_kv, ws, rank)
     # a step runs every layer of the workload (config 4: 32); layers alternate between two
     # distinct input sets (each layer's inputs are far larger than L2, so nothing is reused)
     n_layers = w.layers
-    sets = [make_batch_torch(w, seed=1 + rank, device=dev, layer=l) for l in range(min(n_layers, 2))]
+    sets = []
+    for li in range(min(n_layers, 2)):
+        full = make_batch_torch(w, seed=1, device=dev, layer=li)
+        sets.append(tuple(x.contiguous() for x in slice_inputs(*full, shard)))
+        del full
+    torch.cuda.empty_cache()
     q, kr, kw, v = sets[0]
     B, Hq, L, d = q.shape
-    plan = ems.Plan(B, Hq, w.heads_kv, L, d, q.dtype, cfg, dev, args.score_impl, want_out=True)
+    plan = ems.Plan(B, Hq, kr.shape[1], L, d, q.dtype, cfg, dev, args.score_impl, want_out=True)
     stream = torch.cuda.current_stream()
 
     def step(score_events=None):
@@ -327,9 +364,17 @@ def main():
             plan.compact(kwl, vl)
 
     def barrier():
+        torch.cuda.synchronize()
         if ws > 1:
             dist.barrier()
         torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if ws == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev if not args.oversubscribe else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.item()
 
     clk = ClockSampler(local).start()
     for _ in range(args.warmup):
@@ -357,16 +402,14 @@ def main():
     total_ms = t_start.elapsed_time(t_end)
     score_ms = sum(a.elapsed_time(b) for i in range(args.steps) for a, b in sev[i]) / args.steps
     tail_ms = sum(starts[i].elapsed_time(ends[i]) for i in range(args.steps)) / args.steps - score_ms
-    t = torch.tensor([total_ms], device=dev)
-    if ws > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_step = t.item() / args.steps
-    tokens_step = B * L * ws
+    ms_step = max_over_ranks(total_ms) / args.steps
+    tokens_step = w.batch * L  # the whole workload's tokens (every rank holds a slice of its units)
     value = tokens_step / (ms_step / 1e3)
 
     # e2e through the public API the reference's callers use: engine::prefill on RAW host
-    # matrices (ems_prefill_host): pinned host Q/K/V in, RoPE on the device, compressed cache
-    # back to pinned host memory; copies pipelined with compute in --e2e-chunks unit groups.
+    # matrices (ems_prefill_host): pinned host Q/K/V in, RoPE on the device, compressed cache and
+    # the attention output O (PrefillResult.per_head) back to pinned host memory; copies
+    # pipelined with compute in --e2e-chunks unit groups.
     e2e = None
     if not args.no_e2e:
         base = w.rope_base or 0.0
@@ -376,16 +419,19 @@ def main():
             hsets.append(tuple(x.cpu().pin_memory() for x in (q_raw, kwl, vl)))
             del q_raw
         host_cache = plan.host_cache()
+        h_out = torch.empty(plan.out.shape, dtype=plan.out.dtype, pin_memory=True)
         h2d = n_layers * sum(x.numel() * x.element_size() for x in hsets[0])
-        d2h = n_layers * sum(x.numel() * x.element_size() for x in host_cache.values())
+        d2h = n_layers * (sum(x.numel() * x.element_size() for x in host_cache.values())
+                          + h_out.numel() * h_out.element_size())
 
-        def e2e_step():  # every layer: its host inputs in, its compressed cache out
+        def e2e_step():  # every layer: its host inputs in, its compressed cache and O out
             for li in range(n_layers):
                 hq, hk, hv = hsets[li % len(hsets)]
-                plan.run_host(hq, hk, hv, base, h_k_raw=None if base else hk, chunks=args.e2e_chunks)
+                plan.run_host(hq, hk, hv, base, h_k_raw=None if base else hk, chunks=args.e2e_chunks, h_out=h_out)
 
         for _ in range(2):
             e2e_step()
+        plan.sync_status()
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
@@ -394,35 +440,36 @@ def main():
             e2e_step()
         e1.record(stream)
         barrier()
-        te = torch.tensor([e0.elapsed_time(e1) / n_e2e], device=dev)
-        if ws > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": tokens_step / (te.item() / 1e3), "unit": "tokens/s",
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": te.item(),
-               "api": f"ems.Plan.run_host (ems_prefill_host, raw Q/K + device RoPE, {args.e2e_chunks} chunks)"}
+        te = max_over_ranks(e0.elapsed_time(e1) / n_e2e)
+        sums = torch.tensor([h2d, d2h], dtype=torch.float64, device="cpu" if args.oversubscribe else dev)
+        if ws > 1:  # whole-job bytes: every rank copies its own units
+            dist.all_reduce(sums, op=dist.ReduceOp.SUM)
+        e2e = {"value": tokens_step / (te / 1e3), "unit": "tokens/s",
+               "h2d_bytes_per_step": int(sums[0].item()), "d2h_bytes_per_step": int(sums[1].item()),
+               "ms_per_step": te,
+               "api": f"ems.Plan.run_host (ems_prefill_host, raw Q/K + device RoPE, cache + O back, "
+                      f"{args.e2e_chunks} chunks)"}
 
     pk = peaks()
-    flops = f_alg(w) * n_layers  # every layer's score pass
+    shard_w = w.with_(batch=1, heads_kv=plan.dims.units, heads_q=plan.dims.units * w.group)
+    flops = f_alg(shard_w) * n_layers  # this rank's score passes
     achieved = flops / (score_ms / 1e3) / 1e12
     peak_tf = pk.get("bf16_tflops", FALLBACK_PEAKS["bf16_tflops"])
-    roof_ms = max(flops / (peak_tf * 1e12), n_layers * score_bytes(w) / (pk.get("hbm_gbs", 6650.0) * 1e9)) * 1e3
+    roof_ms = max(f_alg(w) * n_layers / ws / (peak_tf * 1e12),
+                  n_layers * score_bytes(w) / ws / (pk.get("hbm_gbs", 6650.0) * 1e9)) * 1e3
     # the optional gather of every rank's fixed-size compressed caches, off the
-    # timed path and reported on its own: one NCCL all_gather per cache tensor
+    # timed path and reported on its own: one all_gather per cache tensor
     gather_ms = None
     if ws > 1:
         try:
-            from paper_2412_08521_b200.shard import gather_caches, unit_shard
-            shard = unit_shard(1, ws * plan.dims.units, ws, rank)
-            gather_caches(plan.cache, shard, ws * plan.dims.units)  # warm-up (NCCL communicators)
+            from paper_2412_08521_b200.shard import gather_caches
+            total_units = w.batch * w.heads_kv
+            gather_caches(plan.cache, shard, total_units)  # warm-up (communicators)
             barrier()
-            g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            g0.record(stream)
-            gather_caches(plan.cache, shard, ws * plan.dims.units)
-            g1.record(stream)
+            g0 = time.perf_counter()
+            gather_caches(plan.cache, shard, total_units)
             barrier()
-            tg = torch.tensor([g0.elapsed_time(g1)], device=dev)
-            dist.all_reduce(tg, op=dist.ReduceOp.MAX)
-            gather_ms = tg.item()
+            gather_ms = max_over_ranks((time.perf_counter() - g0) * 1e3)
         except Exception as ex:  # noqa: BLE001 -- informational; never fails the bench line
             gather_ms = f"unavailable: {str(ex)[:120]}"
     # our kernel launches per step, counted by the CUDA profiler on one extra (untimed) step:
@@ -432,39 +479,43 @@ def main():
         step()
         torch.cuda.synchronize()
     kernels_per_step = sum(e.count for e in prof.key_averages() if e.device_time_total > 0 and "ems::" in e.key)
+    launches = int(max_over_ranks(kernels_per_step)) * ws
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "bf16" if w.dtype == "bf16" else "f32", "data": "synthetic",
             "config": config_dict(w, ws),
             "per_gpu_value": value / ws,
+            "units_per_gpu": plan.dims.units,
             "attention_roofline_frac": roof_ms / ms_step,
             "stage_ms": {"score": score_ms, "select+merge+compact": tail_ms},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
-                         "frac": achieved / peak_tf, "traffic": traffic_bytes(w),
+                         "frac": achieved / peak_tf, "traffic": traffic_bytes(w) if ws == 1 else None,
                          "frac_of_sustained_peak": achieved / pk.get("bf16_tflops_sustained", peak_tf),
                          "kernel": "score pass (O+LSE and glo/loc column sums)",
                          "peak_source": f"{pk['source']} bf16_tflops (burst)",
-                         "algorithmic_flops_per_launch": f_alg(w)},
-            "gpu_launches": kernels_per_step * args.steps,
+                         "algorithmic_flops_per_launch": f_alg(shard_w)},
+            "gpu_launches": launches * args.steps,
             "clocks": clk.summary(),
             "step_ms": [round(starts[i].elapsed_time(ends[i]), 3) for i in range(args.steps)],
-            "energy_j_per_step": (clk.energy_j() / args.steps) if clk.energy_j() is not None else None,
             "e2e": e2e,
         }
+        if args.oversubscribe and ws > 1:
+            line["oversubscribed"] = "all ranks on one GPU (plumbing test, not a scaling number)"
         if gather_ms is not None:
             line["cache_allgather_ms"] = gather_ms  # outside the timed region
         if not args.no_cpu_baseline and ws == 1:
             try:
-                tok, desc, cores, _ = _cpu_sample(w, 2.5 * args.cpu_seconds)
+                tok, desc, cores, ex = _cpu_sample(w, args.sample_len or None)
                 line["cpu_baseline"] = {"value": tok, "unit": "tokens/s", "cores": cores,
-                                        "kind": "reference", "sample": desc}
+                                        "kind": "reference", "sample": desc, "extrapolation": ex}
             except Exception as ex:  # noqa: BLE001
                 line["cpu_baseline"] = {"value": None, "error": str(ex)[:200]}
         print(json.dumps(line), flush=True)
     clk.stop()
     if ws > 1:
+        dist.barrier()
         dist.destroy_process_group()
 
 

@@ -56,7 +56,7 @@
 extern "C" {
 #endif
 
-#define EMS_B200_ABI_VERSION 2
+#define EMS_B200_ABI_VERSION 3
 
 #if defined(__GNUC__)
 #define EMS_API __attribute__((visibility("default")))
@@ -209,25 +209,28 @@ EMS_API int ems_prefill(const ems_desc* desc, double rope_base, const void* q, c
                 size_t workspace_bytes, cudaStream_t stream);
 
 /* engine::prefill from HOST memory -- the reference's own calling convention (per-head host
- * matrices, proj/src/engine.cpp:42-82), batched.  h_* are pinned host [B][H][L][d] tensors;
- * d_* are the caller's device staging buffers of the same shapes.  The units are split into
- * `chunks` contiguous groups of geometrically growing size (U/2^(chunks-1), ..., U/4, U/2 units,
- * so compute starts after a small first copy): the host-to-device copy of group c+1 (on copy_stream, or a
- * library-owned per-thread stream when NULL) overlaps the compute of group c (on stream), and
- * each group's compressed cache is copied to h_cache (pinned host SoA with the device
- * cache's shapes; may be NULL) as soon as it is done.  rope_base > 0: h_q/h_k are raw and
- * RoPE runs on the device into d_q_rot/d_k_rot (h_k_raw/d_k_raw unused); rope_base == 0:
- * h_q/h_k are pre-rotated and h_k_raw/d_k_raw carry the raw keys.  Asynchronous: on return
- * `stream` is ordered after every copy, so synchronising it completes the call. */
+ * matrices in, PrefillResult.per_head outputs and the head caches out; proj/src/engine.cpp:42-82,
+ * proj/include/ems/engine.hpp:36-45), batched.  h_* are pinned host [B][H][L][d] tensors; d_* are
+ * the caller's device staging buffers of the same shapes.  The units are split into `chunks`
+ * contiguous groups of geometrically growing size (U/2^(chunks-1), ..., U/4, U/2 units, so compute
+ * starts after a small first copy): the host-to-device copy of group c+1 (on copy_stream, or a
+ * library-owned per-thread stream when NULL) overlaps the compute of group c (on stream), and each
+ * group's results go back as soon as it is done: its compressed cache to h_cache (pinned host SoA
+ * with the device cache's shapes; may be NULL) and its attention output rows to h_out_o (pinned
+ * host [B][Hq][L][d]; may be NULL, needs out_o).  rope_base > 0: h_q/h_k are raw and RoPE runs on
+ * the device into d_q_rot/d_k_rot (h_k_raw/d_k_raw unused); rope_base == 0: h_q/h_k are
+ * pre-rotated and h_k_raw/d_k_raw carry the raw keys.  Asynchronous: on return -- on success and
+ * on every error after the first enqueue -- `stream` is ordered after every copy and the second
+ * compute stream, so synchronising it completes the call. */
 /* Workspace that lets ems_prefill_host keep two unit groups in flight (odd groups on a second,
  * library-owned stream with the second half of the workspace); with ems_workspace_bytes() the
  * groups run one at a time on `stream`. */
 EMS_API size_t ems_prefill_host_workspace_bytes(const ems_desc* desc);
 EMS_API int ems_prefill_host(const ems_desc* desc, double rope_base, const void* h_q, const void* h_k,
                      const void* h_k_raw, const void* h_v, void* d_q, void* d_k, void* d_k_raw,
-                     void* d_v, void* d_q_rot, void* d_k_rot, void* out_o, float* lse, float* glo,
-                     float* loc, const ems_cache* d_cache, const ems_cache* h_cache, int32_t chunks,
-                     void* workspace, size_t workspace_bytes, cudaStream_t stream,
+                     void* d_v, void* d_q_rot, void* d_k_rot, void* out_o, void* h_out_o, float* lse,
+                     float* glo, float* loc, const ems_cache* d_cache, const ems_cache* h_cache,
+                     int32_t chunks, void* workspace, size_t workspace_bytes, cudaStream_t stream,
                      cudaStream_t copy_stream);
 
 /* ---------------------------------------------------------------- decode

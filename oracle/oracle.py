@@ -396,7 +396,7 @@ class RefLib:
                                            C.c_int32, _dp, _dp, C.c_int32]
         L.ems_ref_prefill_units.argtypes = [_dp, _dp, _dp, _dp, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
                                             C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_int64,
-                                            C.c_int32, C.c_int32, _dp, _dp, C.c_int32]
+                                            C.c_int32, C.c_int32, _dp, _dp, C.c_int32, _dp]
         L.ems_ref_engine_prefill.argtypes = [_dp, _dp, _dp, C.c_int64, C.c_int64, C.c_int64,
                                              C.c_int64, C.c_int64, C.c_double, C.c_double,
                                              C.c_int64, C.c_int32, C.c_double, C.c_int64]
@@ -491,14 +491,17 @@ class RefLib:
     def prefill_units(self, q_rot, k_rot, k_raw, v, c: Config, with_out=True, dump=True):
         """U units at once (ems_ref_prefill_units): q_rot [U,G,n,d], k_rot/k_raw/v [U,n,d].
         Every (unit, query head) score pass in one OpenMP region as engine.cpp:65 does.
-        Returns (caches or None, glo [U,n], loc [U,n])."""
+        Returns (caches or None, glo [U,n], loc [U,n]); self.last_seconds = (score passes,
+        GQA mean + compress) wall seconds measured inside the library."""
         q, kr, kw, vv = map(_f64, (q_rot, k_rot, k_raw, v))
         U, G, n, d = q.shape
         glo, loc = np.zeros((U, n)), np.zeros((U, n))
+        secs = np.zeros(2)
         self._chk(self.lib.ems_ref_prefill_units(_ptr(q), _ptr(kr), _ptr(kw), _ptr(vv), U, G, n, d,
                                                  c.n_budget, c.l_win, c.tau, c.gamma, c.kernel_size,
                                                  int(c.zero_class), int(with_out), _ptr(glo), _ptr(loc),
-                                                 int(dump)), "prefill_units")
+                                                 int(dump), _ptr(secs)), "prefill_units")
+        self.last_seconds = (float(secs[0]), float(secs[1]))
         caches = None
         if dump:
             texts = self.lib.ems_ref_last_json().decode().split("\x1e")[:U]

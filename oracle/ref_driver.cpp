@@ -265,11 +265,13 @@ int ems_ref_prefill_unit(const double* q_rot, const double* k_rot, const double*
 //   with_out = 1: prefill_attention (O computed and discarded, as engine::prefill's result);
 //   0: prefill_scores (same glo/loc, scoring.hpp:48-54).  dump = 1: the caches'
 //   cache_dump_json texts, '\x1e'-terminated in unit order (ems_ref_last_json).
+//   seconds (may be NULL) <- {score passes, GQA mean + compress} wall time (omp_get_wtime).
 int ems_ref_prefill_units(const double* q_rot, const double* k_rot, const double* k_raw, const double* v,
                           int64_t U, int64_t G, int64_t n, int64_t d, int64_t n_budget, int64_t l_win,
                           double tau, double gamma, int64_t kernel, int32_t zero_class, int32_t with_out,
-                          double* glo_out, double* loc_out, int32_t dump) {
+                          double* glo_out, double* loc_out, int32_t dump, double* seconds) {
     return guarded([&] {
+        const double t0 = omp_get_wtime();
         const auto cfg = make_config(n_budget, l_win, tau, gamma, kernel, zero_class);
         const std::size_t l_win_eff = std::min<std::size_t>(l_win, n);
         const int64_t items = U * G;
@@ -303,6 +305,7 @@ int ems_ref_prefill_units(const double* q_rot, const double* k_rot, const double
         omp_set_max_active_levels(levels);
         for (auto& e : errs)
             if (!e.empty()) throw std::invalid_argument(e);
+        const double t1 = omp_get_wtime();
         std::vector<std::string> dumps(U);
 #pragma omp parallel for schedule(dynamic, 1)
         for (int64_t u = 0; u < U; ++u) {
@@ -322,6 +325,10 @@ int ems_ref_prefill_units(const double* q_rot, const double* k_rot, const double
             } catch (const std::exception& e) {
                 dumps[u] = std::string("\x1f") + e.what();
             }
+        }
+        if (seconds) {
+            seconds[0] = t1 - t0;
+            seconds[1] = omp_get_wtime() - t1;
         }
         g_json.clear();
         for (auto& s : dumps) {

@@ -634,11 +634,12 @@ struct HostPipeRes {
 __global__ void merge_status_kernel(DevStatus* dst, const DevStatus* src) {
     if (dst->code == 0 && src->code != 0) *dst = *src;
 }
-thread_local HostPipeRes g_pipe[8];
+constexpr int kMaxDevices = 64;
+thread_local HostPipeRes g_pipe[kMaxDevices];
 
 HostPipeRes* pipe_res(int nev) {
     int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 8) return nullptr;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return nullptr;
     HostPipeRes& r = g_pipe[dev];
     if (r.copy == nullptr && cudaStreamCreateWithFlags(&r.copy, cudaStreamNonBlocking) != cudaSuccess)
         return nullptr;
@@ -673,7 +674,7 @@ struct CacheField {
 
 extern "C" int ems_prefill_host(const ems_desc* d, double rope_base, const void* h_q, const void* h_k,
                                 const void* h_k_raw, const void* h_v, void* d_q, void* d_k, void* d_k_raw,
-                                void* d_v, void* d_q_rot, void* d_k_rot, void* out_o, float* lse,
+                                void* d_v, void* d_q_rot, void* d_k_rot, void* out_o, void* h_out_o, float* lse,
                                 float* glo, float* loc, const ems_cache* d_cache, const ems_cache* h_cache,
                                 int32_t chunks, void* ws, size_t ws_bytes, cudaStream_t s,
                                 cudaStream_t copy_stream) {
@@ -682,9 +683,9 @@ extern "C" int ems_prefill_host(const ems_desc* d, double rope_base, const void*
     if (int rc = check_ws(d, ws, ws_bytes)) return rc;
     const bool rope = rope_base > 0.0;
     if (!(rope_base >= 0.0) || !h_q || !h_k || !h_v || !d_q || !d_k || !d_v || !d_cache ||
-        (rope && (!d_q_rot || !d_k_rot)) || (!rope && (!h_k_raw || !d_k_raw))) {
+        (rope && (!d_q_rot || !d_k_rot)) || (!rope && (!h_k_raw || !d_k_raw)) || (h_out_o && !out_o)) {
         set_error("ems_prefill_host: missing buffer (RoPE needs q_rot/k_rot scratch; pre-rotated "
-                  "inputs need k_raw)");
+                  "inputs need k_raw; a host O needs the device O)");
         return EMS_INVALID_ARGUMENT;
     }
     const Dims m = make_dims(*d);
@@ -719,86 +720,95 @@ extern "C" int ems_prefill_host(const ems_desc* d, double rope_base, const void*
     const bool dual = nc >= 2 && ws_bytes >= 2 * one;
     void* ws2 = dual ? off(ws, one) : nullptr;
     cudaStream_t s2 = dual ? res->comp2 : s;
-    EMS_CUDA_CHECK(cudaMemsetAsync(ws, 0, sizeof(DevStatus), s));
-    if (dual) EMS_CUDA_CHECK(cudaMemsetAsync(ws2, 0, sizeof(DevStatus), s));
-    // the copy stream (and the second compute stream) must not overwrite device inputs that
-    // earlier work on `s` still reads
-    EMS_CUDA_CHECK(cudaEventRecord(ev[2 * nc], s));
-    EMS_CUDA_CHECK(cudaStreamWaitEvent(cs, ev[2 * nc], 0));
-    if (dual) EMS_CUDA_CHECK(cudaStreamWaitEvent(s2, ev[2 * nc], 0));
-    // Geometric groups (U / 2^(nc-1), ..., U / 4, U / 2 units): the first group's inputs land
-    // after a small copy, so compute starts early; later groups are large (efficient grids)
-    // and their copies finish while earlier groups compute.
-    auto group_end = [&](int c) {
-        if (c >= nc - 1) return U;
-        const long long e = ((long long)U + (1ll << (nc - 1 - c)) - 1) >> (nc - 1 - c);
-        return (int)(e < c + 1 ? c + 1 : e);
-    };
-    auto unit_range = [&](int c, int& u0, int& n) {
-        u0 = c == 0 ? 0 : group_end(c - 1);
-        n = group_end(c) - u0;
-    };
-    // (1) H2D of every chunk, in chunk order (score inputs first, the raw K of a pre-rotated
-    //     problem last since only the merge/compact stages read it)
-    for (int c = 0; c < nc; ++c) {
-        int u0, n;
-        unit_range(c, u0, n);
-        const size_t oq = (size_t)u0 * G * row, nq = (size_t)n * G * row;
-        const size_t ok = (size_t)u0 * row, nk = (size_t)n * row;
-        EMS_CUDA_CHECK(cudaMemcpyAsync(off(d_q, oq), off(h_q, oq), nq, cudaMemcpyHostToDevice, cs));
-        EMS_CUDA_CHECK(cudaMemcpyAsync(off(d_k, ok), off(h_k, ok), nk, cudaMemcpyHostToDevice, cs));
-        EMS_CUDA_CHECK(cudaMemcpyAsync(off(d_v, ok), off(h_v, ok), nk, cudaMemcpyHostToDevice, cs));
-        if (!rope)
-            EMS_CUDA_CHECK(cudaMemcpyAsync(off(d_k_raw, ok), off(h_k_raw, ok), nk, cudaMemcpyHostToDevice, cs));
-        EMS_CUDA_CHECK(cudaEventRecord(ev[c], cs));
-    }
-    // (2) compute chunk c once its inputs landed; (3) copy its cache back as soon as it is done
-    for (int c = 0; c < nc; ++c) {
-        int u0, n;
-        unit_range(c, u0, n);
-        ems_desc sub = *d;
-        sub.batch = 1;
-        sub.heads_kv = n;
-        sub.heads_q = n * G;
-        const size_t oq = (size_t)u0 * G * row, ok = (size_t)u0 * row;
-        cudaStream_t sc = (c & 1) ? s2 : s;
-        void* wsc = dual && (c & 1) ? ws2 : ws;
-        EMS_CUDA_CHECK(cudaStreamWaitEvent(sc, ev[c], 0));
-        const void* qr = off(d_q, oq);
-        const void* kr = off(d_k, ok);
-        const void* kraw = rope ? kr : off(d_k_raw, ok);
-        if (rope) {
-            EMS_CUDA_CHECK(launch_rope(d->dtype, n * G, m.L, m.d, rope_base, d->first_position, qr,
-                                       off(d_q_rot, oq), sc));
-            EMS_CUDA_CHECK(launch_rope(d->dtype, n, m.L, m.d, rope_base, d->first_position, kr,
-                                       off(d_k_rot, ok), sc));
-            qr = off(d_q_rot, oq);
-            kr = off(d_k_rot, ok);
+    // Everything below is stream-ordered.  Whatever happens (a failed launch part-way through the
+    // groups included), `stream` is finally ordered after the copy stream and the second compute
+    // stream, so a caller that synchronises it never races with copies still in flight.
+    const int rc = [&]() -> int {
+        EMS_CUDA_CHECK(cudaMemsetAsync(ws, 0, sizeof(DevStatus), s));
+        if (dual) EMS_CUDA_CHECK(cudaMemsetAsync(ws2, 0, sizeof(DevStatus), s));
+        // the copy stream (and the second compute stream) must not overwrite device inputs that
+        // earlier work on `s` still reads
+        EMS_CUDA_CHECK(cudaEventRecord(ev[2 * nc], s));
+        EMS_CUDA_CHECK(cudaStreamWaitEvent(cs, ev[2 * nc], 0));
+        if (dual) EMS_CUDA_CHECK(cudaStreamWaitEvent(s2, ev[2 * nc], 0));
+        // Geometric groups (U / 2^(nc-1), ..., U / 4, U / 2 units): the first group's inputs land
+        // after a small copy, so compute starts early; later groups are large (efficient grids)
+        // and their copies finish while earlier groups compute.
+        auto group_end = [&](int c) {
+            if (c >= nc - 1) return U;
+            const long long e = ((long long)U + (1ll << (nc - 1 - c)) - 1) >> (nc - 1 - c);
+            return (int)(e < c + 1 ? c + 1 : e);
+        };
+        auto unit_range = [&](int c, int& u0, int& n) {
+            u0 = c == 0 ? 0 : group_end(c - 1);
+            n = group_end(c) - u0;
+        };
+        // (1) H2D of every chunk, in chunk order (score inputs first, the raw K of a pre-rotated
+        //     problem last since only the merge/compact stages read it)
+        for (int c = 0; c < nc; ++c) {
+            int u0, n;
+            unit_range(c, u0, n);
+            const size_t oq = (size_t)u0 * G * row, nq = (size_t)n * G * row;
+            const size_t ok = (size_t)u0 * row, nk = (size_t)n * row;
+            EMS_CUDA_CHECK(cudaMemcpyAsync(off(d_q, oq), off(h_q, oq), nq, cudaMemcpyHostToDevice, cs));
+            EMS_CUDA_CHECK(cudaMemcpyAsync(off(d_k, ok), off(h_k, ok), nk, cudaMemcpyHostToDevice, cs));
+            EMS_CUDA_CHECK(cudaMemcpyAsync(off(d_v, ok), off(h_v, ok), nk, cudaMemcpyHostToDevice, cs));
+            if (!rope)
+                EMS_CUDA_CHECK(cudaMemcpyAsync(off(d_k_raw, ok), off(h_k_raw, ok), nk, cudaMemcpyHostToDevice, cs));
+            EMS_CUDA_CHECK(cudaEventRecord(ev[c], cs));
         }
-        ems_cache scache = *d_cache;
-        for (const CacheField& f : fields) scache.*f.ptr = off(d_cache->*f.ptr, (size_t)u0 * f.per_unit);
-        const size_t ol = (size_t)u0 * m.L;
-        if (int rc = run_path(&sub, qr, kr, kraw, off(d_v, ok), off(out_o, oq), off(lse, (size_t)u0 * G * m.L * 4),
-                              off(glo, ol * 4), off(loc, ol * 4), nullptr, scache, wsc, sc, u0))
-            return rc;
-        EMS_CUDA_CHECK(cudaEventRecord(ev[nc + c], sc));
-        if (h_cache) {
-            EMS_CUDA_CHECK(cudaStreamWaitEvent(cs, ev[nc + c], 0));
-            for (const CacheField& f : fields)
-                EMS_CUDA_CHECK(cudaMemcpyAsync(off(h_cache->*f.ptr, (size_t)u0 * f.per_unit), scache.*f.ptr,
-                                               (size_t)n * f.per_unit, cudaMemcpyDeviceToHost, cs));
+        // (2) compute chunk c once its inputs landed; (3) copy its cache back as soon as it is done
+        for (int c = 0; c < nc; ++c) {
+            int u0, n;
+            unit_range(c, u0, n);
+            ems_desc sub = *d;
+            sub.batch = 1;
+            sub.heads_kv = n;
+            sub.heads_q = n * G;
+            const size_t oq = (size_t)u0 * G * row, ok = (size_t)u0 * row;
+            cudaStream_t sc = (c & 1) ? s2 : s;
+            void* wsc = dual && (c & 1) ? ws2 : ws;
+            EMS_CUDA_CHECK(cudaStreamWaitEvent(sc, ev[c], 0));
+            const void* qr = off(d_q, oq);
+            const void* kr = off(d_k, ok);
+            const void* kraw = rope ? kr : off(d_k_raw, ok);
+            if (rope) {
+                EMS_CUDA_CHECK(launch_rope(d->dtype, n * G, m.L, m.d, rope_base, d->first_position, qr,
+                                           off(d_q_rot, oq), sc));
+                EMS_CUDA_CHECK(launch_rope(d->dtype, n, m.L, m.d, rope_base, d->first_position, kr,
+                                           off(d_k_rot, ok), sc));
+                qr = off(d_q_rot, oq);
+                kr = off(d_k_rot, ok);
+            }
+            ems_cache scache = *d_cache;
+            for (const CacheField& f : fields) scache.*f.ptr = off(d_cache->*f.ptr, (size_t)u0 * f.per_unit);
+            const size_t ol = (size_t)u0 * m.L;
+            if (int rc = run_path(&sub, qr, kr, kraw, off(d_v, ok), off(out_o, oq), off(lse, (size_t)u0 * G * m.L * 4),
+                                  off(glo, ol * 4), off(loc, ol * 4), nullptr, scache, wsc, sc, u0))
+                return rc;
+            EMS_CUDA_CHECK(cudaEventRecord(ev[nc + c], sc));
+            if (h_cache || h_out_o) EMS_CUDA_CHECK(cudaStreamWaitEvent(cs, ev[nc + c], 0));
+            if (h_cache)
+                for (const CacheField& f : fields)
+                    EMS_CUDA_CHECK(cudaMemcpyAsync(off(h_cache->*f.ptr, (size_t)u0 * f.per_unit), scache.*f.ptr,
+                                                   (size_t)n * f.per_unit, cudaMemcpyDeviceToHost, cs));
+            if (h_out_o)  // engine::prefill's PrefillResult.per_head outputs (engine.hpp:36-45)
+                EMS_CUDA_CHECK(cudaMemcpyAsync(off(h_out_o, oq), off(out_o, oq), (size_t)n * G * row,
+                                               cudaMemcpyDeviceToHost, cs));
         }
-    }
-    // the caller synchronises `s`: make it cover the last cache copy and the second stream
-    EMS_CUDA_CHECK(cudaEventRecord(ev[2 * nc + 1], cs));
-    EMS_CUDA_CHECK(cudaStreamWaitEvent(s, ev[2 * nc + 1], 0));
+        return EMS_OK;
+    }();
+    cudaEventRecord(ev[2 * nc + 1], cs);
+    cudaStreamWaitEvent(s, ev[2 * nc + 1], 0);
     if (dual) {
-        EMS_CUDA_CHECK(cudaEventRecord(ev[2 * nc + 2], s2));
-        EMS_CUDA_CHECK(cudaStreamWaitEvent(s, ev[2 * nc + 2], 0));
-        merge_status_kernel<<<1, 1, 0, s>>>(static_cast<DevStatus*>(ws), static_cast<const DevStatus*>(ws2));
-        EMS_CUDA_CHECK(cudaGetLastError());
+        cudaEventRecord(ev[2 * nc + 2], s2);
+        cudaStreamWaitEvent(s, ev[2 * nc + 2], 0);
+        if (rc == EMS_OK) {
+            merge_status_kernel<<<1, 1, 0, s>>>(static_cast<DevStatus*>(ws), static_cast<const DevStatus*>(ws2));
+            EMS_CUDA_CHECK(cudaGetLastError());
+        }
     }
-    return EMS_OK;
+    return rc;
 }
 
 // ----------------------------------------------------------------------------------------

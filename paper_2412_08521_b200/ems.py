@@ -128,7 +128,7 @@ def lib() -> C.CDLL:
         L.ems_redundancy_rate.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_int32, vp, vp, C.c_double, vp, vp,
                                           C.c_size_t, vp]
         L.ems_prefill_host.argtypes = [C.POINTER(Desc), C.c_double, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,
-                                       fp, fp, fp, C.POINTER(CCache), C.POINTER(CCache), C.c_int32, vp,
+                                       vp, fp, fp, fp, C.POINTER(CCache), C.POINTER(CCache), C.c_int32, vp,
                                        C.c_size_t, vp, vp]
         L.ems_decode_dims_for.argtypes = [C.POINTER(Desc), C.c_int32, C.POINTER(DecodeDims)]
         L.ems_decode_workspace_bytes.restype = C.c_size_t
@@ -295,17 +295,21 @@ class Plan:
         return self._host_cache
 
     def run_host(self, h_q, h_k, h_v, rope_base: float, h_k_raw=None, chunks: int = 8, stream=None,
-                 concurrent: bool = True) -> dict:
+                 concurrent: bool = True, h_out=None) -> dict:
         """engine::prefill from HOST (pinned) tensors (ems_prefill_host): the library stages the
         inputs in `chunks` groups of units and overlaps each group's host-to-device copy with
-        the previous group's compute; every group's compressed cache is copied back to the
-        pinned host cache as soon as it is done.  rope_base > 0: raw Q/K, RoPE on the device;
+        the previous group's compute; every group's compressed cache (and, with h_out, its
+        attention output rows: PrefillResult.per_head, engine.hpp:36-45) is copied back to pinned
+        host memory as soon as it is done.  rope_base > 0: raw Q/K, RoPE on the device;
         rope_base == 0: pre-rotated Q/K plus h_k_raw.  concurrent: two groups in flight (a
         second workspace, ems_prefill_host_workspace_bytes).  Asynchronous; returns the host cache."""
         D = self.desc
         qs = (D.batch, D.heads_q, D.seq_len, D.head_dim)
         ks = (D.batch, D.heads_kv, D.seq_len, D.head_dim)
-        for name, t, shp in (("q", h_q, qs), ("k", h_k, ks), ("v", h_v, ks), ("k_raw", h_k_raw, ks)):
+        if h_out is not None and self.out is None:
+            raise InvalidArgument("h_out needs a plan built with want_out=True")
+        for name, t, shp in (("q", h_q, qs), ("k", h_k, ks), ("v", h_v, ks), ("k_raw", h_k_raw, ks),
+                             ("out", h_out, qs)):
             if t is None:
                 continue
             if tuple(t.shape) != shp or t.dtype != self.dtype or not t.is_contiguous() or t.is_cuda \
@@ -333,7 +337,8 @@ class Plan:
         _check(lib().ems_prefill_host(
             C.byref(self.desc), float(rope_base), _p(h_q), _p(h_k), _p(h_k_raw), _p(h_v), _p(st["q"]), _p(st["k"]),
             _p(kraw_d), _p(st["v"]), _p(self.q_rot) if rope_base > 0 else None,
-            _p(self.k_rot) if rope_base > 0 else None, _p(self.out), _p(self.lse), _p(self.glo), _p(self.loc),
+            _p(self.k_rot) if rope_base > 0 else None, _p(self.out), _p(h_out), _p(self.lse), _p(self.glo),
+            _p(self.loc),
             C.byref(self._ccache), C.byref(self._hcache), int(chunks), _p(ws), ws.numel(),
             _stream(stream), None))
         return hc
@@ -446,11 +451,13 @@ def prefill_host(q, k, v, cfg: EmsConfig, rope_base: float, chunks: int = 8, wan
                  first_position=0) -> Plan:
     """engine::prefill (proj/src/engine.cpp:42-82) on pinned HOST [B][H][L][d] tensors, the
     reference's own calling convention: copies pipelined with compute (ems_prefill_host).
-    Returns the Plan; plan.host_cache() holds the compressed cache on the host."""
+    Returns the Plan; plan.host_cache() holds the compressed cache on the host and, with
+    want_out, plan.host_out the attention outputs (PrefillResult.per_head, engine.hpp:36-45)."""
     B, Hq, L, d = q.shape
     plan = Plan(B, Hq, k.shape[1], L, d, q.dtype, cfg, "cuda", score_impl, want_out,
                 first_position=first_position)
-    plan.run_host(q, k, v, rope_base, chunks=chunks)
+    plan.host_out = torch.empty(q.shape, dtype=q.dtype, pin_memory=True) if want_out else None
+    plan.run_host(q, k, v, rope_base, chunks=chunks, h_out=plan.host_out)
     plan.sync_status()
     return plan
 
