@@ -29,7 +29,7 @@ def test_exports_every_declared_symbol(L):
     assert len(syms) >= 12, syms
     for s in syms:
         assert hasattr(L, s), f"libems_b200.so does not export {s}"
-    assert L.ems_abi_version() == 2
+    assert L.ems_abi_version() == 3
 
 
 def _desc(**kw):
