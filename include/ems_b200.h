@@ -239,7 +239,7 @@ EMS_API int ems_prefill_host(const ems_desc* desc, double rope_base, const void*
  * fixed-capacity device SoA (HeadCacheState, proj/include/ems/cache.hpp:81-111): center
  * slots (slot_alive marks live std::optional slots; a freed slot is reused lowest-first), a
  * ring buffer of exact locals, the position-sorted LUT, and meta[8] = {ring head, locals,
- * LUT entries, window_fill, compressed, live centers, 0, 0}.  Keys/values fp32, scores fp64.
+ * LUT entries, window_fill, compressed, live centers, error code, 0}.  Keys/values fp32, scores fp64.
  * Every policy's decode rule (policy_decode_compress, proj/src/policies.cpp:182-242): EMS
  * decode_update; SnapKV graduates locals (decode tokens accumulate); H2O graduates and drops
  * the lowest-glo center; StreamingLLM graduates and drops the oldest non-sink center; full
@@ -290,6 +290,11 @@ EMS_API int ems_decode_step(const ems_desc* desc, int64_t position, const void* 
                     int32_t max_positions, const void* q, const void* k, const void* v, void* out,
                     int32_t* argmax_position, const ems_decode_state* state, void* workspace,
                     size_t workspace_bytes, cudaStream_t stream);
+
+/* Synchronises `stream` and returns the first unit's decode error (EMS_CORRUPTION: stepped past the
+ * capacity the state was sized for -- more steps than max_positions - seq_len -- or no free center
+ * slot), recorded in meta[6] by the step kernel; a failed unit stops updating. */
+EMS_API int ems_decode_sync_status(const ems_desc* desc, const ems_decode_state* state, cudaStream_t stream);
 
 /* Standalone redundancy_cross (analysis.hpp:19-20) for one pair of token groups:
  * k_rows/v_rows [n_rows][d], k_cols/v_cols [n_cols][d] (dtype) -> r [n_rows][n_cols] fp32. */

@@ -5,7 +5,7 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
-#include <set>
+#include <map>
 #include <utility>
 #include <vector>
 
@@ -32,10 +32,11 @@ cudaError_t launch_merge_assign(const Dims& dm, int dtype, const void* k, const 
 cudaError_t launch_merge_scatter(const Dims& dm, int dtype, const void* k, const void* v,
                                  const float* glo, const float* loc, const ems_stage& sg,
                                  int32_t* ws_count, int32_t* ws_members, const ems_cache& cache,
-                                 cudaStream_t s);
+                                 DevStatus* status, cudaStream_t s);
 cudaError_t launch_compact(const Dims& dm, int dtype, const void* k, const void* v,
                            const float* glo, const float* loc, const ems_stage& sg,
-                           const ems_cache& c, int zero_class, int64_t first_pos, cudaStream_t s);
+                           const ems_cache& c, int zero_class, int64_t first_pos, DevStatus* status,
+                           cudaStream_t s);
 cudaError_t launch_keep_all(const Dims& dm, int dtype, const void* k, const void* v,
                             const float* glo, const float* loc, const ems_stage& sg,
                             const ems_cache& c, int64_t first_pos, cudaStream_t s);
@@ -50,6 +51,7 @@ cudaError_t launch_decode_step(const Dims& m, int dtype, int S, int W, int T, in
                                int32_t* argmax_pos, const ems_decode_state& st, void* ws, cudaStream_t s,
                                int policy, int sink, int n_budget);
 size_t decode_workspace_bytes(const Dims& m, int R);
+size_t decode_smem_bytes(const Dims& m, int S, int W);
 cudaError_t launch_redundancy_cross(int dtype, int d, const void* kr, const void* vr, int nr,
                                     const void* kc, const void* vc, int nc, int key_only,
                                     float* r, cudaStream_t s);
@@ -72,14 +74,16 @@ void set_error(const char* fmt, ...) {
 
 cudaError_t smem_optin(const void* kernel, int bytes) {
     static std::mutex mu;
-    static std::set<std::pair<const void*, int>> done;  // (kernel, device) pairs already opted in
+    static std::map<std::pair<const void*, int>, int> done;  // (kernel, device) -> bytes opted in
+    if (bytes <= 48 * 1024) return cudaSuccess;              // always available without opt-in
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
     std::lock_guard<std::mutex> lock(mu);
-    if (done.count({kernel, dev})) return cudaSuccess;
+    int& have = done[{kernel, dev}];
+    if (have >= bytes) return cudaSuccess;
     e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    if (e == cudaSuccess) done.insert({kernel, dev});
+    if (e == cudaSuccess) have = bytes;
     return e;
 }
 
@@ -282,8 +286,9 @@ int run_merge(const ems_desc* desc, const void* k_raw, const void* v, const ems_
 
 int run_compact(const ems_desc* desc, const void* k_raw, const void* v, const float* glo,
                 const float* loc, const ems_stage& sg, const ems_cache& c, void* ws,
-                cudaStream_t s) {
-    const Dims m = make_dims(*desc);
+                cudaStream_t s, int unit_base = 0) {
+    Dims m = make_dims(*desc);
+    m.unit_base = unit_base;
     const Layout l = layout(*desc);
     cudaError_t e;
     if (m.L <= desc->n_budget || desc->policy == EMS_POLICY_FULL) {  // policies.cpp:136-138
@@ -292,10 +297,15 @@ int run_compact(const ems_desc* desc, const void* k_raw, const void* v, const fl
         ems_stage sg2 = sg;
         if (m.cap_tbm <= 0) sg2.dest = at<int32_t>(ws, l.dest);  // never read (no TBM tokens)
         e = launch_compact(m, desc->dtype, k_raw, v, glo, loc, sg2, c, desc->zero_class,
-                           desc->first_position, s);
-        if (e == cudaSuccess && m.cap_tbm > 0)
+                           desc->first_position, at<DevStatus>(ws, l.status), s);
+        if (e == cudaSuccess && m.cap_tbm > 0) {
             e = launch_merge_scatter(m, desc->dtype, k_raw, v, glo, loc, sg, at<int32_t>(ws, l.cnt),
-                                     at<int32_t>(ws, l.mem), c, s);
+                                     at<int32_t>(ws, l.mem), c, at<DevStatus>(ws, l.status), s);
+            if (e != cudaSuccess) {
+                set_error("weighted-merge launch: %s", cudaGetErrorString(e));
+                return EMS_CUDA_ERROR;
+            }
+        }
     }
     if (e != cudaSuccess) {
         set_error("compact launch: %s", cudaGetErrorString(e));
@@ -468,7 +478,7 @@ int run_path(const ems_desc* d, const void* q_rot, const void* k_rot, const void
         if (int rc = run_select(d, g, lc, sg, ws, s, unit_base)) return rc;
         if (int rc = run_merge(d, k_raw, v, sg, ws, s)) return rc;
     }
-    return run_compact(d, k_raw, v, g, lc, sg, c, ws, s);
+    return run_compact(d, k_raw, v, g, lc, sg, c, ws, s, unit_base);
 }
 }  // namespace
 }  // namespace ems
@@ -847,7 +857,7 @@ void decode_caps(const ems_desc& d, int max_pos, int& S, int& W, int& T, int& R)
     }
     R = T + W;
 }
-int decode_check(const ems_desc* d) {
+int decode_check(const ems_desc* d, int max_pos) {
     if (int rc = ems_validate(d)) return rc;
     if (d->heads_q / d->heads_kv > 8) {
         set_error("decode: at most 8 query heads per KV head");
@@ -856,6 +866,22 @@ int decode_check(const ems_desc* d) {
     if (d->position_mode != 0 && d->position_mode != 1) {
         set_error("bad position_mode");
         return EMS_INVALID_ARGUMENT;
+    }
+    if (max_pos < d->seq_len) {
+        set_error("decode: max_positions %d < seq_len %d", max_pos, d->seq_len);
+        return EMS_INVALID_ARGUMENT;
+    }
+    // the step keeps one fp64 accumulator per slot + local in shared memory: the full and SnapKV
+    // policies grow S + W with the prompt and the horizon
+    int S, W, T, R;
+    decode_caps(*d, max_pos, S, W, T, R);
+    const size_t smem = decode_smem_bytes(make_dims(*d), S, W);
+    constexpr size_t kSmemLimit = 227 * 1024 - 8 * 1024;  // opt-in maximum minus the static part
+    if (smem > kSmemLimit) {
+        set_error("decode: %zu B of shared memory for %d slots + %d locals exceeds the %zu B available "
+                  "(shorter prompt or horizon, or the EMS / H2O / StreamingLLM policies)",
+                  smem, S, W, kSmemLimit);
+        return EMS_UNSUPPORTED;
     }
     return EMS_OK;
 }
@@ -866,7 +892,7 @@ extern "C" {
 
 int ems_decode_dims_for(const ems_desc* d, int32_t max_pos, ems_decode_dims* out) {
     using namespace ems;
-    if (int rc = decode_check(d)) return rc;
+    if (int rc = decode_check(d, max_pos)) return rc;
     int S, W, T, R;
     decode_caps(*d, max_pos, S, W, T, R);
     out->units = d->batch * d->heads_kv;
@@ -879,7 +905,7 @@ int ems_decode_dims_for(const ems_desc* d, int32_t max_pos, ems_decode_dims* out
 
 size_t ems_decode_workspace_bytes(const ems_desc* d, int32_t max_pos) {
     using namespace ems;
-    if (decode_check(d) != EMS_OK) return 0;
+    if (decode_check(d, max_pos) != EMS_OK) return 0;
     int S, W, T, R;
     decode_caps(*d, max_pos, S, W, T, R);
     return decode_workspace_bytes(make_dims(*d), R);
@@ -902,7 +928,7 @@ int ems_rope_table(int32_t d, double base, int32_t max_pos, void* table, cudaStr
 int ems_decode_init(const ems_desc* d, int32_t max_pos, const ems_cache* c, const ems_decode_state* st,
                     cudaStream_t s) {
     using namespace ems;
-    if (int rc = decode_check(d)) return rc;
+    if (int rc = decode_check(d, max_pos)) return rc;
     if (!c || !st) {
         set_error("ems_decode_init: null cache/state");
         return EMS_INVALID_ARGUMENT;
@@ -917,11 +943,30 @@ int ems_decode_init(const ems_desc* d, int32_t max_pos, const ems_cache* c, cons
     return EMS_OK;
 }
 
+int ems_decode_sync_status(const ems_desc* d, const ems_decode_state* st, cudaStream_t s) {
+    using namespace ems;
+    if (int rc = ems_validate(d)) return rc;
+    if (!st || !st->meta) {
+        set_error("ems_decode_sync_status: null state");
+        return EMS_INVALID_ARGUMENT;
+    }
+    const int U = d->batch * d->heads_kv;
+    std::vector<int32_t> meta((size_t)U * 8);
+    EMS_CUDA_CHECK(cudaStreamSynchronize(s));
+    EMS_CUDA_CHECK(cudaMemcpy(meta.data(), st->meta, meta.size() * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    for (int u = 0; u < U; ++u)
+        if (meta[(size_t)u * 8 + 6] != 0) {
+            set_error("decode state of unit %d is corrupt (stepped past its capacity or no free slot)", u);
+            return meta[(size_t)u * 8 + 6];
+        }
+    return EMS_OK;
+}
+
 int ems_decode_step(const ems_desc* d, int64_t position, const void* table, int32_t max_pos, const void* q,
                     const void* k, const void* v, void* out, int32_t* argmax_pos, const ems_decode_state* st,
                     void* ws, size_t ws_bytes, cudaStream_t s) {
     using namespace ems;
-    if (int rc = decode_check(d)) return rc;
+    if (int rc = decode_check(d, max_pos)) return rc;
     if (!table || !q || !k || !v || !out || !argmax_pos || !st) {
         set_error("ems_decode_step: null argument");
         return EMS_INVALID_ARGUMENT;

@@ -92,10 +92,15 @@ __global__ void __launch_bounds__(256) compact_entries_kernel(
 
 // Position-sorted LUT via a block-wide scan over the class bytes, one CTA per unit.
 constexpr int kLutThreads = 1024;
+// The kernel ends with HeadCacheState::check_integrity (proj/src/cache.cpp:66-80) on the LUT it
+// just wrote: every non-zero-class entry names a live center slot and positions are strictly
+// increasing; a violation (possible only through inconsistent caller-supplied stage buffers)
+// records EMS_CORRUPTION, the reference's CorruptionError.
 __global__ void __launch_bounds__(kLutThreads) compact_lut_kernel(
     int L, const int8_t* __restrict__ cls_all, const int32_t* __restrict__ dest_all,
     const int32_t* __restrict__ counts, int cap_t, int cap_lut, int zero_class, int64_t first_pos,
-    int32_t* __restrict__ lut_pos, int32_t* __restrict__ lut_slot, int32_t* __restrict__ out_counts) {
+    int32_t* __restrict__ lut_pos, int32_t* __restrict__ lut_slot, int32_t* __restrict__ out_counts,
+    DevStatus* status, int unit_base) {
     __shared__ int shs[32];
     const int u = blockIdx.x, tid = threadIdx.x;
     const int8_t* cls = cls_all + (size_t)u * L;
@@ -113,7 +118,7 @@ __global__ void __launch_bounds__(kLutThreads) compact_lut_kernel(
         int rt = rt0;
         for (int i = s0; i < s1; ++i) {
             if (cls[i] == 2) ++cl;
-            else if (cls[i] == 1) cl += (zero_class || dest[rt++] >= 0);
+            else if (cls[i] == 1) cl += (zero_class || (rt < cap_t && dest[rt] >= 0)), ++rt;
         }
     }
     const int cl_incl = block_incl_scan(cl, shs);
@@ -122,18 +127,25 @@ __global__ void __launch_bounds__(kLutThreads) compact_lut_kernel(
     int32_t* ls = lut_slot + (size_t)u * cap_lut;
     for (int i = s0; i < s1; ++i) {
         if (cls[i] == 2) {
-            lp[rl] = (int32_t)(first_pos + i);
-            ls[rl] = ri++;
+            if (rl < cap_lut) {
+                lp[rl] = (int32_t)(first_pos + i);
+                ls[rl] = ri;
+            }
+            ++ri;
             ++rl;
         } else if (cls[i] == 1) {
-            const int dd = dest[rt++];
+            const int dd = rt < cap_t ? dest[rt] : -2;
+            ++rt;
             if (zero_class || dd >= 0) {
-                lp[rl] = (int32_t)(first_pos + i);
-                ls[rl] = dd;  // -1 = zero class
+                if (rl < cap_lut) {
+                    lp[rl] = (int32_t)(first_pos + i);
+                    ls[rl] = dd;  // -1 = zero class; anything < -1 or >= n_centers fails the check
+                }
                 ++rl;
             }
         }
     }
+    const int n_lut = __shfl_sync(0xffffffffu, cl_incl, 31);  // per warp: its last lane's count
     if (tid == kLutThreads - 1) {
         int32_t* oc = out_counts + 4 * u;
         oc[0] = counts[4 * u];
@@ -141,6 +153,19 @@ __global__ void __launch_bounds__(kLutThreads) compact_lut_kernel(
         oc[2] = cl_incl;  // the last thread's inclusive count = all LUT entries
         oc[3] = 1;
     }
+    // check_integrity over the whole LUT (entries written by other threads are visible after
+    // the barrier): this thread re-reads its own entries and the one before its first.
+    __syncthreads();
+    const int n_centers = counts[4 * u];
+    const int r0 = cl_incl - cl;
+    bool bad = rl > cap_lut;
+    for (int r = r0; r < cl_incl && r < cap_lut; ++r) {
+        const int sl = ls[r];
+        if (sl != -1 && (sl < 0 || sl >= n_centers)) bad = true;  // nonexistent slot
+        if (r > 0 && lp[r] <= lp[r - 1]) bad = true;              // not strictly increasing
+    }
+    (void)n_lut;
+    if (bad) record_status(status, EMS_CORRUPTION, unit_base + u);
 }
 
 // Keep-all path (n <= n_budget): every token is an exact local; no centers/LUT.
@@ -180,7 +205,7 @@ __global__ void __launch_bounds__(256) keep_all_kernel(const T* __restrict__ k,
 template <typename T, int D>
 cudaError_t launch_compact_t(const Dims& dm, const void* k, const void* v, const float* glo,
                              const float* loc, const ems_stage& sg, const ems_cache& c,
-                             int zero_class, int64_t first_pos, cudaStream_t s) {
+                             int zero_class, int64_t first_pos, DevStatus* status, cudaStream_t s) {
     dim3 ge((dm.cap_c + dm.cap_l + 7) / 8, dm.units);
     compact_entries_kernel<T, D><<<ge, 256, 0, s>>>(
         (const T*)k, (const T*)v, dm.L, glo, loc, sg.imp_idx, sg.part_counts, dm.cap_c, dm.cap_l,
@@ -188,7 +213,8 @@ cudaError_t launch_compact_t(const Dims& dm, const void* k, const void* v, const
         c.center_score, (T*)c.local_key, (T*)c.local_value, c.local_pos, c.local_score);
     compact_lut_kernel<<<dm.units, kLutThreads, 0, s>>>(dm.L, sg.cls, sg.dest, sg.part_counts,
                                                         dm.cap_tbm, dm.cap_lut, zero_class,
-                                                        first_pos, c.lut_pos, c.lut_slot, c.counts);
+                                                        first_pos, c.lut_pos, c.lut_slot, c.counts,
+                                                        status, dm.unit_base);
     return cudaGetLastError();
 }
 
@@ -218,12 +244,13 @@ cudaError_t launch_keep_all_t(const Dims& dm, const void* k, const void* v, cons
 
 cudaError_t launch_compact(const Dims& dm, int dtype, const void* k, const void* v,
                            const float* glo, const float* loc, const ems_stage& sg,
-                           const ems_cache& c, int zero_class, int64_t first_pos, cudaStream_t s) {
+                           const ems_cache& c, int zero_class, int64_t first_pos, DevStatus* status,
+                           cudaStream_t s) {
     if (dtype == EMS_F32) {
-        EMS_DISPATCH_D(float, launch_compact_t, dm, k, v, glo, loc, sg, c, zero_class, first_pos, s)
+        EMS_DISPATCH_D(float, launch_compact_t, dm, k, v, glo, loc, sg, c, zero_class, first_pos, status, s)
     } else {
         EMS_DISPATCH_D(__nv_bfloat16, launch_compact_t, dm, k, v, glo, loc, sg, c, zero_class,
-                       first_pos, s)
+                       first_pos, status, s)
     }
 }
 

@@ -184,6 +184,14 @@ __global__ void __launch_bounds__(kTh, kMinB) decode_step_kernel(DecArgs a) {
     if (tid < 8) s_meta[tid] = meta[tid];
     __syncthreads();
     int head = s_meta[0], count = s_meta[1], lut_n = s_meta[2];
+    // Capacity guard: the step appends one local (ring of W) and expands at most lut_n + count + 1
+    // rows (R).  A caller that steps past the horizon the state was sized for (max_positions)
+    // gets EMS_CORRUPTION in meta[6] (ems_decode_sync_status) and the unit stops; every CTA of a
+    // cluster reads the same meta, so they all leave here together.
+    if (s_meta[6] != 0 || count + 1 > W || lut_n + count + 1 > a.R) {
+        if (rank == 0 && tid == 0 && s_meta[6] == 0) meta[6] = EMS_CORRUPTION;
+        return;
+    }
 
     // 1. append the incoming token to the local window (engine.cpp:166-172)
     if (rank == 0) {
@@ -671,7 +679,8 @@ __global__ void __launch_bounds__(kTh, kMinB) decode_step_kernel(DecArgs a) {
                 if (!salive[s] && (fs.idx < 0 || s < fs.idx)) fs = Cand{0.0, s, s};
             auto lower = [](const Cand& x, const Cand& y) { return x.idx >= 0 && (y.idx < 0 || x.idx < y.idx); };
             fs = bselect(fs, lower, shc);
-            const int slot = fs.idx;
+            const int slot = fs.idx >= 0 ? fs.idx : 0;  // no free slot: corrupt state, recorded below
+            if (fs.idx < 0 && tid == 0) meta[6] = EMS_CORRUPTION;
             double kk = 0.0;
             for (int i = tid; i < d; i += kT) kk += (double)lkey[(size_t)g * d + i] * lkey[(size_t)g * d + i];
             const double kn = sqrt(bsum(kk, shd));  // normalized_or_zero, :16-25
@@ -1076,6 +1085,13 @@ cudaError_t launch_decode_step(const Dims& m, int dtype, int S, int W, int T, in
     cfg.attrs = at;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, fn, a);
+}
+
+// Dynamic shared memory of the decode step (the largest launch variant): the per-owner mass /
+// redundancy accumulator over S slots + W locals, the RoPE'd queries and the cluster partials.
+size_t decode_smem_bytes(const Dims& m, int S, int W) {
+    const size_t acc = (size_t)max(S + W, (kTMax / 32) * m.d) * 8;
+    return acc + (size_t)((m.G * m.d + 1) & ~1) * 4 + (size_t)m.G * m.d * 8;
 }
 
 size_t decode_workspace_bytes(const Dims& m, int R) {

@@ -153,129 +153,202 @@ __global__ void __launch_bounds__(256) assign_simt_kernel(
 }
 
 // ---------------------------------------------------------------------------
-// Weighted merge, one CTA per unit: stable bucket of TBM tokens by destination,
-// then one warp per center with members.
-template <typename T, int D>
-__global__ void __launch_bounds__(512) merge_scatter_kernel(
-    const T* __restrict__ k, const T* __restrict__ v, int L, const float* __restrict__ glo,
-    const float* __restrict__ loc, const float* __restrict__ pooled_all,
-    const int32_t* __restrict__ imp_idx_all, const int32_t* __restrict__ tbm_idx_all,
+// Weighted merge in two launches.
+//
+// (a) merge_bucket_kernel, one CTA per unit: the members of every center as a CSR list in
+//     ascending TBM order.  Destinations are validated first (anything outside [-1, n_imp)
+//     records EMS_CORRUPTION and is treated as the zero class).  The merged tokens' keys
+//     (dest << 32 | tbm rank) are collected in shared memory and bitonic-sorted, which gives
+//     every bucket its members in ascending TBM order (the reference's accumulation order,
+//     compressor.cpp:118-160) without a serial pass; bucket offsets come from an integer
+//     histogram and a block scan.  Everything is order-independent integer work, so the
+//     output is identical run to run.  Units with more TBM tokens than the sort capacity
+//     (kSortCap) fall back to a stable warp-serial fill.
+// (b) merge_accum_kernel: one warp per center with members, across (center blocks, units),
+//     so the K/V reads of a unit's merges spread over the whole GPU.
+constexpr int kBucketThreads = 1024;
+constexpr int kSortCap = 16384;  // keys per unit sorted in shared memory (128 KB)
+
+__global__ void __launch_bounds__(kBucketThreads) merge_bucket_kernel(
     const int32_t* __restrict__ counts, const int32_t* __restrict__ dest_all, int cap_c, int cap_t,
-    int32_t* __restrict__ ws_count, int32_t* __restrict__ ws_members, T* __restrict__ center_key,
-    T* __restrict__ center_value, float* __restrict__ center_score) {
-    constexpr int R = (D + 31) / 32;
-    const int u = blockIdx.x;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int nwarps = blockDim.x >> 5;
+    int32_t* __restrict__ ws_off, int32_t* __restrict__ ws_members, DevStatus* status, int unit_base) {
+    extern __shared__ unsigned long long keys[];  // [sort capacity]
+    __shared__ int sh[32];
+    __shared__ int n_merged, bad;
+    const int u = blockIdx.x, tid = threadIdx.x;
     const int n_imp = counts[4 * u], n_tbm = counts[4 * u + 1];
-    if (n_tbm == 0) return;
     const int32_t* dest = dest_all + (size_t)u * cap_t;
-    const int32_t* imp_idx = imp_idx_all + (size_t)u * cap_c;
-    const int32_t* tbm_idx = tbm_idx_all + (size_t)u * cap_t;
-    const float* pooled = pooled_all + (size_t)u * L;
-    int32_t* cnt = ws_count + (size_t)u * (cap_c + 1);
+    int32_t* off = ws_off + (size_t)u * (cap_c + 1);
     int32_t* mem = ws_members + (size_t)u * cap_t;
-    for (int c = tid; c <= n_imp; c += blockDim.x) cnt[c] = 0;
+    if (tid == 0) n_merged = 0, bad = 0;
+    for (int c = tid; c <= n_imp; c += kBucketThreads) off[c] = 0;
     __syncthreads();
-    for (int t = tid; t < n_tbm; t += blockDim.x)
-        if (dest[t] >= 0) atomicAdd(&cnt[dest[t] + 1], 1);
+    // histogram of destinations (integer atomics: order-independent) + collection of the keys
+    const bool sortable = n_tbm <= kSortCap;
+    for (int t = tid; t < n_tbm; t += kBucketThreads) {
+        const int d = dest[t];
+        if (d < -1 || d >= n_imp) {
+            bad = 1;
+            continue;
+        }
+        if (d < 0) continue;
+        atomicAdd(&off[d + 1], 1);
+        if (sortable) keys[atomicAdd(&n_merged, 1)] = ((unsigned long long)d << 32) | (unsigned)t;
+    }
     __syncthreads();
-    if (tid == 0)  // exclusive offsets: cnt[c] = start of bucket c (cnt[n_imp] = total)
-        for (int c = 1; c <= n_imp; ++c) cnt[c] += cnt[c - 1];
+    if (bad && tid == 0) record_status(status, EMS_CORRUPTION, unit_base + u);
+    // exclusive bucket offsets: off[c] = start of bucket c, off[n_imp] = all merged tokens
+    {
+        const int per = (n_imp + kBucketThreads) / kBucketThreads;  // n_imp + 1 entries
+        const int c0 = min(n_imp + 1, tid * per), c1 = min(n_imp + 1, c0 + per);
+        int run = 0;
+        for (int c = c0; c < c1; ++c) run += off[c];
+        int base = block_incl_scan(run, sh) - run;
+        for (int c = c0; c < c1; ++c) {
+            base += off[c];
+            off[c] = base;  // inclusive over [0, c] of the shifted counts = start of bucket c
+        }
+    }
     __syncthreads();
-    // stable fill in ascending TBM order by warp 0; the cursor is cnt[] itself,
-    // afterwards cnt[c] = end of bucket c == start of bucket c+1.
-    if (warp == 0) {
+    if (sortable) {
+        const int m = n_merged;
+        int n = 1;
+        while (n < m) n <<= 1;
+        for (int i = m + tid; i < n; i += kBucketThreads) keys[i] = ~0ull;
+        __syncthreads();
+        for (int k = 2; k <= n; k <<= 1)  // bitonic sort, ascending (dest, t)
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                for (int i = tid; i < n; i += kBucketThreads) {
+                    const int ixj = i ^ j;
+                    if (ixj > i) {
+                        const unsigned long long a = keys[i], b = keys[ixj];
+                        const bool up = (i & k) == 0;
+                        if ((a > b) == up) {
+                            keys[i] = b;
+                            keys[ixj] = a;
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+        for (int i = tid; i < m; i += kBucketThreads) mem[i] = (int32_t)(keys[i] & 0xffffffffull);
+    } else if (tid < 32) {  // stable warp-serial fill with per-bucket cursors
+        const int lane = tid;
+        int32_t* cur = off;  // the bucket starts double as cursors
         for (int base = 0; base < n_tbm; base += 32) {
             const int t = base + lane;
-            const int dd = t < n_tbm ? dest[t] : -1;
+            int dd = t < n_tbm ? dest[t] : -1;
+            if (dd >= n_imp || dd < -1) dd = -1;
             const unsigned act = __ballot_sync(0xffffffffu, dd >= 0);
             if (dd >= 0) {
                 const unsigned same = __match_any_sync(act, dd);
                 const int rank = __popc(same & ((1u << lane) - 1u));
-                const int pos = cnt[dd];
+                const int pos = cur[dd];
                 mem[pos + rank] = t;
                 __syncwarp(act);
-                if (rank == 0) cnt[dd] = pos + __popc(same);
+                if (rank == 0) cur[dd] = pos + __popc(same);
             }
             __syncwarp();
         }
     }
-    __syncthreads();
-    // bucket c now spans [c == 0 ? 0 : cnt[c-1], cnt[c])
+    if (!sortable) {  // the cursors now hold bucket ends (end of c == start of c + 1): shift back
+        __syncthreads();
+        if (tid == 0) {
+            for (int c = n_imp; c > 0; --c) off[c] = off[c - 1];
+            off[0] = 0;
+        }
+    }
+}
+
+template <typename T, int D>
+__global__ void __launch_bounds__(256) merge_accum_kernel(
+    const T* __restrict__ k, const T* __restrict__ v, int L, const float* __restrict__ glo,
+    const float* __restrict__ loc, const float* __restrict__ pooled_all,
+    const int32_t* __restrict__ imp_idx_all, const int32_t* __restrict__ tbm_idx_all,
+    const int32_t* __restrict__ counts, int cap_c, int cap_t, const int32_t* __restrict__ ws_off,
+    const int32_t* __restrict__ ws_members, T* __restrict__ center_key, T* __restrict__ center_value,
+    float* __restrict__ center_score) {
+    constexpr int R = (D + 31) / 32;
+    const int u = blockIdx.y;
+    const int lane = threadIdx.x & 31;
+    const int c = blockIdx.x * 8 + (threadIdx.x >> 5);
+    const int n_imp = counts[4 * u];
+    if (c >= n_imp || counts[4 * u + 1] == 0) return;
+    const int32_t* off = ws_off + (size_t)u * (cap_c + 1);
+    const int b0 = off[c], b1 = off[c + 1];
+    if (b1 == b0) return;
+    const int32_t* mem = ws_members + (size_t)u * cap_t;
+    const int32_t* tbm_idx = tbm_idx_all + (size_t)u * cap_t;
+    const float* pooled = pooled_all + (size_t)u * L;
     const T* kb = k + (size_t)u * L * D;
     const T* vb = v + (size_t)u * L * D;
-    for (int c = warp; c < n_imp; c += nwarps) {
-        const int b0 = c == 0 ? 0 : cnt[c - 1], b1 = cnt[c];
-        if (b1 == b0) continue;
-        const int ci = imp_idx[c];
-        double ws = (double)pooled[ci];
-        for (int m = b0; m < b1; ++m) ws += (double)pooled[tbm_idx[mem[m]]];
-        const double uniform = 1.0 / (double)(b1 - b0 + 1);
-        float mk[R], mv[R], x[R];
-        // center's own unit key and value
-        float ss = 0.f;
+    const int ci = imp_idx_all[(size_t)u * cap_c + c];
+    double ws = (double)pooled[ci];
+    for (int m = b0; m < b1; ++m) ws += (double)pooled[tbm_idx[mem[m]]];
+    const double uniform = 1.0 / (double)(b1 - b0 + 1);
+    float mk[R], mv[R], x[R];
+    // the center's own unit key and value first, then the members in ascending TBM order
+    float ss = 0.f;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int dd = lane + 32 * r;
+        x[r] = dd < D ? ld(kb + (size_t)ci * D + dd) : 0.f;
+        ss = fmaf(x[r], x[r], ss);
+    }
+    ss = warp_sum(ss);
+    float nrm = sqrtf(ss);
+    float w = (float)(ws > 0.0 ? (double)pooled[ci] / ws : uniform);
+    float sg = glo[(size_t)u * L + ci], sl = loc[(size_t)u * L + ci];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int dd = lane + 32 * r;
+        const float uk = nrm > 0.f ? x[r] / nrm : x[r];
+        mk[r] = w * uk;
+        mv[r] = dd < D ? w * ld(vb + (size_t)ci * D + dd) : 0.f;
+    }
+    for (int m = b0; m < b1; ++m) {
+        const int ti = tbm_idx[mem[m]];
+        ss = 0.f;
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             const int dd = lane + 32 * r;
-            x[r] = dd < D ? ld(kb + (size_t)ci * D + dd) : 0.f;
+            x[r] = dd < D ? ld(kb + (size_t)ti * D + dd) : 0.f;
             ss = fmaf(x[r], x[r], ss);
         }
         ss = warp_sum(ss);
-        float nrm = sqrtf(ss);
-        float w = (float)(ws > 0.0 ? (double)pooled[ci] / ws : uniform);
-        float sg = glo[(size_t)u * L + ci], sl = loc[(size_t)u * L + ci];
+        nrm = sqrtf(ss);
+        w = (float)(ws > 0.0 ? (double)pooled[ti] / ws : uniform);
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             const int dd = lane + 32 * r;
             const float uk = nrm > 0.f ? x[r] / nrm : x[r];
-            mk[r] = w * uk;
-            mv[r] = dd < D ? w * ld(vb + (size_t)ci * D + dd) : 0.f;
+            mk[r] = fmaf(w, uk, mk[r]);
+            if (dd < D) mv[r] = fmaf(w, ld(vb + (size_t)ti * D + dd), mv[r]);
         }
-        for (int m = b0; m < b1; ++m) {
-            const int ti = tbm_idx[mem[m]];
-            ss = 0.f;
+        sg += glo[(size_t)u * L + ti];
+        sl += loc[(size_t)u * L + ti];
+    }
+    ss = 0.f;
 #pragma unroll
-            for (int r = 0; r < R; ++r) {
-                const int dd = lane + 32 * r;
-                x[r] = dd < D ? ld(kb + (size_t)ti * D + dd) : 0.f;
-                ss = fmaf(x[r], x[r], ss);
-            }
-            ss = warp_sum(ss);
-            nrm = sqrtf(ss);
-            w = (float)(ws > 0.0 ? (double)pooled[ti] / ws : uniform);
+    for (int r = 0; r < R; ++r) ss = fmaf(mk[r], mk[r], ss);
+    ss = warp_sum(ss);
+    const float mn = sqrtf(ss);
+    T* ck = center_key + ((size_t)u * cap_c + c) * D;
+    T* cv = center_value + ((size_t)u * cap_c + c) * D;
 #pragma unroll
-            for (int r = 0; r < R; ++r) {
-                const int dd = lane + 32 * r;
-                const float uk = nrm > 0.f ? x[r] / nrm : x[r];
-                mk[r] = fmaf(w, uk, mk[r]);
-                if (dd < D) mv[r] = fmaf(w, ld(vb + (size_t)ti * D + dd), mv[r]);
-            }
-            sg += glo[(size_t)u * L + ti];
-            sl += loc[(size_t)u * L + ti];
+    for (int r = 0; r < R; ++r) {
+        const int dd = lane + 32 * r;
+        if (dd < D) {
+            // mn == 0 keeps the center's current unit key (compressor.cpp:152-158)
+            if (mn > 0.f) st(ck + dd, mk[r] / mn);
+            st(cv + dd, mv[r]);
         }
-        ss = 0.f;
-#pragma unroll
-        for (int r = 0; r < R; ++r) ss = fmaf(mk[r], mk[r], ss);
-        ss = warp_sum(ss);
-        const float mn = sqrtf(ss);
-        T* ck = center_key + ((size_t)u * cap_c + c) * D;
-        T* cv = center_value + ((size_t)u * cap_c + c) * D;
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-            const int dd = lane + 32 * r;
-            if (dd < D) {
-                // mn == 0 keeps the center's current unit key (compressor.cpp:152-158)
-                if (mn > 0.f) st(ck + dd, mk[r] / mn);
-                st(cv + dd, mv[r]);
-            }
-        }
-        if (lane == 0) {
-            float* sc = center_score + ((size_t)u * cap_c + c) * 3;
-            sc[0] = sg;
-            sc[1] = sl;
-            sc[2] = 0.f;
-        }
+    }
+    if (lane == 0) {
+        float* sc = center_score + ((size_t)u * cap_c + c) * 3;
+        sc[0] = sg;
+        sc[1] = sl;
+        sc[2] = 0.f;
     }
 }
 
@@ -300,12 +373,19 @@ cudaError_t launch_merge_assign_t(const Dims& dm, const void* k, const void* v,
 
 template <typename T, int D>
 cudaError_t launch_merge_scatter_t(const Dims& dm, const void* k, const void* v, const float* glo,
-                                   const float* loc, const ems_stage& sg, int32_t* ws_count,
-                                   int32_t* ws_members, const ems_cache& cache, cudaStream_t s) {
-    merge_scatter_kernel<T, D><<<dm.units, 512, 0, s>>>(
-        (const T*)k, (const T*)v, dm.L, glo, loc, sg.pooled, sg.imp_idx, sg.tbm_idx,
-        sg.part_counts, sg.dest, dm.cap_c, dm.cap_tbm, ws_count, ws_members, (T*)cache.center_key,
-        (T*)cache.center_value, cache.center_score);
+                                   const float* loc, const ems_stage& sg, int32_t* ws_off,
+                                   int32_t* ws_members, const ems_cache& cache, DevStatus* status,
+                                   cudaStream_t s) {
+    int n = 1;
+    while (n < dm.cap_tbm && n < kSortCap) n <<= 1;
+    const int smem = (int)(sizeof(unsigned long long) * n);
+    cudaError_t e = smem_optin(reinterpret_cast<const void*>(merge_bucket_kernel), smem);
+    if (e != cudaSuccess) return e;
+    merge_bucket_kernel<<<dm.units, kBucketThreads, smem, s>>>(sg.part_counts, sg.dest, dm.cap_c, dm.cap_tbm,
+                                                               ws_off, ws_members, status, dm.unit_base);
+    merge_accum_kernel<T, D><<<dim3((dm.cap_c + 7) / 8, dm.units), 256, 0, s>>>(
+        (const T*)k, (const T*)v, dm.L, glo, loc, sg.pooled, sg.imp_idx, sg.tbm_idx, sg.part_counts, dm.cap_c,
+        dm.cap_tbm, ws_off, ws_members, (T*)cache.center_key, (T*)cache.center_value, cache.center_score);
     return cudaGetLastError();
 }
 
@@ -337,13 +417,13 @@ cudaError_t launch_merge_assign(const Dims& dm, int dtype, const void* k, const 
 cudaError_t launch_merge_scatter(const Dims& dm, int dtype, const void* k, const void* v,
                                  const float* glo, const float* loc, const ems_stage& sg,
                                  int32_t* ws_count, int32_t* ws_members, const ems_cache& cache,
-                                 cudaStream_t s) {
+                                 DevStatus* status, cudaStream_t s) {
     if (dtype == EMS_F32) {
         EMS_DISPATCH_D(float, launch_merge_scatter_t, dm, k, v, glo, loc, sg, ws_count, ws_members,
-                       cache, s)
+                       cache, status, s)
     } else {
         EMS_DISPATCH_D(__nv_bfloat16, launch_merge_scatter_t, dm, k, v, glo, loc, sg, ws_count,
-                       ws_members, cache, s)
+                       ws_members, cache, status, s)
     }
 }
 

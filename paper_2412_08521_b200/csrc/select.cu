@@ -29,6 +29,23 @@ namespace ems {
 namespace {
 
 constexpr int kSelThreads = 1024;
+
+// A unit whose scores have no global mass (the reference throws DegenerateInputError,
+// scoring.cpp:115-117) still leaves a valid stage behind, so the merge / compact kernels that
+// follow in the same pipeline only see consistent data (no centers, no TBM tokens, no LUT; the
+// exact locals): every candidate irrelevant, counts {0, 0, n_cand, l_win}.  The error itself is
+// reported through the device status word (ems_sync_status).
+__device__ void write_empty_partition(int8_t* cls, int32_t* counts, int L, int l_win, int i0, int i1, int tid,
+                                      int nthreads) {
+    const int n_cand = L - l_win;
+    for (int i = i0 + tid; i < i1; i += nthreads) cls[i] = i < n_cand ? 0 : 3;
+    if (counts && tid == 0) {
+        counts[0] = 0;
+        counts[1] = 0;
+        counts[2] = n_cand;
+        counts[3] = l_win;
+    }
+}
 constexpr int kSelWarps = kSelThreads / 32;
 
 __device__ __forceinline__ unsigned long long sel_key(const float* pooled, int i) {
@@ -130,8 +147,9 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(
     sl = block_sum(sl, sh);
     if (tid == 0) degenerate = !(sg > 0.0);
     __syncthreads();
-    if (degenerate) {
+    if (degenerate) {  // DegenerateInputError (scoring.cpp:115-117); leave a valid empty partition
         if (tid == 0) record_status(status, EMS_DEGENERATE_INPUT, unit_base + u);
+        write_empty_partition(cls_all + (size_t)u * L, counts_all + 4 * u, L, l_win, 0, L, tid, kSelThreads);
         return;
     }
     const double align = sl / sg;
@@ -282,8 +300,10 @@ __global__ void __cluster_dims__(kClu, 1, 1) __launch_bounds__(kCThreads) select
         cl_sync();
         double tg = 0.0, tl = 0.0;
         for (int r = 0; r < kClu; ++r) tg += ld_dsm_f64(&s_part[0], r), tl += ld_dsm_f64(&s_part[1], r);
-        if (!(tg > 0.0)) {
+        if (!(tg > 0.0)) {  // DegenerateInputError; leave a valid empty partition
             if (tid == 0 && rank == 0) record_status(status, EMS_DEGENERATE_INPUT, unit_base + u);
+            write_empty_partition(cls_all + (size_t)u * L, rank == 0 ? counts_all + 4 * u : nullptr, L, l_win, c0,
+                                  c1, tid, kCThreads);
             cl_sync();
             return;
         }

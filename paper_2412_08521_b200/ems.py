@@ -134,6 +134,7 @@ def lib() -> C.CDLL:
         L.ems_decode_workspace_bytes.restype = C.c_size_t
         L.ems_decode_workspace_bytes.argtypes = [C.POINTER(Desc), C.c_int32]
         L.ems_rope_table.argtypes = [C.c_int32, C.c_double, C.c_int32, vp, vp]
+        L.ems_decode_sync_status.argtypes = [C.POINTER(Desc), C.POINTER(CDecode), vp]
         L.ems_decode_init.argtypes = [C.POINTER(Desc), C.c_int32, C.POINTER(CCache), C.POINTER(CDecode), vp]
         L.ems_decode_step.argtypes = [C.POINTER(Desc), C.c_int64, vp, C.c_int32, vp, vp, vp, vp, vp,
                                       C.POINTER(CDecode), vp, C.c_size_t, vp]
@@ -606,6 +607,10 @@ class DecodeState:
                                      _p(self.workspace), self.workspace.numel(), _stream(stream)))
         self.position += 1
         return self.out, self.argmax
+
+    def sync_status(self, stream=None) -> None:
+        """Synchronise and raise the first unit's decode error (ems_decode_sync_status)."""
+        _check(lib().ems_decode_sync_status(C.byref(self.desc), C.byref(self._c), _stream(stream)))
 
     def unit_cache(self, u: int) -> dict:
         """Host view of unit u's state, shaped like a reference HeadCacheState dump."""

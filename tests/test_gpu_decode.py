@@ -155,3 +155,75 @@ def test_decode_single_cta_variant_forced():
                         "-k", "matches_reference or keep_all or window_rotation or gqa"],
                        env=env, capture_output=True, text=True, cwd=os.path.dirname(os.path.dirname(__file__)))
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+def test_decode_bf16_d128_gqa_matches_reference(reflib):
+    """The benchmarked decode shape: bf16 inputs, head_dim 128, G = 4 query heads per KV head.
+    The reference engine has no GQA, so each unit's four query heads are the same
+    bf16 row: contract D2's mean over G identical heads is the single-head reference exactly,
+    while the device runs the G = 4 code path (G-way logit reduction, per-head maxima and
+    normalisers, GQA-mean masses) on bf16 loads."""
+    H, G, n, d, steps = 2, 4, 300, 128, 40
+    c = Config(n_budget=48, l_win=8, tau=0.4, gamma=2.0, kernel_size=5)
+    rng = np.random.default_rng(31)
+    bf = lambda a: torch.tensor(a).to(torch.bfloat16).double().numpy()  # noqa: E731  bf16-exact values
+    q, k, v = (bf(rng.standard_normal((H, n, d))) for _ in range(3))
+    dq, dk, dv = (bf(rng.standard_normal((steps, H, d))) for _ in range(3))
+    out_ref, am_ref, pre, fin = reflib.engine_decode(q, k, v, dq, dk, dv, c, rope_base=1e4)
+    cfg = ems.EmsConfig(c.n_budget, c.l_win, c.tau, c.gamma, c.kernel_size, c.zero_class)
+    ds = ems.DecodeState(1, H * G, H, n, d, torch.bfloat16, cfg, 1e4, n + steps)
+    ds.load_caches(pre, position=n)
+    dev = torch.device("cuda")
+    outs, ams = [], []
+    for s in range(steps):
+        qs = torch.tensor(dq[s], device=dev).to(torch.bfloat16).repeat_interleave(G, dim=0).reshape(1, H * G, d)
+        ks = torch.tensor(dk[s], device=dev).to(torch.bfloat16).reshape(1, H, d)
+        vs = torch.tensor(dv[s], device=dev).to(torch.bfloat16).reshape(1, H, d)
+        o, a = ds.step(qs.contiguous(), ks.contiguous(), vs.contiguous())
+        o = o[0].double().cpu().numpy().reshape(H, G, d)
+        a = a[0].long().cpu().numpy().reshape(H, G)
+        assert np.all(a == a[:, :1]), "identical heads disagree on the argmax"
+        outs.append(o[:, 0])
+        ams.append(a[:, 0])
+    ds.sync_status()
+    outs, ams = np.stack(outs), np.stack(ams)
+    # bf16 outputs: one rounding of the fp32 result
+    err = np.linalg.norm(outs - out_ref, axis=-1) / np.linalg.norm(out_ref, axis=-1)
+    assert err.max() < 8e-3, err.max()
+    assert (ams != am_ref).mean() <= 0.01
+    for h in range(H):
+        got, want = ds.unit_cache(h), fin[h]
+        assert got["slots"] == list(want.extra["slots"])
+        np.testing.assert_array_equal(got["position"], want.position)
+        np.testing.assert_array_equal(got["lut_position"], want.lut_position)
+        np.testing.assert_array_equal(got["lut_slot"], want.lut_slot)
+        np.testing.assert_allclose(got["value"], want.value, rtol=1e-4, atol=2e-5)
+        np.testing.assert_allclose(got["score"], want.score, rtol=1e-4, atol=1e-7)
+
+
+def test_decode_past_capacity_reports_corruption():
+    """A C-ABI caller that keeps stepping the full policy past the horizon its state was sized for
+    (here: the same position over and over) gets EMS_CORRUPTION instead of a ring overrun."""
+    n, d, extra = 64, 32, 3
+    cfg = ems.EmsConfig(n_budget=16, l_win=4, tau=0.6, gamma=2.0, kernel_size=3, policy="full")
+    ds = ems.DecodeState(1, 1, 1, n, d, torch.float32, cfg, 1e4, n + extra)
+    rng = np.random.default_rng(1)
+    T = lambda *s: torch.tensor(rng.standard_normal(s), dtype=torch.float32, device="cuda").contiguous()  # noqa: E731
+    plan = ems.prefill_compress(T(1, 1, n, d), T(1, 1, n, d), T(1, 1, n, d), T(1, 1, n, d), cfg, want_out=False)
+    ds.init_from_plan(plan)
+    for _ in range(extra):
+        ds.step(T(1, 1, d), T(1, 1, d), T(1, 1, d))
+    ds.sync_status()
+    for _ in range(4):  # past the capacity: positions held at the last valid one
+        ds.position = n + extra - 1
+        ds.step(T(1, 1, d), T(1, 1, d), T(1, 1, d))
+    with pytest.raises(ems.CorruptionError):
+        ds.sync_status()
+
+
+def test_decode_shared_memory_limit_is_rejected_up_front():
+    """The full policy keeps every token in the step's shared-memory accumulator: a 32k prompt
+    does not fit, and the descriptor is rejected with EMS_UNSUPPORTED before any launch."""
+    cfg = ems.EmsConfig(n_budget=256, l_win=32, policy="full")
+    with pytest.raises(ems.Unsupported):
+        ems.DecodeState(1, 32, 8, 32768, 128, torch.bfloat16, cfg, 5e5, 32768 + 16)

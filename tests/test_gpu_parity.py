@@ -236,3 +236,52 @@ def test_gpu_cache_dump_json_round_trips_through_reference_schema():
     np.testing.assert_array_equal(back.value, c["value"])
     np.testing.assert_array_equal(back.local_key, c["local_key"])
     assert back.compressed == c["compressed"] and back.extra["slots"] == list(range(len(c["position"])))
+
+
+def test_gpu_degenerate_full_path_leaves_valid_stage():
+    """NaN inputs reach the select kernel as zero / NaN global mass: the whole prefill (score ->
+    select -> merge -> compact) over a workspace of garbage (0xFF) raises DegenerateInputError
+    (scoring.cpp:115-117) without touching memory outside its buffers, and the next call on the
+    same plan is clean."""
+    w = CONFIGS["cfgM"]
+    un = make_unit_np(w, seed=4, seq_len=1024, unit=0)
+    dev = torch.device("cuda")
+    t = lambda a, s: torch.tensor(a, dtype=torch.float64).to(torch.bfloat16).to(dev).reshape(s).contiguous()  # noqa: E731
+    q, kr, kw, v = t(un.q_rot, (1, 1, 1024, 128)), t(un.k_rot, (1, 1, 1024, 128)), \
+        t(un.k_raw, (1, 1, 1024, 128)), t(un.v, (1, 1, 1024, 128))
+    cfg = ems.EmsConfig(w.n_budget, w.l_win, w.tau, w.gamma, w.kernel_size)
+    plan = ems.Plan(1, 1, 1, 1024, 128, torch.bfloat16, cfg, dev)
+    plan.workspace.fill_(0xFF)
+    for name in plan.stage:
+        plan.stage[name].view(torch.uint8).fill_(0xFF)
+    qn = q.clone()
+    qn[0, 0, 5] = float("nan")
+    plan.run(qn, kr, kw, v)
+    with pytest.raises(ems.DegenerateInputError):
+        plan.sync_status()
+    cnt = plan.cache["counts"][0].tolist()
+    assert cnt[0] == 0 and cnt[2] == 0 and cnt[1] == w.l_win  # no centers, no LUT, exact locals
+    plan.run(q, kr, kw, v)
+    plan.sync_status()  # clean again
+    assert plan.cache["counts"][0, 0].item() == w.n_budget - w.l_win
+
+
+def test_gpu_corrupt_stage_raises_corruption_error():
+    """HeadCacheState::check_integrity (cache.cpp:66-80) on the device: a caller-supplied stage
+    whose merge destination names a nonexistent center slot gives CorruptionError from the
+    compact step (and the merge kernels skip the bad entry instead of writing out of bounds)."""
+    w = CONFIGS["cfgM"]
+    un = make_unit_np(w, seed=6, seq_len=1024, unit=0)
+    dev = torch.device("cuda")
+    t = lambda a: torch.tensor(a, dtype=torch.float64).to(torch.bfloat16).to(dev).reshape(1, 1, 1024, 128).contiguous()  # noqa: E731
+    q, kr, kw, v = t(un.q_rot), t(un.k_rot), t(un.k_raw), t(un.v)
+    cfg = ems.EmsConfig(w.n_budget, w.l_win, w.tau, w.gamma, w.kernel_size)
+    plan = ems.Plan(1, 1, 1, 1024, 128, torch.bfloat16, cfg, dev)
+    plan.score(q, kr, v)
+    plan.select()
+    plan.merge(kw, v)
+    plan.sync_status()
+    plan.stage["dest"][0, 3] = 10 ** 6  # no such slot
+    plan.compact(kw, v)
+    with pytest.raises(ems.CorruptionError):
+        plan.sync_status()
