@@ -6,8 +6,10 @@
  * functions on fp64 per-head matrices; here they are batched, stream-ordered,
  * device-pointer entry points over contiguous [B][H][L][d] tensors, so each
  * (b, h) slice is byte-for-byte a reference `Matrix` (proj/include/ems/types.hpp:13-34)
- * in fp32 or bf16.  include/ems_b200/ems.hpp restores the reference's exact
- * C++ signatures on top of this ABI; INTEGRATION.md shows the bindings.
+ * in fp32 or bf16.  include/ems_b200/ems.hpp restores the reference's C++
+ * signatures (same names, argument order and exceptions, plus a trailing dtype
+ * argument where the device precision is selectable) on top of this ABI;
+ * INTEGRATION.md shows the bindings.
  *
  *   reference entry point (file:line)                          replaced by
  *   ---------------------------------------------------------  -------------------------
@@ -16,10 +18,12 @@
  *   global/local_score_prefill  scoring.hpp:40-45               ems_score
  *   combine_glo_loc + effective_score  scoring.hpp:58,66        ems_select (prologue)
  *   init_score_state    scoring.hpp:70                          implicit: loc -> loc_past
- *   partition_tokens    proj/include/ems/compressor.hpp:14-25   ems_select
+ *   effective_score     scoring.hpp:66                          ems_effective_score
+ *   partition_tokens    proj/include/ems/compressor.hpp:14-25   ems_select (fused) / ems_partition
  *   redundancy_cross    proj/include/ems/analysis.hpp:19-20     ems_redundancy_cross / ems_merge
- *   assign_merge_destinations  compressor.hpp:29               ems_merge
- *   weighted_merge      compressor.hpp:32-51                    ems_compact (merge epilogue)
+ *   assign_merge_destinations  compressor.hpp:29               ems_merge (fused) /
+ *                                                              ems_assign_merge_destinations
+ *   weighted_merge      compressor.hpp:32-51                    ems_compact (fused) / ems_weighted_merge
  *   compress_prefill    compressor.hpp:58-60                    ems_select+ems_merge+ems_compact
  *   engine prefill (score -> compress)  proj/src/engine.cpp:42-82  ems_prefill_compress
  *   engine prefill incl. RoPE           proj/src/engine.cpp:42-82  ems_prefill (raw Q/K)
@@ -174,6 +178,39 @@ EMS_API int ems_score(const ems_desc* desc, const void* q_rot, const void* k_rot
 /* (2) Select: align + combine + pool + radix top-k + classify + index lists. */
 EMS_API int ems_select(const ems_desc* desc, const float* glo, const float* loc, const ems_stage* stage,
                void* workspace, size_t workspace_bytes, cudaStream_t stream);
+
+/* partition_tokens (proj/include/ems/compressor.hpp:25, compressor.cpp:48-74) on CALLER pooled
+ * scores: pooled [units][L] fp32 -> the stage's class bytes, ascending important / TBM index
+ * lists and counts (stage->pooled receives a copy).  The (score desc, index asc) order of the
+ * reference's stable sort is exact; ties are decided on the fp32 values.  Needs L > l_win. */
+EMS_API int ems_partition(const ems_desc* desc, const float* pooled, const ems_stage* stage, void* workspace,
+                          size_t workspace_bytes, cudaStream_t stream);
+
+/* effective_score (proj/include/ems/scoring.hpp:66, scoring.cpp:146-152): mean_pool_1d(
+ * combine_glo_loc(glo, loc_past + loc_cur), kernel) for `units` rows of length L (loc_cur may be
+ * NULL = zeros), fp64 arithmetic on fp32 scores.  kernel odd and <= L (numerics.cpp:63-68).
+ * Zero global mass -> EMS_DEGENERATE_INPUT via ems_sync_status(NULL, workspace, stream);
+ * workspace >= 16 bytes. */
+EMS_API int ems_effective_score(int32_t units, int32_t L, int32_t kernel, const float* glo, const float* loc_past,
+                                const float* loc_cur, float* pooled, void* workspace, size_t workspace_bytes,
+                                cudaStream_t stream);
+
+/* assign_merge_destinations (compressor.hpp:29, compressor.cpp:76-95): per row of r [n_rows][n_cols]
+ * (fp32) the argmax column (strictly greater wins, so ties go to the lower column) when it reaches
+ * tau, else -1 (kZeroClass) -> dest [n_rows]. */
+EMS_API int ems_assign_merge_destinations(int32_t n_rows, int32_t n_cols, const float* r, double tau,
+                                          int32_t* dest, cudaStream_t stream);
+
+/* weighted_merge (compressor.hpp:46-51, compressor.cpp:97-161) on fp64 device arrays: center
+ * column c (unit key [d], value [d], score triple, weight) absorbs the TBM rows i with dest[i] == c
+ * in ascending i: ws = w_c + sum w_i; key <- normalize((w_c/ws) u_c + sum (w_i/ws) k_i/|k_i|)
+ * (unchanged when that is zero), value <- (w_c/ws) v_c + sum (w_i/ws) v_i, score += member
+ * triples; uniform weights when ws <= 0.  Columns without members are untouched.  The LUT
+ * entries are the caller's (include/ems_b200/ems.hpp appends them as the reference does). */
+EMS_API int ems_weighted_merge(int32_t d, int32_t n_cols, double* center_unit_key, double* center_value,
+                               double* center_score, const double* center_weight, int32_t n_tbm,
+                               const double* tbm_key, const double* tbm_value, const double* tbm_weight,
+                               const double* tbm_score, const int32_t* dest, cudaStream_t stream);
 
 /* (3) Merge assignment: R = cos_k*cos_v (TBM x centers) on raw K/V, argmax with
  * ties to the lower column, tau threshold -> stage->dest. */

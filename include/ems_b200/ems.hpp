@@ -89,6 +89,7 @@ struct HeadCacheState {  // proj/include/ems/cache.hpp:81-111 (prefill subset)
     std::deque<LocalEntry> locals;
     std::vector<LutEntry> lut;
     bool compressed = false;
+    std::size_t window_fill = 0;
 };
 struct ScoreState {  // proj/include/ems/scoring.hpp:13-24
     Vector glo, loc_past, loc_cur;
@@ -116,6 +117,10 @@ class CorruptionError : public std::runtime_error {
    public:
     explicit CorruptionError(const std::string& w) : std::runtime_error(w) {}
 };
+class StateError : public std::runtime_error {  // proj/include/ems/errors.hpp
+   public:
+    explicit StateError(const std::string& w) : std::runtime_error(w) {}
+};
 class CudaError : public std::runtime_error {
    public:
     explicit CudaError(const std::string& w) : std::runtime_error(w) {}
@@ -130,6 +135,7 @@ inline void check(int status) {
         case EMS_INVALID_ARGUMENT: throw std::invalid_argument(msg);
         case EMS_DEGENERATE_INPUT: throw DegenerateInputError(msg);
         case EMS_CORRUPTION: throw CorruptionError(msg);
+        case EMS_UNSUPPORTED: throw std::invalid_argument(msg);
         default: throw CudaError(msg);
     }
 }
@@ -326,11 +332,13 @@ struct CompressResult {
 // compress_prefill on device for one KV head with externally supplied scores.
 inline CompressResult compress_device(const Matrix& k_raw, const Matrix& v_raw, const Vector& glo,
                                       const Vector& loc, const CompressionConfig& c, int dtype,
-                                      int policy = EMS_POLICY_EMS, std::size_t sink_count = 4) {
+                                      int policy = EMS_POLICY_EMS, std::size_t sink_count = 4,
+                                      std::int64_t first_position = 0) {
     const std::size_t n = k_raw.rows, d = k_raw.cols;
     if (n == 0 || v_raw.rows != n || glo.size() != n || loc.size() != n)
         throw std::invalid_argument("compress_prefill: inconsistent token counts");
     ems_desc desc = make_desc(1, 1, n, d, dtype, c);
+    desc.first_position = first_position;
     desc.policy = policy;
     desc.sink_count = static_cast<int32_t>(sink_count);
     check(ems_validate(&desc));
@@ -396,14 +404,152 @@ inline CompressResult compress_device(const Matrix& k_raw, const Matrix& v_raw, 
 
 }  // namespace detail
 
-// compress_prefill, proj/include/ems/compressor.hpp:58-60 (first_position = 0).
+// compress_prefill, proj/include/ems/compressor.hpp:58-60: token i has logical position
+// first_position + i.  dtype (trailing, not in the reference) selects the device precision of K/V.
 inline HeadCacheState compress_prefill(const Matrix& k_raw, const Matrix& v_raw,
                                        const ScoreState& scores, const CompressionConfig& config,
-                                       int dtype = EMS_F32) {
+                                       std::int64_t first_position = 0, int dtype = EMS_F32) {
     Vector loc(scores.size());
     for (std::size_t i = 0; i < loc.size(); ++i)
         loc[i] = scores.loc_past[i] + (scores.loc_cur.empty() ? 0.0 : scores.loc_cur[i]);
-    return detail::compress_device(k_raw, v_raw, scores.glo, loc, config, dtype).cache;
+    return detail::compress_device(k_raw, v_raw, scores.glo, loc, config, dtype, EMS_POLICY_EMS, 4, first_position)
+        .cache;
+}
+
+// effective_score, proj/include/ems/scoring.hpp:66 (scoring.cpp:146-152): mean_pool_1d(
+// combine_glo_loc(glo, loc_past + loc_cur), kernel_size) on the device (fp32 scores, D9).
+inline Vector effective_score(const ScoreState& state, std::size_t kernel_size) {
+    const std::size_t n = state.size();
+    if (state.loc_past.size() != n || (!state.loc_cur.empty() && state.loc_cur.size() != n))
+        throw std::invalid_argument("combine_glo_loc: length mismatch");
+    if (kernel_size % 2 == 0 || kernel_size == 0) throw std::invalid_argument("mean_pool_1d: kernel_size must be odd");
+    if (kernel_size > n) throw std::invalid_argument("mean_pool_1d: kernel_size exceeds input length");
+    std::vector<float> g(state.glo.begin(), state.glo.end()), lp(state.loc_past.begin(), state.loc_past.end());
+    std::vector<float> lc(state.loc_cur.begin(), state.loc_cur.end());
+    detail::DevBuf dg(n * 4), dlp(n * 4), dlc(lc.empty() ? 0 : n * 4), out(n * 4), ws(256);
+    detail::cuda(cudaMemcpy(dg.p, g.data(), n * 4, cudaMemcpyHostToDevice));
+    detail::cuda(cudaMemcpy(dlp.p, lp.data(), n * 4, cudaMemcpyHostToDevice));
+    if (!lc.empty()) detail::cuda(cudaMemcpy(dlc.p, lc.data(), n * 4, cudaMemcpyHostToDevice));
+    detail::check(ems_effective_score(1, static_cast<int32_t>(n), static_cast<int32_t>(kernel_size), dg.as<float>(),
+                                      dlp.as<float>(), lc.empty() ? nullptr : dlc.as<float>(), out.as<float>(), ws.p,
+                                      ws.n, nullptr));
+    detail::check(ems_sync_status(nullptr, ws.p, nullptr));
+    const auto h = detail::download_raw<float>(out.p, n);
+    return Vector(h.begin(), h.end());
+}
+
+// partition_tokens, proj/include/ems/compressor.hpp:25 (compressor.cpp:48-74), on the device
+// select kernels: (score desc, index asc) decided on the fp32 values of pooled_score.
+inline TokenPartition partition_tokens(const Vector& pooled_score, const CompressionConfig& config) {
+    const std::size_t n = pooled_score.size();
+    if (n < config.l_win + 1) throw std::invalid_argument("partition_tokens: need more tokens than the local window");
+    ems_desc desc = detail::make_desc(1, 1, n, 1, EMS_F32, config);
+    desc.head_dim = 8;  // unused by the partition; any supported head_dim
+    detail::check(ems_validate(&desc));
+    ems_cache_dims dims{};
+    detail::check(ems_cache_dims_for(&desc, &dims));
+    const std::size_t C = std::max(dims.centers, 1), T = std::max(dims.tbm, 1);
+    std::vector<float> h(pooled_score.begin(), pooled_score.end());
+    detail::DevBuf dp(n * 4), pooled(n * 4), cls(n), imp(C * 4), tbm(T * 4), pc(16), dest(T * 4);
+    detail::cuda(cudaMemcpy(dp.p, h.data(), n * 4, cudaMemcpyHostToDevice));
+    ems_stage stage{pooled.as<float>(), cls.as<int8_t>(), imp.as<int32_t>(), tbm.as<int32_t>(), pc.as<int32_t>(),
+                    dest.as<int32_t>()};
+    detail::DevBuf ws(ems_workspace_bytes(&desc));
+    detail::check(ems_partition(&desc, dp.as<float>(), &stage, ws.p, ws.n, nullptr));
+    detail::check(ems_sync_status(&desc, ws.p, nullptr));
+    const auto c = detail::download_raw<int8_t>(cls.p, n);
+    TokenPartition p;
+    for (std::size_t i = 0; i < n; ++i) {
+        if (c[i] == 2) p.important.push_back(i);
+        else if (c[i] == 1) p.tbm.push_back(i);
+        else if (c[i] == 0) p.irrelevant.push_back(i);
+        else p.local.push_back(i);
+    }
+    return p;
+}
+
+// assign_merge_destinations, proj/include/ems/compressor.hpp:29 (compressor.cpp:76-95).
+inline std::vector<std::int32_t> assign_merge_destinations(const Matrix& r_tbm_to_centers, double tau) {
+    const std::size_t R = r_tbm_to_centers.rows, C = r_tbm_to_centers.cols;
+    std::vector<std::int32_t> dest(R, kZeroClass);
+    if (R == 0 || C == 0) return dest;
+    std::vector<float> h(r_tbm_to_centers.data.begin(), r_tbm_to_centers.data.end());
+    detail::DevBuf dr(h.size() * 4), dd(R * 4);
+    detail::cuda(cudaMemcpy(dr.p, h.data(), h.size() * 4, cudaMemcpyHostToDevice));
+    detail::check(ems_assign_merge_destinations(static_cast<int32_t>(R), static_cast<int32_t>(C), dr.as<float>(), tau,
+                                                dd.as<int32_t>(), nullptr));
+    return detail::download_raw<int32_t>(dd.p, R);
+}
+
+// TbmTokens + weighted_merge, proj/include/ems/compressor.hpp:32-51 (compressor.cpp:97-161): the
+// merge arithmetic in fp64 on the device (ems_weighted_merge); the LUT entries are appended here in
+// the reference's order (zero-class rows first, in row order, only in zero_class mode; then each
+// column's members in row order).
+struct TbmTokens {
+    Matrix k_raw;
+    Matrix v_raw;
+    std::vector<std::int64_t> positions;
+    Vector weights;
+    std::vector<ScoreTriple> score_triples;
+};
+inline void weighted_merge(HeadCacheState& cache, const std::vector<std::int32_t>& center_slot_by_column,
+                           const Vector& center_weights, const TbmTokens& tbm,
+                           const std::vector<std::int32_t>& destinations, const CompressionConfig& config) {
+    if (destinations.size() != tbm.positions.size())
+        throw std::invalid_argument("weighted_merge: destination count mismatch");
+    const std::size_t n_cols = center_slot_by_column.size(), n_tbm = destinations.size(), d = cache.head_dim;
+    if (center_weights.size() != n_cols || tbm.weights.size() != n_tbm || tbm.score_triples.size() != n_tbm ||
+        tbm.k_raw.rows != n_tbm || tbm.v_raw.rows != n_tbm || (n_tbm && (tbm.k_raw.cols != d || tbm.v_raw.cols != d)))
+        throw std::invalid_argument("weighted_merge: inconsistent sizes");
+    std::vector<std::vector<std::size_t>> members(n_cols);
+    for (std::size_t i = 0; i < n_tbm; ++i) {
+        const std::int32_t c = destinations[i];
+        if (c == kZeroClass) {
+            if (config.eviction == EvictionRealization::zero_class) cache.lut.push_back({tbm.positions[i], kZeroClass});
+            continue;
+        }
+        if (c < 0 || static_cast<std::size_t>(c) >= n_cols) throw std::invalid_argument("weighted_merge: bad destination");
+        members[static_cast<std::size_t>(c)].push_back(i);
+    }
+    std::vector<double> uk(n_cols * d), val(n_cols * d), sc(n_cols * 3), tk(n_tbm * d), tv(n_tbm * d), ts(n_tbm * 3);
+    for (std::size_t c = 0; c < n_cols; ++c) {
+        const std::int32_t slot = center_slot_by_column[c];
+        if (slot < 0 || static_cast<std::size_t>(slot) >= cache.slots.size() || !cache.slots[slot])
+            throw CorruptionError("weighted_merge: column names a nonexistent slot");
+        const CenterEntry& e = *cache.slots[slot];
+        std::copy(e.unit_key.begin(), e.unit_key.end(), uk.begin() + c * d);
+        std::copy(e.value.begin(), e.value.end(), val.begin() + c * d);
+        sc[3 * c] = e.score.glo, sc[3 * c + 1] = e.score.loc_past, sc[3 * c + 2] = e.score.loc_cur;
+    }
+    for (std::size_t i = 0; i < n_tbm; ++i) {
+        std::copy(tbm.k_raw.data.begin() + i * d, tbm.k_raw.data.begin() + (i + 1) * d, tk.begin() + i * d);
+        std::copy(tbm.v_raw.data.begin() + i * d, tbm.v_raw.data.begin() + (i + 1) * d, tv.begin() + i * d);
+        const ScoreTriple& t = tbm.score_triples[i];
+        ts[3 * i] = t.glo, ts[3 * i + 1] = t.loc_past, ts[3 * i + 2] = t.loc_cur;
+    }
+    auto up = [](const std::vector<double>& h) {
+        detail::DevBuf b(h.size() * 8);
+        if (!h.empty()) detail::cuda(cudaMemcpy(b.p, h.data(), h.size() * 8, cudaMemcpyHostToDevice));
+        return b;
+    };
+    detail::DevBuf duk = up(uk), dval = up(val), dsc = up(sc), dcw = up(center_weights), dtk = up(tk), dtv = up(tv),
+                   dtw = up(tbm.weights), dts = up(ts), ddest(n_tbm * 4);
+    if (n_tbm) detail::cuda(cudaMemcpy(ddest.p, destinations.data(), n_tbm * 4, cudaMemcpyHostToDevice));
+    detail::check(ems_weighted_merge(static_cast<int32_t>(d), static_cast<int32_t>(n_cols), duk.as<double>(),
+                                     dval.as<double>(), dsc.as<double>(), dcw.as<double>(), static_cast<int32_t>(n_tbm),
+                                     dtk.as<double>(), dtv.as<double>(), dtw.as<double>(), dts.as<double>(),
+                                     ddest.as<int32_t>(), nullptr));
+    const auto uk2 = detail::download_raw<double>(duk.p, uk.size()), val2 = detail::download_raw<double>(dval.p, val.size());
+    const auto sc2 = detail::download_raw<double>(dsc.p, sc.size());
+    for (std::size_t c = 0; c < n_cols; ++c) {
+        if (members[c].empty()) continue;  // untouched, bit for bit
+        const std::int32_t slot = center_slot_by_column[c];
+        CenterEntry& e = *cache.slots[slot];
+        e.unit_key.assign(uk2.begin() + c * d, uk2.begin() + (c + 1) * d);
+        e.value.assign(val2.begin() + c * d, val2.begin() + (c + 1) * d);
+        e.score = {sc2[3 * c], sc2[3 * c + 1], sc2[3 * c + 2]};
+        for (std::size_t i : members[c]) cache.lut.push_back({tbm.positions[i], slot});
+    }
 }
 
 // policies.hpp: PolicyKind / PolicyHandle (proj/include/ems/policies.hpp:12-20) and
@@ -502,24 +648,25 @@ inline double redundancy_rate_direct(const Matrix& k_raw, const Matrix& v_raw, d
     return detail::download_raw<double>(rate.p, 1)[0];
 }
 
-// engine::prefill's per-head work (proj/src/engine.cpp:65-76) for pre-rotated
-// blocks: score + attention on (q_rot, k_rot, v), compress on (k_raw, v).
-// With GQA (q_rot.size() = G * k_raw.size()) the KV head's scores are the mean of
-// its G query heads' scores (contract D2).
-struct PrefillResult {
-    std::vector<Matrix> outputs;       // per query head
-    std::vector<HeadCacheState> heads; // per KV head
+// engine::prefill's per-head work (proj/src/engine.cpp:65-76) for PRE-ROTATED blocks with GQA:
+// score + attention on (q_rot, k_rot, v), compress on (k_raw, v).  With q_rot.size() = G *
+// k_raw.size() the KV head's scores are the mean of its G query heads' scores (contract D2).
+// (The reference's own engine entry point, on raw blocks with RoPE inside, is prefill(EngineState&,
+// ...) below.)
+struct RotatedPrefillResult {
+    std::vector<Matrix> outputs;        // per query head
+    std::vector<HeadCacheState> heads;  // per KV head
     bool compression_applied = false;
 };
-inline PrefillResult prefill(const std::vector<Matrix>& q_rot, const std::vector<Matrix>& k_rot,
-                             const std::vector<Matrix>& k_raw, const std::vector<Matrix>& v,
-                             const CompressionConfig& config, int dtype = EMS_F32) {
+inline RotatedPrefillResult prefill_rotated(const std::vector<Matrix>& q_rot, const std::vector<Matrix>& k_rot,
+                                            const std::vector<Matrix>& k_raw, const std::vector<Matrix>& v,
+                                            const CompressionConfig& config, int dtype = EMS_F32) {
     if (k_rot.empty() || k_rot.size() != k_raw.size() || k_raw.size() != v.size() ||
         q_rot.size() % k_rot.size() != 0)
         throw std::invalid_argument("prefill: head count mismatch");
     const std::size_t G = q_rot.size() / k_rot.size(), n = k_rot[0].rows;
     if (n == 0) throw std::invalid_argument("prefill: empty prompt");
-    PrefillResult res;
+    RotatedPrefillResult res;
     for (std::size_t h = 0; h < k_rot.size(); ++h) {
         std::vector<const Matrix*> qs;
         for (std::size_t g = 0; g < G; ++g) qs.push_back(&q_rot[h * G + g]);
@@ -531,6 +678,133 @@ inline PrefillResult prefill(const std::vector<Matrix>& q_rot, const std::vector
     }
     res.compression_applied = !res.heads.empty() && res.heads[0].compressed;
     return res;
+}
+
+// ---------------------------------------------------------------- engine.hpp (prefill)
+struct RopeParams {  // proj/include/ems/rope.hpp:9-12
+    std::size_t head_dim = 0;
+    double base = 10000.0;
+};
+struct AttentionOutput {  // proj/include/ems/engine.hpp:14-18
+    Matrix outputs;
+    bool weights_available = false;
+    Matrix weights;
+};
+struct EngineState {  // proj/include/ems/engine.hpp:22-31
+    std::size_t num_heads = 0;
+    std::size_t head_dim = 0;
+    CompressionConfig config;
+    PolicyHandle policy;
+    RopeParams rope;
+    std::vector<HeadCacheState> heads;
+    std::int64_t next_position = 0;
+    bool prefilled = false;
+    int dtype = EMS_F32;  // device precision of Q/K/V (not in the reference)
+};
+struct PrefillResult {  // proj/include/ems/engine.hpp:36-39
+    std::vector<AttentionOutput> per_head;
+    bool compression_applied = false;
+};
+
+// make_engine, proj/src/engine.cpp:26-40.
+inline EngineState make_engine(std::size_t num_heads, std::size_t head_dim, PolicyHandle policy,
+                               CompressionConfig config, double rope_base = 10000.0) {
+    if (num_heads == 0 || head_dim == 0 || head_dim % 2 != 0)
+        throw std::invalid_argument("make_engine: need heads >= 1 and even head_dim");
+    policy.validate(config);
+    EngineState s;
+    s.num_heads = num_heads;
+    s.head_dim = head_dim;
+    s.config = config;
+    s.policy = policy;
+    s.rope = RopeParams{head_dim, rope_base};
+    s.heads.resize(num_heads);
+    return s;
+}
+
+// prefill, proj/include/ems/engine.hpp:44-45 (engine.cpp:42-82): RAW per-head blocks; RoPE
+// (positions 0..n-1), causal attention with the Global-Local score, init_score_state and the
+// policy's prefill compression run on the device for all heads in one ems_prefill call.
+inline PrefillResult prefill(EngineState& state, const std::vector<Matrix>& q_blocks,
+                             const std::vector<Matrix>& k_blocks, const std::vector<Matrix>& v_blocks) {
+    if (q_blocks.size() != state.num_heads || k_blocks.size() != state.num_heads ||
+        v_blocks.size() != state.num_heads)
+        throw std::invalid_argument("prefill: head count mismatch");
+    const std::size_t n = q_blocks[0].rows, d = state.head_dim, H = state.num_heads;
+    if (n == 0) throw std::invalid_argument("prefill: empty prompt");
+    for (std::size_t h = 0; h < H; ++h)
+        if (q_blocks[h].rows != n || k_blocks[h].rows != n || v_blocks[h].rows != n)
+            throw std::invalid_argument("prefill: token count mismatch across blocks");
+    if (state.prefilled) throw StateError("prefill: engine already prefilled");
+    for (std::size_t h = 0; h < H; ++h)
+        if (q_blocks[h].cols != d || k_blocks[h].cols != d || v_blocks[h].cols != d)
+            throw std::invalid_argument("prefill: head_dim mismatch");
+    const int dtype = state.dtype;
+    ems_desc desc = detail::make_desc(H, H, n, d, dtype, state.config);
+    desc.policy = policy_code(state.policy.kind);
+    desc.sink_count = static_cast<int32_t>(state.policy.sink_count);
+    detail::check(ems_validate(&desc));
+    ems_cache_dims dims{};
+    detail::check(ems_cache_dims_for(&desc, &dims));
+    std::vector<const Matrix*> qs, ks, vs;
+    for (std::size_t h = 0; h < H; ++h) qs.push_back(&q_blocks[h]), ks.push_back(&k_blocks[h]), vs.push_back(&v_blocks[h]);
+    detail::DevBuf dq = detail::upload(qs, dtype), dk = detail::upload(ks, dtype), dv = detail::upload(vs, dtype);
+    const std::size_t es = dtype == EMS_F32 ? 4 : 2;
+    detail::DevBuf dqr(H * n * d * es), dkr(H * n * d * es), dout(H * n * d * es);
+    const std::size_t C = dims.centers, Lc = dims.locals, U = std::max(dims.lut, 1);
+    detail::DevBuf ck(H * C * d * es), cn(H * C * 4), cv(H * C * d * es), cp(H * C * 4), cs(H * C * 12),
+        lk(H * Lc * d * es), lv(H * Lc * d * es), lp(H * Lc * 4), ls(H * Lc * 12), up(H * U * 4), us(H * U * 4),
+        cnt(H * 16);
+    ems_cache cache{ck.p, cn.as<float>(), cv.p, cp.as<int32_t>(), cs.as<float>(), lk.p, lv.p,
+                    lp.as<int32_t>(), ls.as<float>(), up.as<int32_t>(), us.as<int32_t>(), cnt.as<int32_t>()};
+    detail::DevBuf ws(ems_workspace_bytes(&desc));
+    detail::check(ems_prefill(&desc, state.rope.base, dq.p, dk.p, dv.p, dqr.p, dkr.p, dout.p, nullptr, nullptr,
+                              nullptr, nullptr, &cache, ws.p, ws.n, nullptr));
+    detail::check(ems_sync_status(&desc, ws.p, nullptr));
+    PrefillResult result;
+    const auto o = detail::download(dout.p, H * n * d, dtype);
+    result.per_head.resize(H);
+    const auto counts = detail::download_raw<int32_t>(cnt.p, H * 4);
+    const auto ckh = detail::download(ck.p, H * C * d, dtype), cvh = detail::download(cv.p, H * C * d, dtype);
+    const auto cnh = detail::download_raw<float>(cn.p, H * C), csh = detail::download_raw<float>(cs.p, H * C * 3);
+    const auto cph = detail::download_raw<int32_t>(cp.p, H * C);
+    const auto lkh = detail::download(lk.p, H * Lc * d, dtype), lvh = detail::download(lv.p, H * Lc * d, dtype);
+    const auto lph = detail::download_raw<int32_t>(lp.p, H * Lc);
+    const auto lsh = detail::download_raw<float>(ls.p, H * Lc * 3);
+    const auto uph = detail::download_raw<int32_t>(up.p, H * U), ush = detail::download_raw<int32_t>(us.p, H * U);
+    for (std::size_t h = 0; h < H; ++h) {
+        result.per_head[h].outputs = Matrix(n, d);
+        std::copy(o.begin() + h * n * d, o.begin() + (h + 1) * n * d, result.per_head[h].outputs.data.begin());
+        HeadCacheState hc;
+        hc.head_dim = d;
+        hc.compressed = counts[4 * h + 3] != 0;
+        for (int s = 0; s < counts[4 * h]; ++s) {
+            const std::size_t e = h * C + s;
+            CenterEntry c;
+            c.unit_key.assign(ckh.begin() + e * d, ckh.begin() + (e + 1) * d);
+            c.value.assign(cvh.begin() + e * d, cvh.begin() + (e + 1) * d);
+            c.key_norm = cnh[e];
+            c.position = cph[e];
+            c.score = {csh[3 * e], csh[3 * e + 1], csh[3 * e + 2]};
+            hc.slots.emplace_back(std::move(c));
+        }
+        for (int i = 0; i < counts[4 * h + 1]; ++i) {
+            const std::size_t e = h * Lc + i;
+            LocalEntry l;
+            l.key.assign(lkh.begin() + e * d, lkh.begin() + (e + 1) * d);
+            l.value.assign(lvh.begin() + e * d, lvh.begin() + (e + 1) * d);
+            l.position = lph[e];
+            l.score = {lsh[3 * e], lsh[3 * e + 1], lsh[3 * e + 2]};
+            hc.locals.push_back(std::move(l));
+        }
+        for (int i = 0; i < counts[4 * h + 2]; ++i) hc.lut.push_back({uph[h * U + i], ush[h * U + i]});
+        hc.window_fill = 0;
+        state.heads[h] = std::move(hc);
+    }
+    state.next_position = static_cast<std::int64_t>(n);
+    state.prefilled = true;
+    result.compression_applied = state.heads[0].compressed;
+    return result;
 }
 
 }  // namespace ems_b200

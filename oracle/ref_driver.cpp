@@ -360,6 +360,107 @@ int ems_ref_engine_prefill(const double* q, const double* k, const double* v, in
     });
 }
 
+// ---- the fine-grained operators, for the C++ API test (tests/cpp/test_ems_hpp.cpp) ----------
+// partition_tokens (compressor.cpp:48-74) -> class bytes: 0 irrelevant, 1 TBM, 2 important, 3 local.
+int ems_ref_partition_tokens(const double* pooled, int64_t n, int64_t n_budget, int64_t l_win, double gamma,
+                             int8_t* cls) {
+    return guarded([&] {
+        const auto cfg = make_config(n_budget, l_win, 0.6, gamma, 1, 1);
+        const ems::TokenPartition p = ems::partition_tokens(ems::Vector(pooled, pooled + n), cfg);
+        for (auto i : p.irrelevant) cls[i] = 0;
+        for (auto i : p.tbm) cls[i] = 1;
+        for (auto i : p.important) cls[i] = 2;
+        for (auto i : p.local) cls[i] = 3;
+    });
+}
+
+// assign_merge_destinations (compressor.cpp:76-95).
+int ems_ref_assign_merge_destinations(const double* r, int64_t rows, int64_t cols, double tau, int32_t* dest) {
+    return guarded([&] {
+        const auto d = ems::assign_merge_destinations(to_matrix(r, rows, cols), tau);
+        std::copy(d.begin(), d.end(), dest);
+    });
+}
+
+// weighted_merge (compressor.cpp:97-161) on a cache whose slot c holds center column c; writes the
+// merged centers back and the appended LUT entries (lut_pos / lut_slot, *n_lut of them).
+int ems_ref_weighted_merge(int64_t d, int64_t n_cols, double* center_unit_key, double* center_value,
+                           double* center_score, const double* center_weight, int64_t n_tbm, const double* tbm_k,
+                           const double* tbm_v, const int64_t* tbm_pos, const double* tbm_w, const double* tbm_score,
+                           const int32_t* dest, int32_t zero_class, int64_t* lut_pos, int32_t* lut_slot,
+                           int64_t* n_lut) {
+    return guarded([&] {
+        ems::HeadCacheState cache;
+        cache.head_dim = (std::size_t)d;
+        std::vector<std::int32_t> slot_by_col(n_cols);
+        for (int64_t c = 0; c < n_cols; ++c) {
+            ems::CenterEntry e;
+            e.unit_key.assign(center_unit_key + c * d, center_unit_key + (c + 1) * d);
+            e.value.assign(center_value + c * d, center_value + (c + 1) * d);
+            e.score = ems::ScoreTriple{center_score[3 * c], center_score[3 * c + 1], center_score[3 * c + 2]};
+            slot_by_col[c] = cache.insert_center(std::move(e));
+        }
+        ems::TbmTokens t;
+        t.k_raw = to_matrix(tbm_k, n_tbm, d);
+        t.v_raw = to_matrix(tbm_v, n_tbm, d);
+        t.positions.assign(tbm_pos, tbm_pos + n_tbm);
+        t.weights.assign(tbm_w, tbm_w + n_tbm);
+        for (int64_t i = 0; i < n_tbm; ++i)
+            t.score_triples.push_back(ems::ScoreTriple{tbm_score[3 * i], tbm_score[3 * i + 1], tbm_score[3 * i + 2]});
+        const auto cfg = make_config(64, 8, 0.6, 4.0, 1, zero_class);
+        ems::weighted_merge(cache, slot_by_col, ems::Vector(center_weight, center_weight + n_cols), t,
+                            std::vector<std::int32_t>(dest, dest + n_tbm), cfg);
+        for (int64_t c = 0; c < n_cols; ++c) {
+            const ems::CenterEntry& e = *cache.slots[slot_by_col[c]];
+            std::copy(e.unit_key.begin(), e.unit_key.end(), center_unit_key + c * d);
+            std::copy(e.value.begin(), e.value.end(), center_value + c * d);
+            center_score[3 * c] = e.score.glo, center_score[3 * c + 1] = e.score.loc_past,
+                         center_score[3 * c + 2] = e.score.loc_cur;
+        }
+        *n_lut = (int64_t)cache.lut.size();
+        for (std::size_t i = 0; i < cache.lut.size(); ++i) lut_pos[i] = cache.lut[i].position, lut_slot[i] = cache.lut[i].slot;
+    });
+}
+
+// engine::prefill (make_engine + prefill, engine.cpp:26-82) over raw blocks [H][n][d] with any
+// policy (0 ems, 1 full, 2 streaming_llm, 3 h2o, 4 snapkv): outputs [H][n][d]; per head the center
+// positions (slot order, [H][cap_c], n_centers [H]), the LUT ([H][cap_lut], n_lut [H]) and the
+// compressed flag.
+int ems_ref_engine_prefill_arrays(const double* q, const double* k, const double* v, int64_t H, int64_t n, int64_t d,
+                                  int64_t n_budget, int64_t l_win, double tau, double gamma, int64_t kernel,
+                                  int32_t zero_class, double rope_base, int32_t policy, int64_t sink, double* out,
+                                  int64_t cap_c, int64_t* center_pos, int64_t* n_centers, int64_t cap_lut,
+                                  int64_t* lut_pos, int32_t* lut_slot, int64_t* n_lut, int32_t* compressed) {
+    return guarded([&] {
+        static const ems::PolicyKind kinds[] = {ems::PolicyKind::ems, ems::PolicyKind::full,
+                                                ems::PolicyKind::streaming_llm, ems::PolicyKind::h2o,
+                                                ems::PolicyKind::snapkv};
+        ems::PolicyHandle ph{kinds[policy]};
+        ph.sink_count = (std::size_t)sink;
+        const auto cfg = make_config(n_budget, l_win, tau, gamma, kernel, zero_class);
+        ems::EngineState e = ems::make_engine(H, d, ph, cfg, rope_base);
+        std::vector<ems::Matrix> qb, kb, vb;
+        for (int64_t h = 0; h < H; ++h) {
+            qb.push_back(to_matrix(q + h * n * d, n, d));
+            kb.push_back(to_matrix(k + h * n * d, n, d));
+            vb.push_back(to_matrix(v + h * n * d, n, d));
+        }
+        const ems::PrefillResult r = ems::prefill(e, qb, kb, vb);
+        for (int64_t h = 0; h < H; ++h) {
+            std::memcpy(out + h * n * d, r.per_head[h].outputs.data.data(), sizeof(double) * n * d);
+            const ems::HeadCacheState& c = e.heads[h];
+            int64_t nc = 0;
+            for (const auto& s : c.slots)
+                if (s.has_value() && nc < cap_c) center_pos[h * cap_c + nc++] = s->position;
+            n_centers[h] = nc;
+            n_lut[h] = std::min<int64_t>((int64_t)c.lut.size(), cap_lut);
+            for (int64_t i = 0; i < n_lut[h]; ++i)
+                lut_pos[h * cap_lut + i] = c.lut[i].position, lut_slot[h * cap_lut + i] = c.lut[i].slot;
+            compressed[h] = c.compressed;
+        }
+    });
+}
+
 // gen_synthetic prefill step, blocks laid out [H][n][d] (fp64 holding f32 values).
 int ems_ref_gen_synthetic(int32_t kind, uint64_t seed, int64_t tokens, int64_t heads, int64_t dim,
                           int64_t decode_steps, double level, double perturb, double* q, double* k,

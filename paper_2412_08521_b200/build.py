@@ -89,18 +89,23 @@ ORACLE_DIR = os.path.join(ROOT, "oracle")
 
 def build_cpp_tests(force: bool = False) -> str:
     """Test-only binary: the C++ reference-shaped API (include/ems_b200/ems.hpp) checked
-    against the C oracle.  Needs oracle/_build/libems_oracle.so (oracle.build())."""
+    against the C oracle and the reference itself.  Needs oracle/_build/libems_oracle.so and
+    oracle/_ref/libems_ref.so (oracle.build())."""
     oracle_so = os.path.join(ORACLE_DIR, "_build", "libems_oracle.so")
-    if not (os.path.exists(CPP_TEST_SRC) and os.path.exists(oracle_so)):
+    ref_so = os.path.join(ORACLE_DIR, "_ref", "libems_ref.so")
+    if not (os.path.exists(CPP_TEST_SRC) and os.path.exists(oracle_so) and os.path.exists(ref_so)):
         return ""
-    deps = [CPP_TEST_SRC, os.path.join(INCLUDE, "ems_b200", "ems.hpp"), LIB, oracle_so]
+    deps = [CPP_TEST_SRC, os.path.join(INCLUDE, "ems_b200", "ems.hpp"), LIB, oracle_so, ref_so]
     if force or not os.path.exists(CPP_TEST_BIN) or os.path.getmtime(CPP_TEST_BIN) < max(map(os.path.getmtime, deps)):
         os.makedirs(os.path.dirname(CPP_TEST_BIN), exist_ok=True)
         cmd = [NVCC, *ARCH, "-O2", "-std=c++17", "-I", INCLUDE, "-I", ORACLE_DIR, CPP_TEST_SRC,
                "-L", PKG, "-lems_b200", "-L", os.path.dirname(oracle_so), "-lems_oracle",
+               "-L", os.path.dirname(ref_so), "-lems_ref",
                "-Xlinker", "-rpath," + PKG, "-Xlinker", "-rpath," + os.path.dirname(oracle_so),
+               "-Xlinker", "-rpath," + os.path.dirname(ref_so),
                "-Xlinker", "-rpath,$ORIGIN/../../paper_2412_08521_b200",
-               "-Xlinker", "-rpath,$ORIGIN/../../oracle/_build", "-o", CPP_TEST_BIN]
+               "-Xlinker", "-rpath,$ORIGIN/../../oracle/_build",
+               "-Xlinker", "-rpath,$ORIGIN/../../oracle/_ref", "-o", CPP_TEST_BIN]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"cpp test build failed:\n{r.stdout}\n{r.stderr}")

@@ -56,6 +56,12 @@ cudaError_t launch_redundancy_cross(int dtype, int d, const void* kr, const void
                                     const void* kc, const void* vc, int nc, int key_only,
                                     float* r, cudaStream_t s);
 size_t diag_workspace_bytes(int units, int L);
+cudaError_t launch_effective_score(int units, int L, int kernel, const float* glo, const float* loc_past,
+                                   const float* loc_cur, float* pooled, DevStatus* status, cudaStream_t s);
+cudaError_t launch_assign_rows(const float* r, int n_rows, int n_cols, double tau, int32_t* dest, cudaStream_t s);
+cudaError_t launch_weighted_merge(int d, int n_cols, double* uk, double* val, double* score, const double* cw,
+                                  int n_tbm, const double* tk, const double* tv, const double* tw, const double* ts,
+                                  const int32_t* dest, cudaStream_t s);
 cudaError_t launch_sparsity(int units, int L, const float* glo, const float* loc, double zeta, double* rate,
                             void* ws, int unit_base, cudaStream_t s);
 cudaError_t launch_redundancy(int units, int L, int d, int dtype, const void* k, const void* v, double tau,
@@ -235,7 +241,7 @@ int run_score(const ems_desc* desc, const void* q, const void* k, const void* v,
 }
 
 int run_select(const ems_desc* desc, const float* glo, const float* loc, const ems_stage& sg,
-               void* ws, cudaStream_t s, int unit_base = 0) {
+               void* ws, cudaStream_t s, int unit_base = 0, bool pooled_given = false) {
     Dims m = make_dims(*desc);
     m.unit_base = unit_base;
     const int n_cand = m.L - desc->l_win;
@@ -249,8 +255,8 @@ int run_select(const ems_desc* desc, const float* glo, const float* loc, const e
         n_imp = (int)(sink + (n_cand > lo ? n_cand - lo : 0));
     }
     cudaError_t e = launch_select(m, desc->l_win, n_imp, n_tbm, kernel_eff(*desc), glo, loc, sg,
-                                  at<DevStatus>(ws, layout(*desc).status), s, desc->policy,
-                                  desc->sink_count, desc->n_budget);
+                                  at<DevStatus>(ws, layout(*desc).status), s,
+                                  pooled_given ? kPolicyPooled : desc->policy, desc->sink_count, desc->n_budget);
     if (e != cudaSuccess) {
         set_error("select launch: %s", cudaGetErrorString(e));
         return EMS_CUDA_ERROR;
@@ -416,6 +422,7 @@ size_t ems_prefill_host_workspace_bytes(const ems_desc* d) {
 
 int ems_score(const ems_desc* d, const void* q, const void* k, const void* v, void* out_o,
               float* lse, float* glo, float* loc, void* ws, size_t ws_bytes, cudaStream_t s) {
+    ems::NvtxRange ems_nvtx_range_("ems_score");
     if (int rc = ems_validate(d)) return rc;
     if (int rc = check_ws(d, ws, ws_bytes)) return rc;
     if (!q || !k || !glo || !loc || (out_o && !v)) {
@@ -428,6 +435,7 @@ int ems_score(const ems_desc* d, const void* q, const void* k, const void* v, vo
 
 int ems_select(const ems_desc* d, const float* glo, const float* loc, const ems_stage* st,
                void* ws, size_t ws_bytes, cudaStream_t s) {
+    ems::NvtxRange ems_nvtx_range_("ems_select");
     if (int rc = ems_validate(d)) return rc;
     if (int rc = check_ws(d, ws, ws_bytes)) return rc;
     if (d->seq_len <= d->n_budget || d->policy == EMS_POLICY_FULL) {
@@ -439,8 +447,71 @@ int ems_select(const ems_desc* d, const float* glo, const float* loc, const ems_
     return run_select(d, glo, loc, sg, ws, s);
 }
 
+int ems_partition(const ems_desc* d, const float* pooled, const ems_stage* st, void* ws, size_t ws_bytes,
+                  cudaStream_t s) {
+    ems::NvtxRange ems_nvtx_range_("ems_partition");
+    if (int rc = ems_validate(d)) return rc;
+    if (int rc = check_ws(d, ws, ws_bytes)) return rc;
+    if (!pooled || !st) {
+        set_error("ems_partition: null pooled scores or stage");
+        return EMS_INVALID_ARGUMENT;
+    }
+    if (d->seq_len < d->l_win + 1 || d->policy != EMS_POLICY_EMS) {  // compressor.cpp:50-52
+        set_error("partition_tokens: need more tokens than the local window (EMS policy)");
+        return EMS_INVALID_ARGUMENT;
+    }
+    EMS_CUDA_CHECK(cudaMemsetAsync(ws, 0, sizeof(DevStatus), s));
+    return run_select(d, pooled, pooled, *st, ws, s, 0, true);
+}
+
+int ems_effective_score(int32_t units, int32_t L, int32_t kernel, const float* glo, const float* loc_past,
+                        const float* loc_cur, float* pooled, void* ws, size_t ws_bytes, cudaStream_t s) {
+    ems::NvtxRange ems_nvtx_range_("ems_effective_score");
+    if (units < 0 || L < 1 || kernel < 1 || kernel % 2 == 0 || kernel > L) {  // numerics.cpp:63-68
+        set_error("effective_score: kernel_size must be odd and <= the input length");
+        return EMS_INVALID_ARGUMENT;
+    }
+    if ((units > 0 && (!glo || !loc_past || !pooled)) || !ws || ws_bytes < sizeof(DevStatus)) {
+        set_error("effective_score: null buffer or workspace < %zu bytes", sizeof(DevStatus));
+        return EMS_INVALID_ARGUMENT;
+    }
+    EMS_CUDA_CHECK(cudaMemsetAsync(ws, 0, sizeof(DevStatus), s));
+    if (units == 0) return EMS_OK;
+    EMS_CUDA_CHECK(launch_effective_score(units, L, kernel, glo, loc_past, loc_cur, pooled,
+                                          static_cast<DevStatus*>(ws), s));
+    return EMS_OK;
+}
+
+int ems_assign_merge_destinations(int32_t n_rows, int32_t n_cols, const float* r, double tau, int32_t* dest,
+                                  cudaStream_t s) {
+    ems::NvtxRange ems_nvtx_range_("ems_assign_merge_destinations");
+    if (n_rows < 0 || n_cols < 0 || (n_rows > 0 && (!dest || (n_cols > 0 && !r)))) {
+        set_error("assign_merge_destinations: bad arguments");
+        return EMS_INVALID_ARGUMENT;
+    }
+    EMS_CUDA_CHECK(launch_assign_rows(r, n_rows, n_cols, tau, dest, s));
+    return EMS_OK;
+}
+
+int ems_weighted_merge(int32_t d, int32_t n_cols, double* center_unit_key, double* center_value,
+                       double* center_score, const double* center_weight, int32_t n_tbm, const double* tbm_key,
+                       const double* tbm_value, const double* tbm_weight, const double* tbm_score,
+                       const int32_t* dest, cudaStream_t s) {
+    ems::NvtxRange ems_nvtx_range_("ems_weighted_merge");
+    if (d < 1 || d > 512 || n_cols < 0 || n_tbm < 0 ||
+        (n_cols > 0 && (!center_unit_key || !center_value || !center_score || !center_weight)) ||
+        (n_tbm > 0 && (!tbm_key || !tbm_value || !tbm_weight || !tbm_score || !dest))) {
+        set_error("weighted_merge: bad arguments (head_dim in [1, 512], non-null buffers)");
+        return EMS_INVALID_ARGUMENT;
+    }
+    EMS_CUDA_CHECK(launch_weighted_merge(d, n_cols, center_unit_key, center_value, center_score, center_weight,
+                                         n_tbm, tbm_key, tbm_value, tbm_weight, tbm_score, dest, s));
+    return EMS_OK;
+}
+
 int ems_merge(const ems_desc* d, const void* k_raw, const void* v, const ems_stage* st, void* ws,
               size_t ws_bytes, cudaStream_t s) {
+    ems::NvtxRange ems_nvtx_range_("ems_merge");
     if (int rc = ems_validate(d)) return rc;
     if (int rc = check_ws(d, ws, ws_bytes)) return rc;
     const ems_stage sg = st ? *st : default_stage(*d, ws);
@@ -450,6 +521,7 @@ int ems_merge(const ems_desc* d, const void* k_raw, const void* v, const ems_sta
 int ems_compact(const ems_desc* d, const void* k_raw, const void* v, const float* glo,
                 const float* loc, const ems_stage* st, const ems_cache* c, void* ws,
                 size_t ws_bytes, cudaStream_t s) {
+    ems::NvtxRange ems_nvtx_range_("ems_compact");
     if (int rc = ems_validate(d)) return rc;
     if (int rc = check_ws(d, ws, ws_bytes)) return rc;
     if (!c) {
@@ -489,6 +561,7 @@ int ems_prefill_compress(const ems_desc* d, const void* q_rot, const void* k_rot
                          const void* k_raw, const void* v, void* out_o, float* lse, float* glo,
                          float* loc, const ems_stage* st, const ems_cache* c, void* ws,
                          size_t ws_bytes, cudaStream_t s) {
+    ems::NvtxRange ems_nvtx_range_("ems_prefill_compress");
     if (int rc = ems_validate(d)) return rc;
     if (int rc = check_ws(d, ws, ws_bytes)) return rc;
     if (!q_rot || !k_rot || !k_raw || !v || !c) {
@@ -501,6 +574,7 @@ int ems_prefill_compress(const ems_desc* d, const void* q_rot, const void* k_rot
 
 int ems_rope(int32_t dtype, int32_t planes, int32_t L, int32_t d, double base, int64_t first_pos,
              const void* x, void* y, cudaStream_t s) {
+    ems::NvtxRange ems_nvtx_range_("ems_rope");
     if ((dtype != EMS_F32 && dtype != EMS_BF16) || planes < 0 || L < 0 || d <= 0 || d % 2 != 0 ||
         d > 512 || !(base > 0.0) || (planes > 0 && L > 0 && (!x || !y))) {
         set_error("ems_rope: bad arguments (need even head_dim <= 512, base > 0)");  // rope.cpp:11-13
@@ -521,6 +595,7 @@ int ems_rope(int32_t dtype, int32_t planes, int32_t L, int32_t d, double base, i
 int ems_prefill(const ems_desc* d, double rope_base, const void* q, const void* k, const void* v,
                 void* q_rot, void* k_rot, void* out_o, float* lse, float* glo, float* loc,
                 const ems_stage* st, const ems_cache* c, void* ws, size_t ws_bytes, cudaStream_t s) {
+    ems::NvtxRange ems_nvtx_range_("ems_prefill");
     if (int rc = ems_validate(d)) return rc;
     if (!(rope_base >= 0.0)) {
         set_error("ems_prefill: rope_base must be >= 0 (0 = no RoPE)");
@@ -549,6 +624,7 @@ int ems_prefill(const ems_desc* d, double rope_base, const void* q, const void* 
 int ems_redundancy_cross(int32_t dtype, int32_t d, const void* k_rows, const void* v_rows,
                          int32_t n_rows, const void* k_cols, const void* v_cols, int32_t n_cols,
                          int32_t key_only, float* r, cudaStream_t s) {
+    ems::NvtxRange ems_nvtx_range_("ems_redundancy_cross");
     if ((dtype != EMS_F32 && dtype != EMS_BF16) || !supported_dim(d) || n_rows < 0 || n_cols < 0) {
         set_error("ems_redundancy_cross: bad arguments");
         return EMS_INVALID_ARGUMENT;
@@ -570,6 +646,7 @@ size_t ems_diagnostics_workspace_bytes(int32_t units, int32_t L) {
 
 int ems_sparsity_rate(int32_t units, int32_t L, const float* glo, const float* loc, double zeta, double* rate,
                       void* ws, size_t ws_bytes, cudaStream_t s) {
+    ems::NvtxRange ems_nvtx_range_("ems_sparsity_rate");
     using namespace ems;
     if (units <= 0 || L <= 0 || !glo || !loc || !rate || !ws) {
         set_error("ems_sparsity_rate: bad arguments");
@@ -593,6 +670,7 @@ int ems_sparsity_rate(int32_t units, int32_t L, const float* glo, const float* l
 
 int ems_redundancy_rate(int32_t dtype, int32_t d, int32_t units, int32_t L, const void* k, const void* v,
                         double tau, double* rate, void* ws, size_t ws_bytes, cudaStream_t s) {
+    ems::NvtxRange ems_nvtx_range_("ems_redundancy_rate");
     using namespace ems;
     if ((dtype != EMS_F32 && dtype != EMS_BF16) || !supported_dim(d) || units <= 0 || L <= 0 || !k || !v ||
         !rate || !ws) {
@@ -613,6 +691,7 @@ int ems_redundancy_rate(int32_t dtype, int32_t d, int32_t units, int32_t L, cons
 }
 
 int ems_sync_status(const ems_desc* d, void* ws, cudaStream_t s) {
+    ems::NvtxRange ems_nvtx_range_("ems_sync_status");
     (void)d;
     EMS_CUDA_CHECK(cudaStreamSynchronize(s));
     DevStatus st;
@@ -688,6 +767,7 @@ extern "C" int ems_prefill_host(const ems_desc* d, double rope_base, const void*
                                 float* glo, float* loc, const ems_cache* d_cache, const ems_cache* h_cache,
                                 int32_t chunks, void* ws, size_t ws_bytes, cudaStream_t s,
                                 cudaStream_t copy_stream) {
+    ems::NvtxRange ems_nvtx_range_("ems_prefill_host");
     using namespace ems;
     if (int rc = ems_validate(d)) return rc;
     if (int rc = check_ws(d, ws, ws_bytes)) return rc;
@@ -912,6 +992,7 @@ size_t ems_decode_workspace_bytes(const ems_desc* d, int32_t max_pos) {
 }
 
 int ems_rope_table(int32_t d, double base, int32_t max_pos, void* table, cudaStream_t s) {
+    ems::NvtxRange ems_nvtx_range_("ems_rope_table");
     using namespace ems;
     if (d <= 0 || d % 2 || !(base > 0.0) || max_pos <= 0 || !table) {
         set_error("ems_rope_table: bad arguments");
@@ -927,6 +1008,7 @@ int ems_rope_table(int32_t d, double base, int32_t max_pos, void* table, cudaStr
 
 int ems_decode_init(const ems_desc* d, int32_t max_pos, const ems_cache* c, const ems_decode_state* st,
                     cudaStream_t s) {
+    ems::NvtxRange ems_nvtx_range_("ems_decode_init");
     using namespace ems;
     if (int rc = decode_check(d, max_pos)) return rc;
     if (!c || !st) {
@@ -944,6 +1026,7 @@ int ems_decode_init(const ems_desc* d, int32_t max_pos, const ems_cache* c, cons
 }
 
 int ems_decode_sync_status(const ems_desc* d, const ems_decode_state* st, cudaStream_t s) {
+    ems::NvtxRange ems_nvtx_range_("ems_decode_sync_status");
     using namespace ems;
     if (int rc = ems_validate(d)) return rc;
     if (!st || !st->meta) {
@@ -965,6 +1048,7 @@ int ems_decode_sync_status(const ems_desc* d, const ems_decode_state* st, cudaSt
 int ems_decode_step(const ems_desc* d, int64_t position, const void* table, int32_t max_pos, const void* q,
                     const void* k, const void* v, void* out, int32_t* argmax_pos, const ems_decode_state* st,
                     void* ws, size_t ws_bytes, cudaStream_t s) {
+    ems::NvtxRange ems_nvtx_range_("ems_decode_step");
     using namespace ems;
     if (int rc = decode_check(d, max_pos)) return rc;
     if (!table || !q || !k || !v || !out || !argmax_pos || !st) {

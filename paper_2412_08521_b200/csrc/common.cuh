@@ -3,6 +3,7 @@
 
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <stdint.h>
 
 #include "ems_b200.h"
@@ -10,6 +11,10 @@
 namespace ems {
 
 constexpr int kWarp = 32;
+
+// Internal select mode (never a descriptor policy): rank caller-supplied pooled scores passed in
+// the glo slot (partition_tokens, compressor.cpp:48-74) with the EMS caps.
+constexpr int kPolicyPooled = 100;
 
 // Device-side status word (first 16 bytes of the workspace).
 struct DevStatus {
@@ -103,6 +108,16 @@ struct Dims {
 Dims make_dims(const ems_desc& d);
 
 void set_error(const char* fmt, ...);
+
+// One NVTX range per C-ABI call (header-only NVTX 3: a no-op unless a profiler is attached), so
+// nsight / ncu timelines show which entry point launched which kernels.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+#define EMS_NVTX(name) ::ems::NvtxRange ems_nvtx_range_(name)
 
 // Dynamic shared memory above 48 KB is a function attribute of the CURRENT DEVICE's context:
 // set it once per (kernel, device), so one process can drive several GPUs (one host thread

@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(
         const int lo_recent = max(L - (n_budget - sink), sink);
         for (int i = tid; i < L; i += kSelThreads) {
             float v;
-            if (policy == EMS_POLICY_H2O) {
+            if ((policy == EMS_POLICY_H2O || policy == kPolicyPooled)) {
                 v = g[i];  // top_k_by(scores.glo, ...)
             } else if (policy == EMS_POLICY_SNAPKV) {  // mean_pool_1d(loc_past + loc_cur)
                 const int a = max(0, i - half), bnd = min(L - 1, i + half);
@@ -313,7 +313,7 @@ __global__ void __cluster_dims__(kClu, 1, 1) __launch_bounds__(kCThreads) select
     const int lo_recent = max(L - (n_budget - sink), sink);
     for (int i = c0 + tid; i < c1; i += kCThreads) {
         float v;
-        if (policy == EMS_POLICY_H2O) {
+        if ((policy == EMS_POLICY_H2O || policy == kPolicyPooled)) {
             v = g[i];
         } else if (policy == EMS_POLICY_STREAMING) {
             v = (i < sink || (i >= lo_recent && i < n_cand_b)) ? 1.f : 0.f;

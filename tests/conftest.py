@@ -11,6 +11,7 @@ if ROOT not in sys.path:
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (run via gpurun); parity tests proper")
     config.addinivalue_line("markers", "slow: long-running")
+    config.addinivalue_line("markers", "sanitizer: compute-sanitizer runs, one tool per GPU session (not in -m gpu)")
 
 
 @pytest.fixture(scope="session")

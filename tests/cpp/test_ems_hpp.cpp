@@ -1,5 +1,7 @@
 // test_ems_hpp.cpp -- TEST ONLY: the reference-shaped C++ API (include/ems_b200/ems.hpp)
-// against the C restatement of the reference (oracle/ems_oracle.h) on seeded inputs.
+// against the C restatement of the reference (oracle/ems_oracle.h) and against the REFERENCE
+// ITSELF (oracle/_ref/libems_ref.so: the reference's sources behind the extern "C" shim
+// oracle/ref_driver.cpp) on seeded inputs and the reference's own hand cases.
 // Exit code = number of failed checks.  Run by tests/test_gpu_cpp_api.py.
 #include <cmath>
 #include <cstdio>
@@ -10,6 +12,25 @@
 #include "ems_oracle.h"
 
 using namespace ems_b200;
+
+// the reference's own operators (oracle/ref_driver.cpp)
+extern "C" {
+int ems_ref_effective_score(const double* glo, const double* loc_past, const double* loc_cur, int64_t n,
+                            int64_t kernel, double* out);
+int ems_ref_partition_tokens(const double* pooled, int64_t n, int64_t n_budget, int64_t l_win, double gamma,
+                             int8_t* cls);
+int ems_ref_assign_merge_destinations(const double* r, int64_t rows, int64_t cols, double tau, int32_t* dest);
+int ems_ref_weighted_merge(int64_t d, int64_t n_cols, double* center_unit_key, double* center_value,
+                           double* center_score, const double* center_weight, int64_t n_tbm, const double* tbm_k,
+                           const double* tbm_v, const int64_t* tbm_pos, const double* tbm_w, const double* tbm_score,
+                           const int32_t* dest, int32_t zero_class, int64_t* lut_pos, int32_t* lut_slot,
+                           int64_t* n_lut);
+int ems_ref_engine_prefill_arrays(const double* q, const double* k, const double* v, int64_t H, int64_t n, int64_t d,
+                                  int64_t n_budget, int64_t l_win, double tau, double gamma, int64_t kernel,
+                                  int32_t zero_class, double rope_base, int32_t policy, int64_t sink, double* out,
+                                  int64_t cap_c, int64_t* center_pos, int64_t* n_centers, int64_t cap_lut,
+                                  int64_t* lut_pos, int32_t* lut_slot, int64_t* n_lut, int32_t* compressed);
+}
 
 static int g_fail = 0;
 #define CHECK(cond, ...)                                          \
@@ -181,9 +202,208 @@ int main() {
 
     // --- engine-level prefill with GQA (G = 2), bf16 on device
     std::vector<Matrix> qs{q, random_matrix(gen, n, d)}, ks{k}, vs{v};
-    const PrefillResult pr = prefill(qs, ks, ks, vs, cfg, EMS_BF16);
+    const RotatedPrefillResult pr = prefill_rotated(qs, ks, ks, vs, cfg, EMS_BF16);
     CHECK(pr.outputs.size() == 2 && pr.heads.size() == 1 && pr.compression_applied, "prefill shapes");
     CHECK(pr.heads[0].slots.size() == cfg.center_capacity(), "prefill centers");
+
+    // ===================== against the reference itself (oracle/_ref) =====================
+    {  // effective_score (scoring.cpp:146-152)
+        std::mt19937_64 g2(7);
+        std::uniform_real_distribution<double> ud(0.0, 2.0);
+        ScoreState st;
+        const std::size_t m = 500;
+        for (std::size_t i = 0; i < m; ++i) st.glo.push_back(ud(g2)), st.loc_past.push_back(ud(g2) * (i > 400)),
+            st.loc_cur.push_back(0.1 * ud(g2));
+        const Vector got = effective_score(st, 7);
+        Vector want(m);
+        ems_ref_effective_score(st.glo.data(), st.loc_past.data(), st.loc_cur.data(), m, 7, want.data());
+        CHECK(max_rel(got, want) < 1e-6, "effective_score rel err %g", max_rel(got, want));
+        bool thr = false;
+        try {
+            ScoreState z = st;
+            std::fill(z.glo.begin(), z.glo.end(), 0.0);
+            effective_score(z, 7);
+        } catch (const DegenerateInputError&) {
+            thr = true;
+        }
+        CHECK(thr, "effective_score with no global mass must throw DegenerateInputError");
+        // partition_tokens on the reference's pooled scores (compressor.cpp:48-74)
+        CompressionConfig pc;
+        pc.n_budget = 64, pc.l_win = 16, pc.gamma = 3.0;
+        const TokenPartition tp = partition_tokens(want, pc);
+        std::vector<int8_t> cls(m);
+        ems_ref_partition_tokens(want.data(), m, pc.n_budget, pc.l_win, pc.gamma, cls.data());
+        int mism = 0;
+        for (auto i : tp.important) mism += cls[i] != 2;
+        for (auto i : tp.tbm) mism += cls[i] != 1;
+        for (auto i : tp.irrelevant) mism += cls[i] != 0;
+        for (auto i : tp.local) mism += cls[i] != 3;
+        CHECK(mism == 0 && tp.important.size() == 48 && tp.tbm.size() == 128 && tp.local.size() == 16,
+              "partition_tokens vs reference: %d differ (%zu/%zu/%zu)", mism, tp.important.size(), tp.tbm.size(),
+              tp.local.size());
+    }
+    {  // the reference's hand partitions (test_compressor.cpp:63-148)
+        Vector sc(20);
+        for (int i = 0; i < 20; ++i) sc[i] = 20.0 - i;
+        CompressionConfig hc;
+        hc.n_budget = 8, hc.l_win = 4, hc.gamma = 1.5;
+        const TokenPartition p = partition_tokens(sc, hc);
+        CHECK(p.important == std::vector<std::size_t>({0, 1, 2, 3}) && p.tbm == std::vector<std::size_t>({4, 5, 6, 7}) &&
+                  p.irrelevant.size() == 8 && p.irrelevant.front() == 8 && p.local.front() == 16,
+              "hand partition 20-i");
+        CompressionConfig tc;
+        tc.n_budget = 6, tc.l_win = 2, tc.gamma = 1.0;
+        const TokenPartition t = partition_tokens(Vector(9, 1.0), tc);
+        CHECK(t.important == std::vector<std::size_t>({0, 1, 2, 3}) && t.tbm.empty(), "ties break low");
+        bool thr = false;
+        try {
+            partition_tokens(Vector(4, 1.0), tc);
+        } catch (const std::invalid_argument&) {
+            thr = true;
+        }
+        CHECK(!thr, "4 tokens > l_win 2 is a valid partition");
+    }
+    {  // assign_merge_destinations (compressor.cpp:76-95): hand case + random vs reference
+        Matrix r(1, 3);
+        r.data = {0.3, 0.7, 0.5};
+        CHECK(assign_merge_destinations(r, 0.6)[0] == 1 && assign_merge_destinations(r, 0.71)[0] == kZeroClass,
+              "argmax / threshold hand case");
+        Matrix tie(1, 3);
+        tie.data = {0.5, 0.9, 0.9};
+        CHECK(assign_merge_destinations(tie, 0.0)[0] == 1, "ties go to the lower column");
+        std::mt19937_64 g3(11);
+        std::uniform_real_distribution<double> ud(-1.0, 1.0);
+        Matrix rr(300, 77);
+        for (double& x : rr.data) x = static_cast<double>(static_cast<float>(ud(g3)));
+        for (std::size_t c = 0; c < 77; ++c) rr.at(5, c) = 0.25;  // an all-ties row
+        const auto got = assign_merge_destinations(rr, 0.5);
+        std::vector<int32_t> want(300);
+        ems_ref_assign_merge_destinations(rr.data.data(), 300, 77, 0.5, want.data());
+        CHECK(got == want, "assign_merge_destinations vs reference");
+    }
+    {  // weighted_merge (compressor.cpp:97-161) vs reference, zero class and explicit removal
+        std::mt19937_64 g4(13);
+        std::normal_distribution<double> nd(0.0, 1.0);
+        const std::size_t dm = 32, cols = 9, nt = 40;
+        for (int zc = 0; zc < 2; ++zc) {
+            HeadCacheState cache;
+            cache.head_dim = dm;
+            std::vector<double> uk(cols * dm), val(cols * dm), scs(cols * 3), cw(cols);
+            std::vector<int32_t> slot_by_col;
+            for (std::size_t c = 0; c < cols; ++c) {
+                CenterEntry e;
+                double nn = 0.0;
+                for (std::size_t x = 0; x < dm; ++x) e.unit_key.push_back(nd(g4)), nn += e.unit_key.back() * e.unit_key.back();
+                for (double& x : e.unit_key) x /= std::sqrt(nn);
+                for (std::size_t x = 0; x < dm; ++x) e.value.push_back(nd(g4));
+                e.score = {std::abs(nd(g4)), std::abs(nd(g4)), 0.0};
+                e.position = (std::int64_t)(10 * c);
+                std::copy(e.unit_key.begin(), e.unit_key.end(), uk.begin() + c * dm);
+                std::copy(e.value.begin(), e.value.end(), val.begin() + c * dm);
+                scs[3 * c] = e.score.glo, scs[3 * c + 1] = e.score.loc_past, scs[3 * c + 2] = e.score.loc_cur;
+                cw[c] = c == 3 ? 0.0 : std::abs(nd(g4));
+                cache.slots.emplace_back(std::move(e));
+                slot_by_col.push_back((int32_t)c);
+            }
+            TbmTokens t;
+            t.k_raw = Matrix(nt, dm);
+            t.v_raw = Matrix(nt, dm);
+            std::vector<int32_t> dest(nt);
+            std::vector<double> tsc(nt * 3);
+            for (std::size_t i = 0; i < nt; ++i) {
+                for (std::size_t x = 0; x < dm; ++x) t.k_raw.at(i, x) = nd(g4), t.v_raw.at(i, x) = nd(g4);
+                t.positions.push_back((std::int64_t)(1000 + i));
+                t.weights.push_back(i % 7 == 0 ? 0.0 : std::abs(nd(g4)));
+                t.score_triples.push_back({std::abs(nd(g4)), std::abs(nd(g4)), 0.0});
+                tsc[3 * i] = t.score_triples.back().glo, tsc[3 * i + 1] = t.score_triples.back().loc_past;
+                dest[i] = (i % 5 == 0) ? kZeroClass : (int32_t)((i * 7) % cols);
+            }
+            for (std::size_t i = 0; i < nt; ++i)  // column 3: zero weights everywhere -> uniform
+                if (dest[i] == 3) t.weights[i] = 0.0;
+            CompressionConfig mc;
+            mc.eviction = zc ? EvictionRealization::zero_class : EvictionRealization::explicit_removal;
+            weighted_merge(cache, slot_by_col, cw, t, dest, mc);
+            std::vector<int64_t> lp(nt);
+            std::vector<int32_t> ls(nt);
+            int64_t nl = 0;
+            ems_ref_weighted_merge(dm, cols, uk.data(), val.data(), scs.data(), cw.data(), nt, t.k_raw.data.data(),
+                                   t.v_raw.data.data(), t.positions.data(), t.weights.data(), tsc.data(), dest.data(),
+                                   zc, lp.data(), ls.data(), &nl);
+            double err = 0.0;
+            for (std::size_t c = 0; c < cols; ++c) {
+                const CenterEntry& e = *cache.slots[c];
+                for (std::size_t x = 0; x < dm; ++x)
+                    err = std::max(err, std::max(std::abs(e.unit_key[x] - uk[c * dm + x]), std::abs(e.value[x] - val[c * dm + x])));
+                err = std::max(err, std::abs(e.score.glo - scs[3 * c]) + std::abs(e.score.loc_past - scs[3 * c + 1]));
+            }
+            CHECK(err < 1e-12, "weighted_merge vs reference (zero_class=%d): max abs err %g", zc, err);
+            bool same = (int64_t)cache.lut.size() == nl;
+            for (int64_t i = 0; same && i < nl; ++i) same = cache.lut[i].position == lp[i] && cache.lut[i].slot == ls[i];
+            CHECK(same, "weighted_merge LUT entries vs reference (zero_class=%d)", zc);
+        }
+    }
+    {  // compress_prefill with a first_position (compressor.hpp:58-60)
+        CompressionConfig c2;
+        c2.n_budget = 64, c2.l_win = 8, c2.gamma = 2.0;
+        const HeadCacheState a = compress_prefill(k, v, init_score_state(og, ol, 8), c2);
+        const HeadCacheState b = compress_prefill(k, v, init_score_state(og, ol, 8), c2, 1000);
+        bool ok = a.slots.size() == b.slots.size() && a.lut.size() == b.lut.size();
+        for (std::size_t s = 0; ok && s < a.slots.size(); ++s) ok = b.slots[s]->position == a.slots[s]->position + 1000;
+        for (std::size_t e = 0; ok && e < a.lut.size(); ++e)
+            ok = b.lut[e].position == a.lut[e].position + 1000 && b.lut[e].slot == a.lut[e].slot;
+        CHECK(ok, "compress_prefill(first_position = 1000) shifts every position");
+    }
+    {  // make_engine + prefill(EngineState&, ...) vs the reference engine (engine.cpp:26-82)
+        const std::size_t H = 3, ne = 400, de = 64;
+        std::vector<Matrix> qb, kb, vb;
+        for (std::size_t h = 0; h < H; ++h)
+            qb.push_back(random_matrix(gen, ne, de)), kb.push_back(random_matrix(gen, ne, de)),
+                vb.push_back(random_matrix(gen, ne, de));
+        std::vector<double> qf, kf, vf;
+        for (std::size_t h = 0; h < H; ++h)
+            qf.insert(qf.end(), qb[h].data.begin(), qb[h].data.end()), kf.insert(kf.end(), kb[h].data.begin(), kb[h].data.end()),
+                vf.insert(vf.end(), vb[h].data.begin(), vb[h].data.end());
+        const PolicyKind kinds[] = {PolicyKind::ems, PolicyKind::h2o};
+        const int codes[] = {0, 3};
+        for (int pi = 0; pi < 2; ++pi) {
+            CompressionConfig ec;
+            ec.n_budget = 96, ec.l_win = 16, ec.gamma = 2.5, ec.tau = 0.3, ec.kernel_size = 5;
+            EngineState es = make_engine(H, de, PolicyHandle{kinds[pi], 4}, ec, 10000.0);
+            const PrefillResult pr = prefill(es, qb, kb, vb);
+            const std::size_t cap_c = 96, cap_l = 400;
+            std::vector<double> out(H * ne * de);
+            std::vector<int64_t> cpos(H * cap_c), ncen(H), lpos(H * cap_l), nlut(H);
+            std::vector<int32_t> lslot(H * cap_l), comp(H);
+            ems_ref_engine_prefill_arrays(qf.data(), kf.data(), vf.data(), H, ne, de, ec.n_budget, ec.l_win, ec.tau,
+                                          ec.gamma, ec.kernel_size, 1, 10000.0, codes[pi], 4, out.data(), cap_c,
+                                          cpos.data(), ncen.data(), cap_l, lpos.data(), lslot.data(), nlut.data(),
+                                          comp.data());
+            double oerr = 0.0;
+            int mism = 0;
+            for (std::size_t h = 0; h < H; ++h) {
+                for (std::size_t i = 0; i < ne * de; ++i)
+                    oerr = std::max(oerr, std::abs(pr.per_head[h].outputs.data[i] - out[h * ne * de + i]));
+                const HeadCacheState& c = es.heads[h];
+                mism += (int)c.slots.size() != ncen[h] || (int)c.lut.size() != nlut[h] || c.compressed != (bool)comp[h];
+                for (std::size_t s = 0; s < std::min<std::size_t>(c.slots.size(), ncen[h]); ++s)
+                    mism += c.slots[s]->position != cpos[h * cap_c + s];
+                for (std::size_t e = 0; e < std::min<std::size_t>(c.lut.size(), nlut[h]); ++e)
+                    mism += c.lut[e].position != lpos[h * cap_l + e] || c.lut[e].slot != lslot[h * cap_l + e];
+            }
+            // fp32 device arithmetic vs fp64: outputs to ~1e-6; positions exact (fp32 scores decide the
+            // same cut here -- a tie within 1e-5 of the cut would be excluded by the D10 band)
+            CHECK(oerr < 1e-4, "engine prefill outputs vs reference (policy %d): %g", codes[pi], oerr);
+            CHECK(mism == 0, "engine prefill caches vs reference (policy %d): %d differ", codes[pi], mism);
+            CHECK(es.prefilled && es.next_position == (int64_t)ne && pr.compression_applied, "engine state");
+            bool thr = false;
+            try {
+                prefill(es, qb, kb, vb);
+            } catch (const StateError&) {
+                thr = true;
+            }
+            CHECK(thr, "a second prefill must throw StateError");
+        }
+    }
 
     std::printf("%s (%d failures)\n", g_fail ? "FAILED" : "ok", g_fail);
     return g_fail;
