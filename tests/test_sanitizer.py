@@ -4,7 +4,9 @@ Marked `sanitizer`, NOT `gpu`: the B200 profiling recipe (driver 580.159) report
 several compute-sanitizer tools back to back in one GPU session left the GPU unusable, so the
 default `-m gpu` suite never runs them; run ONE tool per GPU session instead:
     pytest -m sanitizer -k memcheck    (then racecheck, synccheck in separate sessions)
-Summaries of the runs are committed under profiles/."""
+Summaries of the runs are committed under profiles/.  On this pool the wrapper refuses
+compute-sanitizer outright ("closed on this pool"), so the out-of-bounds evidence comes from
+tests/test_gpu_guard_bands.py (guard bands around every buffer the kernels write)."""
 import os
 import shutil
 import subprocess
@@ -33,4 +35,6 @@ def test_sanitizer_clean(tool):
     os.makedirs(os.path.dirname(log), exist_ok=True)
     with open(log, "w") as f:
         f.write(out)
+    if "closed on this pool" in out:  # the pool's wrapper refuses the tool (profiles/r2_sanitizer.md)
+        pytest.skip(out.strip().splitlines()[-1][:200])
     assert r.returncode == 0 and "sanitize case done" in out, out[-4000:]
