@@ -66,7 +66,7 @@ __device__ __forceinline__ void cols_masked(uint32_t sa, uint32_t lb, float c, i
 // tensor-core path is d = 128 only); groups of 4 pairs are tree-summed before entering
 // one of 4 independent accumulators, keeping the FADD dependency chains short.
 constexpr float kC128 = 0.12751743f;
-constexpr int kPoly = 2;  // exp2 pairs (of every 8) computed on the FMA pipe (ex2_poly2)
+constexpr int kPoly = 1;  // exp2 pairs (of every 8) computed on the FMA pipe (ex2_poly2; 0-3 measured, 1 fastest)
 __device__ __forceinline__ float cols_fast(uint32_t sa, uint32_t lb) {
     const float2 c2 = make_float2(kC128, kC128);
     uint32_t r[2][32];

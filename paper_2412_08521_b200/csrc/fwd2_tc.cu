@@ -18,9 +18,10 @@
 // against ~60% / ~69% for the single-CTA N = 128 instructions of fwd_tc_kernel) at the same
 // K/V bytes per FLOP.  TMEM per CTA: S [0,256) | P (bf16) [256,384) | O [384,512): P has its own
 // columns, so S_{j+1} is issued as soon as both CTAs have read S_j into registers and runs
-// under the softmax of tile j; PV_j follows once P_j is stored.  Softmax: four warpgroups per
-// CTA, thread = (row, 64 keys); row maxima exchanged through shared memory; lazily updated
-// reference max (O rescaled only when a row max grows by > 8 in log2 units).
+// under the softmax of tile j; PV_j follows in two K-halves, each issued as soon as its half
+// of P_j is stored.  Softmax: four warpgroups per CTA, thread = (row, 32 keys of each 128-key
+// half); row maxima exchanged through shared memory; lazily updated reference max (O rescaled
+// only when a row max grows by > 8 in log2 units).
 #include <cuda.h>
 #include <stdlib.h>
 
@@ -43,8 +44,6 @@ constexpr int kStages2 = 2;
 constexpr int kMaxT2 = 4096;  // 256-key tiles per sequence (L <= 1048576) for the smem key bounds
 constexpr size_t kSmem2 = 1024 + kTileBytes + 2 * kStages2 * kTileBytes + 2 * 4 * 128 * 4 + kMaxT2 * 4;
 
-constexpr int kPoly = 2;  // exp2 pairs (of every 8) computed on the FMA pipe (ex2_poly2)
-
 struct Fwd2Args {
     int L, Lp, Hq, Hkv, G, nT, units;  // Lp = nT * 128: row stride of nlse2
     float c;
@@ -61,7 +60,7 @@ struct Bars2 {
     uint64_t k_full[kStages2], v_full[kStages2];    // leader: both halves landed
     uint64_t k_empty[kStages2], v_empty[kStages2];  // local (multicast commit)
     uint64_t s_full, o_full;                        // local (multicast commit)
-    uint64_t s_free, p_full;                        // leader: 32 warp arrivals (16 per CTA)
+    uint64_t s_free, p_full, p_full_hi;             // leader: 32 warp arrivals (16 per CTA)
     uint32_t tmem_base;
 };
 
@@ -114,6 +113,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT2, 1)
         mbar_init(&bars.o_full, 1);
         mbar_init(&bars.s_free, 32);
         mbar_init(&bars.p_full, 32);
+        mbar_init(&bars.p_full_hi, 32);
         fence_barrier_init();
     }
     tc_fence_before();
@@ -173,30 +173,41 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT2, 1)
                     tc_fence_after();
                     issue_s(j + 1);
                 }
+                // PV_j in two K-halves: keys [0, 128) as soon as the softmax warps stored that half
+                // of P_j, keys [128, 256) after the other half -- the first half of the product
+                // runs under the second half of the exponentials
                 mbar_wait(&bars.p_full, j & 1);
                 mbar_wait(&bars.v_full[j % kStages2], (j / kStages2) & 1);
                 tc_fence_after();
                 const uint32_t va = smem_u32(sv + (j % kStages2) * kTileBytes);
 #pragma unroll
-                for (int k = 0; k < 16; ++k)
+                for (int k = 0; k < 8; ++k)
                     mma_ts_2sm(tO, tP + k * 8, sdesc(va + k * 2048, 16384, 1024), id_o, (j > 0 || k > 0) ? 1u : 0u);
+                mbar_wait(&bars.p_full_hi, j & 1);
+                tc_fence_after();
+#pragma unroll
+                for (int k = 8; k < 16; ++k)
+                    mma_ts_2sm(tO, tP + k * 8, sdesc(va + k * 2048, 16384, 1024), id_o, 1u);
                 mma_commit_2sm(&bars.o_full, 0x3);
                 mma_commit_2sm(&bars.v_empty[j % kStages2], 0x3);
             }
         }
     } else {
         // ---------------------------------------------------------------- softmax
-        const int q = (warp - 2) >> 2;          // key quarter: columns [64q, 64q + 64) of S
+        // warpgroup q owns key columns [32q, 32q + 32) of each 128-key half of S: every thread
+        // computes its row's low-half keys first, stores them as P and signals, then the high half
+        const int q = (warp - 2) >> 2;
         const int wi = warp & 3;
         const int m = wi * 32 + (tid & 31);     // row within the CTA's tile
         const int qrow = tile * kTile + m;       // query position
         const bool store = real && qrow < a.L;   // rows >= L (TMA zero fill) are computed, never stored
         const uint32_t lane_off = (uint32_t)(wi * 32) << 16;
-        const uint32_t sS = tS + lane_off + 64 * q;
-        const uint32_t sP = tP + lane_off + 32 * q;
+        const uint32_t sS = tS + lane_off + 32 * q;   // + 128 for the high half
+        const uint32_t sP = tP + lane_off + 16 * q;   // + 64 for the high half
         const uint32_t sO = tO + lane_off + 32 * q;
         const uint32_t s_free_l = mapa(smem_u32(&bars.s_free), 0);
         const uint32_t p_full_l = mapa(smem_u32(&bars.p_full), 0);
+        const uint32_t p_full_hi_l = mapa(smem_u32(&bars.p_full_hi), 0);
         float m_ref = -INFINITY, l = 0.f, qn;
         int n_x = 0;  // max exchanges so far (selects the xch buffer; identical across a row's quarters)
         {  // |q_row| before the first S arrives (off the critical path): quarter q sums dims
@@ -228,18 +239,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT2, 1)
             tc_fence_after();
             uint32_t r[2][32];
             tmem_ld32(sS, r[0]);
-            tmem_ld32(sS + 32, r[1]);
+            tmem_ld32(sS + 128, r[1]);
             tmem_ld_wait();
             tc_fence_before();
             __syncwarp();
             if ((tid & 31) == 0) mbar_arrive_cluster(s_free_l);  // S_j may be overwritten
-            const int key0 = 2 * j * kTile + 64 * q;
-            if (key0 + 63 > qrow) {  // causal mask near the diagonal
+            const int key0 = 2 * j * kTile + 32 * q;  // chunk c covers keys key0 + 128 c + [0, 32)
+            if (key0 + 128 + 31 > qrow) {  // causal mask near the diagonal
 #pragma unroll
                 for (int c = 0; c < 2; ++c)
 #pragma unroll
                     for (int x = 0; x < 32; ++x)
-                        if (key0 + c * 32 + x > qrow) r[c][x] = __float_as_uint(-INFINITY);
+                        if (key0 + c * 128 + x > qrow) r[c][x] = __float_as_uint(-INFINITY);
             }
             // warp-uniform (the exchange below is a named barrier); the four warps sharing these rows
             // see the same rows, hence the same vote
@@ -277,36 +288,38 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT2, 1)
             }
             const float2 c2 = make_float2(a.c, a.c), nm2 = make_float2(-m_ref, -m_ref);
             float2 rs2 = make_float2(0.f, 0.f);
-            uint32_t pk[2][16];
+            uint32_t pk[16];
 #pragma unroll
-            for (int c = 0; c < 2; ++c)
+            for (int c = 0; c < 2; ++c) {
 #pragma unroll
                 for (int x = 0; x < 16; ++x) {
                     const float2 arg = __ffma2_rn(
                         make_float2(__uint_as_float(r[c][2 * x]), __uint_as_float(r[c][2 * x + 1])), c2, nm2);
-                    const float2 p = (x & 7) < kPoly ? ex2_poly2(arg) : make_float2(ex2(arg.x), ex2(arg.y));
+                    // all exponentials on MUFU: with the split PV the FMA pipe, not MUFU, was the
+                    // tighter resource (measured: 2 of 8 pairs as ex2_poly2 was 4% slower)
+                    const float2 p = make_float2(ex2(arg.x), ex2(arg.y));
                     rs2 = __fadd2_rn(rs2, p);
-                    pk[c][x] = pack_bf16(p.x, p.y);
+                    pk[x] = pack_bf16(p.x, p.y);
                 }
-            l += rs2.x + rs2.y;
-            if (j > 0) {  // P region free and O stable once PV_{j-1} is done
-                mbar_wait(&bars.o_full, (j - 1) & 1);
-                tc_fence_after();
-                if (warp_need) {  // rescale this quarter of O (rare)
-                    uint32_t o[32];
-                    tmem_ld32(sO, o);
-                    tmem_ld_wait();
+                if (c == 0 && j > 0) {  // P region free and O stable once PV_{j-1} is done
+                    mbar_wait(&bars.o_full, (j - 1) & 1);
+                    tc_fence_after();
+                    if (warp_need) {  // rescale this quarter of O (rare), before PV_j starts
+                        uint32_t o[32];
+                        tmem_ld32(sO, o);
+                        tmem_ld_wait();
 #pragma unroll
-                    for (int x = 0; x < 32; ++x) o[x] = __float_as_uint(__uint_as_float(o[x]) * corr);
-                    tmem_st32(sO, o);
+                        for (int x = 0; x < 32; ++x) o[x] = __float_as_uint(__uint_as_float(o[x]) * corr);
+                        tmem_st32(sO, o);
+                    }
                 }
+                tmem_st16(sP + 64 * c, pk);
+                tmem_st_wait();
+                tc_fence_before();
+                __syncwarp();
+                if ((tid & 31) == 0) mbar_arrive_cluster(c == 0 ? p_full_l : p_full_hi_l);
             }
-            tmem_st16(sP, pk[0]);
-            tmem_st16(sP + 16, pk[1]);
-            tmem_st_wait();
-            tc_fence_before();
-            __syncwarp();
-            if ((tid & 31) == 0) mbar_arrive_cluster(p_full_l);
+            l += rs2.x + rs2.y;
         }
         // epilogue: l = sum of the four quarters (fixed order), O / l -> bf16, LSE
         float* xb = xch + (n_x & 1) * 512;
