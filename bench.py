@@ -52,11 +52,11 @@ def peaks():
 
 
 def traffic_bytes(w):
-    """ncu-measured DRAM bytes per score pass (profiles/r1_traffic.json; config 3 only)."""
+    """ncu-measured DRAM bytes per score pass (profiles/r2_traffic.json; config 3 only)."""
     if not w.name.startswith("cfg3") or w.seq_len != 32768 or w.batch != 1 or w.n_budget != 256:
         return None
     try:
-        with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r2_traffic.json")) as f:
             return json.load(f)["score_pass_bytes"]
     except (OSError, KeyError, ValueError):
         return None
