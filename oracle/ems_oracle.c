@@ -3,7 +3,8 @@
  *
  * TEST INFRASTRUCTURE ONLY (see ems_oracle.h).  Each function below cites the
  * reference function it restates; summation orders follow the reference so the
- * two agree to rounding (pinned by tests/test_oracle_vs_ref.py).
+ * two agree to rounding (pinned against the reference itself by tests/test_oracle.py,
+ * tests/test_oracle_policies.py and tests/test_oracle_diagnostics.py).
  */
 #include "ems_oracle.h"
 

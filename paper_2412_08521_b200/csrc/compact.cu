@@ -90,81 +90,93 @@ __global__ void __launch_bounds__(256) compact_entries_kernel(
     }
 }
 
-// Position-sorted LUT via a block-wide scan over the class bytes, one CTA per unit.
+// Position-sorted LUT as a MERGE of the two ascending index lists select produced (important
+// tokens with slots 0..n_imp-1, TBM tokens with their merge destinations), one CTA per unit:
+// an entry's LUT index is its rank in its own list plus the number of entries of the other list
+// before it (a binary search), so the work is O((n_imp + n_tbm) log) instead of a scan over all
+// L class bytes.  In explicit_removal mode the TBM tokens sent to the zero class are dropped: a
+// block scan over the TBM list gives the kept prefix.  The kernel ends with
+// HeadCacheState::check_integrity (proj/src/cache.cpp:66-80) on the LUT it wrote: every
+// non-zero-class entry names a live center slot and positions are strictly increasing; a
+// violation (possible only through inconsistent caller-supplied stage buffers) records
+// EMS_CORRUPTION, the reference's CorruptionError.
 constexpr int kLutThreads = 1024;
-// The kernel ends with HeadCacheState::check_integrity (proj/src/cache.cpp:66-80) on the LUT it
-// just wrote: every non-zero-class entry names a live center slot and positions are strictly
-// increasing; a violation (possible only through inconsistent caller-supplied stage buffers)
-// records EMS_CORRUPTION, the reference's CorruptionError.
-__global__ void __launch_bounds__(kLutThreads) compact_lut_kernel(
-    int L, const int8_t* __restrict__ cls_all, const int32_t* __restrict__ dest_all,
-    const int32_t* __restrict__ counts, int cap_t, int cap_lut, int zero_class, int64_t first_pos,
-    int32_t* __restrict__ lut_pos, int32_t* __restrict__ lut_slot, int32_t* __restrict__ out_counts,
-    DevStatus* status, int unit_base) {
-    __shared__ int shs[32];
-    const int u = blockIdx.x, tid = threadIdx.x;
-    const int8_t* cls = cls_all + (size_t)u * L;
-    const int32_t* dest = dest_all + (size_t)u * cap_t;
-    const int per = (L + kLutThreads - 1) / kLutThreads;
-    const int s0 = min(L, tid * per), s1 = min(L, s0 + per);
-    // pass 1: counts of (important, tbm, lut entries) in this thread's segment.  A TBM
-    // token's destination is found through its TBM rank, so ranks are scanned first.
-    int ci = 0, ct = 0;
-    for (int i = s0; i < s1; ++i) ci += cls[i] == 2, ct += cls[i] == 1;
-    const int ri0 = block_incl_scan(ci, shs) - ci;
-    const int rt0 = block_incl_scan(ct, shs) - ct;
-    int cl = 0;
-    {
-        int rt = rt0;
-        for (int i = s0; i < s1; ++i) {
-            if (cls[i] == 2) ++cl;
-            else if (cls[i] == 1) cl += (zero_class || (rt < cap_t && dest[rt] >= 0)), ++rt;
-        }
+
+__device__ __forceinline__ int lower_bound_i32(const int32_t* __restrict__ a, int n, int x) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (a[mid] < x) lo = mid + 1;
+        else hi = mid;
     }
-    const int cl_incl = block_incl_scan(cl, shs);
-    int rl = cl_incl - cl, ri = ri0, rt = rt0;
+    return lo;
+}
+
+__global__ void __launch_bounds__(kLutThreads) compact_lut_kernel(
+    const int32_t* __restrict__ imp_idx_all, const int32_t* __restrict__ tbm_idx_all,
+    const int32_t* __restrict__ dest_all, const int32_t* __restrict__ counts, int cap_c, int cap_t, int cap_lut,
+    int zero_class, int64_t first_pos, int32_t* __restrict__ lut_pos, int32_t* __restrict__ lut_slot,
+    int32_t* __restrict__ out_counts, DevStatus* status, int unit_base) {
+    __shared__ int shs[32];
+    __shared__ int base[kLutThreads];
+    __shared__ int s_kept;
+    const int u = blockIdx.x, tid = threadIdx.x;
+    const int n_imp = counts[4 * u], n_tbm = cap_t > 0 ? counts[4 * u + 1] : 0;
+    const int32_t* imp = imp_idx_all + (size_t)u * cap_c;
+    const int32_t* tbm = tbm_idx_all + (size_t)u * (cap_t > 0 ? cap_t : 1);
+    const int32_t* dest = dest_all + (size_t)u * (cap_t > 0 ? cap_t : 1);
     int32_t* lp = lut_pos + (size_t)u * cap_lut;
     int32_t* ls = lut_slot + (size_t)u * cap_lut;
-    for (int i = s0; i < s1; ++i) {
-        if (cls[i] == 2) {
-            if (rl < cap_lut) {
-                lp[rl] = (int32_t)(first_pos + i);
-                ls[rl] = ri;
-            }
-            ++ri;
-            ++rl;
-        } else if (cls[i] == 1) {
-            const int dd = rt < cap_t ? dest[rt] : -2;
-            ++rt;
-            if (zero_class || dd >= 0) {
-                if (rl < cap_lut) {
-                    lp[rl] = (int32_t)(first_pos + i);
-                    ls[rl] = dd;  // -1 = zero class; anything < -1 or >= n_centers fails the check
-                }
-                ++rl;
-            }
+    auto keep = [&](int b) { return zero_class || dest[b] >= 0; };
+    // kept prefix over the TBM list: thread t owns the contiguous chunk [t C, t C + C)
+    const int C = (n_tbm + kLutThreads - 1) / kLutThreads;
+    const int t0 = min(n_tbm, tid * C), t1 = min(n_tbm, t0 + C);
+    int cnt = 0;
+    for (int b = t0; b < t1; ++b) cnt += keep(b);
+    const int incl = block_incl_scan(cnt, shs);
+    base[tid] = incl - cnt;
+    if (tid == kLutThreads - 1) s_kept = incl;
+    __syncthreads();
+    const int n_kept = s_kept, n_lut = n_imp + n_kept;
+    auto kept_before = [&](int p) {  // kept TBM entries among tbm[0, p)
+        if (p >= n_tbm) return n_kept;
+        const int ch = p / C;
+        int k = base[ch];
+        for (int b = ch * C; b < p; ++b) k += keep(b);
+        return k;
+    };
+    bool bad = n_lut > cap_lut;
+    // TBM entries (this thread's chunk, kept ones only)
+    for (int b = t0, k = base[tid]; b < t1; ++b) {
+        if (!keep(b)) continue;
+        const int r = k + lower_bound_i32(imp, n_imp, tbm[b]);
+        if (r < cap_lut) {
+            lp[r] = (int32_t)(first_pos + tbm[b]);
+            ls[r] = dest[b];  // -1 = zero class; anything < -1 or >= n_imp fails the check below
+        }
+        ++k;
+    }
+    // important entries: slot a = its rank in position order
+    for (int a = tid; a < n_imp; a += kLutThreads) {
+        const int r = a + kept_before(lower_bound_i32(tbm, n_tbm, imp[a]));
+        if (r < cap_lut) {
+            lp[r] = (int32_t)(first_pos + imp[a]);
+            ls[r] = a;
         }
     }
-    const int n_lut = __shfl_sync(0xffffffffu, cl_incl, 31);  // per warp: its last lane's count
-    if (tid == kLutThreads - 1) {
+    if (tid == 0) {
         int32_t* oc = out_counts + 4 * u;
-        oc[0] = counts[4 * u];
+        oc[0] = n_imp;
         oc[1] = counts[4 * u + 3];
-        oc[2] = cl_incl;  // the last thread's inclusive count = all LUT entries
+        oc[2] = n_lut;
         oc[3] = 1;
     }
-    // check_integrity over the whole LUT (entries written by other threads are visible after
-    // the barrier): this thread re-reads its own entries and the one before its first.
     __syncthreads();
-    const int n_centers = counts[4 * u];
-    const int r0 = cl_incl - cl;
-    bool bad = rl > cap_lut;
-    for (int r = r0; r < cl_incl && r < cap_lut; ++r) {
+    for (int r = tid; r < n_lut && r < cap_lut; r += kLutThreads) {
         const int sl = ls[r];
-        if (sl != -1 && (sl < 0 || sl >= n_centers)) bad = true;  // nonexistent slot
-        if (r > 0 && lp[r] <= lp[r - 1]) bad = true;              // not strictly increasing
+        if (sl != -1 && (sl < 0 || sl >= n_imp)) bad = true;  // nonexistent slot
+        if (r > 0 && lp[r] <= lp[r - 1]) bad = true;          // not strictly increasing
     }
-    (void)n_lut;
     if (bad) record_status(status, EMS_CORRUPTION, unit_base + u);
 }
 
@@ -211,10 +223,9 @@ cudaError_t launch_compact_t(const Dims& dm, const void* k, const void* v, const
         (const T*)k, (const T*)v, dm.L, glo, loc, sg.imp_idx, sg.part_counts, dm.cap_c, dm.cap_l,
         first_pos, (T*)c.center_key, c.center_norm, (T*)c.center_value, c.center_pos,
         c.center_score, (T*)c.local_key, (T*)c.local_value, c.local_pos, c.local_score);
-    compact_lut_kernel<<<dm.units, kLutThreads, 0, s>>>(dm.L, sg.cls, sg.dest, sg.part_counts,
-                                                        dm.cap_tbm, dm.cap_lut, zero_class,
-                                                        first_pos, c.lut_pos, c.lut_slot, c.counts,
-                                                        status, dm.unit_base);
+    compact_lut_kernel<<<dm.units, kLutThreads, 0, s>>>(sg.imp_idx, sg.tbm_idx, sg.dest, sg.part_counts, dm.cap_c,
+                                                        dm.cap_tbm, dm.cap_lut, zero_class, first_pos, c.lut_pos,
+                                                        c.lut_slot, c.counts, status, dm.unit_base);
     return cudaGetLastError();
 }
 

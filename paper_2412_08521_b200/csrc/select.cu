@@ -110,7 +110,8 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(
     int policy, int sink, int n_budget) {
     __shared__ double sh[32];
     __shared__ int hist[2][256];
-    __shared__ int sel_bin[2], sel_above[2];
+    __shared__ int sel_bin[2], sel_above[2], sel_one[2];
+    __shared__ unsigned long long hkey[2][256];
     __shared__ int scan[2][kSelThreads];
     __shared__ int degenerate;
     const int u = blockIdx.x;
@@ -170,9 +171,13 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(
     // 3. radix select of the k1-th and k2-th largest candidate keys
     const int n_cand = L - l_win;
     const int k1 = n_imp, k2 = n_imp + n_tbm;
+    // MSD radix select over the 64-bit keys, both cuts at once.  A bin that holds exactly one
+    // key resolves its cut: that key (recorded next to the histogram) is the cut, and the
+    // remaining passes are skipped (random fp32 scores typically resolve after 3 of the 8).
     unsigned long long pre[2] = {0ull, 0ull};
     int rem[2] = {k1, k2};
-    for (int pass = 0; pass < 8; ++pass) {
+    bool res[2] = {false, false};
+    for (int pass = 0; pass < 8 && !(res[0] && res[1]); ++pass) {
         const int shift = 56 - 8 * pass;
         const unsigned long long hi_mask = pass == 0 ? 0ull : (~0ull << (shift + 8));
         for (int e = tid; e < 512; e += kSelThreads) (&hist[0][0])[e] = 0;
@@ -180,17 +185,30 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(
         for (int i = tid; i < n_cand; i += kSelThreads) {
             const unsigned long long key = sel_key(pooled, i);
             const int bin = (int)((key >> shift) & 255ull);
-            if ((key & hi_mask) == pre[0]) atomicAdd(&hist[0][bin], 1);
-            if ((key & hi_mask) == pre[1]) atomicAdd(&hist[1][bin], 1);
+#pragma unroll
+            for (int t = 0; t < 2; ++t)
+                if (!res[t] && (key & hi_mask) == pre[t]) {
+                    atomicAdd(&hist[t][bin], 1);
+                    hkey[t][bin] = key;  // racy unless the bin ends up holding one key
+                }
         }
         __syncthreads();
         const int warp = tid >> 5;
-        if (warp < 2) find_bin(hist[warp], rem[warp], &sel_bin[warp], &sel_above[warp]);
+        if (warp < 2 && !res[warp]) {
+            find_bin(hist[warp], rem[warp], &sel_bin[warp], &sel_above[warp]);
+            __syncwarp();
+            if ((tid & 31) == 0) sel_one[warp] = hist[warp][sel_bin[warp]] == 1;
+        }
         __syncthreads();
 #pragma unroll
         for (int t = 0; t < 2; ++t) {
+            if (res[t]) continue;
             pre[t] |= (unsigned long long)sel_bin[t] << shift;
             rem[t] -= sel_above[t];
+            if (sel_one[t]) {
+                pre[t] = hkey[t][sel_bin[t]];
+                res[t] = true;
+            }
         }
         __syncthreads();
     }
@@ -277,6 +295,9 @@ __global__ void __cluster_dims__(kClu, 1, 1) __launch_bounds__(kCThreads) select
     __shared__ double sh[32];
     __shared__ double s_part[2];           // this CTA's alignment partials (read remotely)
     __shared__ int hist[2][2][256];        // [parity][target][bin] (read remotely)
+    __shared__ long long hkey[2][2][256];  // [parity][target][bin]: a key of that bin (read remotely)
+    __shared__ long long sel_key_v[2];
+    __shared__ int sel_one[2];
     __shared__ int s_cnt[2];               // this CTA's important / TBM counts (read remotely)
     __shared__ int scan[2][kCThreads];
     __shared__ int sel_bin[2], sel_above[2];
@@ -338,7 +359,8 @@ __global__ void __cluster_dims__(kClu, 1, 1) __launch_bounds__(kCThreads) select
     const int e0 = min(n_cand, c0), e1 = min(n_cand, c1);
     unsigned long long pre[2] = {0ull, 0ull};
     int rem[2] = {n_imp, n_imp + n_tbm};
-    for (int pass = 0; pass < 8; ++pass) {
+    bool res[2] = {false, false};  // cut resolved early (a bin holding exactly one key)
+    for (int pass = 0; pass < 8 && !(res[0] && res[1]); ++pass) {
         const int par = pass & 1;
         const int shift = 56 - 8 * pass;
         const unsigned long long hi_mask = pass == 0 ? 0ull : (~0ull << (shift + 8));
@@ -347,8 +369,12 @@ __global__ void __cluster_dims__(kClu, 1, 1) __launch_bounds__(kCThreads) select
         for (int i = e0 + tid; i < e1; i += kCThreads) {
             const unsigned long long key = sel_key(pooled, i);
             const int bin = (int)((key >> shift) & 255ull);
-            if ((key & hi_mask) == pre[0]) atomicAdd(&hist[par][0][bin], 1);
-            if ((key & hi_mask) == pre[1]) atomicAdd(&hist[par][1][bin], 1);
+#pragma unroll
+            for (int t = 0; t < 2; ++t)
+                if (!res[t] && (key & hi_mask) == pre[t]) {
+                    atomicAdd(&hist[par][t][bin], 1);
+                    hkey[par][t][bin] = (long long)key;  // racy unless this CTA holds one key there
+                }
         }
         cl_sync();  // every CTA's histogram complete (and last pass's reads done: other parity)
         // global histogram = sum over the cluster, in rank order (all CTAs compute the same)
@@ -359,12 +385,27 @@ __global__ void __cluster_dims__(kClu, 1, 1) __launch_bounds__(kCThreads) select
         }
         __syncthreads();
         const int warp = tid >> 5;
-        if (warp < 2) find_bin(&scan[0][256 * warp], rem[warp], &sel_bin[warp], &sel_above[warp]);
+        if (warp < 2 && !res[warp]) {
+            find_bin(&scan[0][256 * warp], rem[warp], &sel_bin[warp], &sel_above[warp]);
+            __syncwarp();
+            if ((tid & 31) == 0) {
+                const int bin = sel_bin[warp];
+                sel_one[warp] = scan[0][256 * warp + bin] == 1;
+                if (sel_one[warp])  // the single key lives in the one CTA whose count is 1
+                    for (int r = 0; r < kClu; ++r)
+                        if (ld_dsm_i32(&hist[par][warp][bin], r) == 1) sel_key_v[warp] = ld_dsm_i64(&hkey[par][warp][bin], r);
+            }
+        }
         __syncthreads();
 #pragma unroll
         for (int t = 0; t < 2; ++t) {
+            if (res[t]) continue;
             pre[t] |= (unsigned long long)sel_bin[t] << shift;
             rem[t] -= sel_above[t];
+            if (sel_one[t]) {
+                pre[t] = (unsigned long long)sel_key_v[t];
+                res[t] = true;
+            }
         }
         __syncthreads();
     }
