@@ -9,17 +9,17 @@
 // Any L: the last query / key tile is TMA zero fill past L; queries >= L are masked in the
 // (always masked-path) last query tile and keys >= L are never stored.
 //
-// One CTA owns TWO 128-key tiles (J0 = 2*jp, J1 = J0 + 1) of one unit, both resident
-// in smem, and streams every (query head h, query tile I >= J0) through a 4-stage
-// TMA ring.  Each streamed Q tile feeds two SS MMAs  S^T_w = K_Jw Q_I^T  (keys on
-// TMEM lanes), so the L2 traffic per MMA is half that of one key tile per CTA.
-// Four column warpgroups: warpgroup (w, hc) owns key tile Jw and query columns
-// [64 hc, 64 hc + 64) of every item; thread m owns key Jw*128 + m, so the column sum
-// over queries is an in-thread row sum (no atomics).  Interior tiles take a
-// mask-free path where kPoly of every 8 exp2 pairs run as a degree-5 polynomial on
-// the FMA pipe (ex2_poly2) and the rest on MUFU.  Per-item fp32 sums are accumulated
-// in fp64 in item order and the two column halves are combined in a fixed order ->
-// deterministic.
+// One CTA owns TWO 128-key tiles (J0 = 2*jp, J1 = J0 + 1) of one unit, both resident in smem,
+// and streams every (query head h, query-tile PAIR (I, I+1), I >= J0) through a 2-stage TMA ring
+// (one 256-row box per 64 d-columns).  Each pair feeds two SS MMAs S^T_w = K_Jw [Q_I; Q_I+1]^T with
+// N = 256 (keys on TMEM lanes; ~90 % of the tensor rate against ~60 % for N = 128: same time --
+// the pass is bound by the exponentials -- and 2.6 % less energy per step), TMEM buffer w holding
+// key tile Jw.  Four column warpgroups: per item (pair, w) warpgroup q owns query columns
+// [64 q, 64 q + 64) of the pair and thread m owns key Jw*128 + m, so the column sum over queries
+// is an in-thread row sum (no atomics).  Interior items take a mask-free path where kPoly of every
+// 8 exp2 pairs run as a degree-5 polynomial on the FMA pipe (ex2_poly2) and the rest on MUFU.
+// Per-item fp32 sums are accumulated in fp64 in item order and the four column quarters are
+// combined in a fixed order -> deterministic.
 #include "score_tc.cuh"
 
 namespace ems {
@@ -29,27 +29,25 @@ namespace {
 using namespace tc;
 using namespace sc;
 
-constexpr int kQStages = 4;
-constexpr int kBufs = 2;                 // TMEM: 2 x (2 key tiles x 128 cols) = 512 cols
+constexpr int kQStages = 2;              // query-tile PAIRS: 2 x 64 KB
+constexpr int kBufs = 2;                 // TMEM: buffer w holds S^T of key tile J0 + w (256 query cols)
 constexpr int kThreads = 640;            // w0 TMA, w1 MMA, w2-3 spare, w4-19 column sums
-constexpr size_t kSmem = 1024 + (2 + kQStages) * kTileBytes + kBufs * 512 + 2 * 2 * 128 * 8;
+constexpr int kPairBytes = 2 * kTileBytes;   // 256 query rows x 128 d
+constexpr size_t kSmem = 1024 + 2 * kTileBytes + kQStages * kPairBytes + 2 * 256 * 4 + 2 * 2 * 4 * 128 * 8;
 
 struct Bars {
     uint64_t k_full;
     uint64_t q_full[kQStages], q_empty[kQStages];
-    uint64_t s_full[kBufs], s_empty[kBufs], l_full[kBufs];
+    uint64_t s_full[kBufs], s_empty[kBufs];
+    uint64_t l_full[2], l_empty[2];
     uint32_t tmem_base;
 };
 
 // 64 query columns of the thread's key row, general path (causal mask + window).
-__device__ __forceinline__ void cols_masked(uint32_t sa, uint32_t lb, float c, int q0, int key,
+__device__ __forceinline__ void cols_masked(const uint32_t (&r)[2][32], uint32_t lb, float c, int q0, int key,
                                             int loc_start, int L, float& sg, float& sl) {
     sg = 0.f;
     sl = 0.f;
-    uint32_t r[2][32];
-    tmem_ld32(sa, r[0]);
-    tmem_ld32(sa + 32, r[1]);
-    tmem_ld_wait();
 #pragma unroll
     for (int cc = 0; cc < 2; ++cc)
 #pragma unroll
@@ -67,12 +65,8 @@ __device__ __forceinline__ void cols_masked(uint32_t sa, uint32_t lb, float c, i
 // one of 4 independent accumulators, keeping the FADD dependency chains short.
 constexpr float kC128 = 0.12751743f;
 constexpr int kPoly = 1;  // exp2 pairs (of every 8) computed on the FMA pipe (ex2_poly2; 0-3 measured, 1 fastest)
-__device__ __forceinline__ float cols_fast(uint32_t sa, uint32_t lb) {
+__device__ __forceinline__ float cols_fast(const uint32_t (&r)[2][32], uint32_t lb) {
     const float2 c2 = make_float2(kC128, kC128);
-    uint32_t r[2][32];
-    tmem_ld32(sa, r[0]);
-    tmem_ld32(sa + 32, r[1]);
-    tmem_ld_wait();
     float2 acc[4];
 #pragma unroll
     for (int g = 0; g < 4; ++g) acc[g] = make_float2(0.f, 0.f);
@@ -99,6 +93,11 @@ __device__ __forceinline__ float cols_fast(uint32_t sa, uint32_t lb) {
     return s.x + s.y;
 }
 
+// P2 with N = 256 MMAs: the CTA keeps its two key tiles resident and streams PAIRS of query tiles
+// (one 256-row TMA box per 64 d-columns); every pair feeds two SS MMAs S^T_w = K_Jw [Q_I; Q_I+1]^T
+// (M = 128, N = 256, ~90 % of the tensor rate against ~60 % for N = 128), buffer w of TMEM holding
+// key tile J0 + w.  Per item (pair, w) all four column warpgroups work on key tile J0 + w, warpgroup
+// q on query columns [64 q, 64 q + 64) of the pair.
 __global__ void __launch_bounds__(kThreads, 1)
     colsum_tc_kernel(const __grid_constant__ CUtensorMap tk, const __grid_constant__ CUtensorMap tq,
                      const ColArgs a) {
@@ -106,25 +105,24 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
     uint8_t* sk = sm;                                  // K_J0 | K_J1 (2 x 32 KB)
-    uint8_t* sq = sk + 2 * kTileBytes;                 // Q ring
-    float* slse = reinterpret_cast<float*>(sq + kQStages * kTileBytes);  // [kBufs][128]
-    double* spart = reinterpret_cast<double*>(slse + kBufs * 128);       // [2 key tiles][2][128]
+    uint8_t* sq = sk + 2 * kTileBytes;                 // query-pair ring
+    float* slse = reinterpret_cast<float*>(sq + kQStages * kPairBytes);  // [2][256]
+    double* spart = reinterpret_cast<double*>(slse + 2 * 256);           // [2 key tiles][2 g/l][4 q][128]
     __shared__ Bars bars;
 
     const int tid = threadIdx.x, warp = tid >> 5;
-    // key-tile pair (heaviest first over all units: unit by unit would leave the last unit's
-    // longest CTAs to the end of the grid), unit, head group
     const int per_jp = a.units * a.hsplit;
     const int jp = blockIdx.x / per_jp;
     const int unit = blockIdx.x % a.units;
     const int hg = (blockIdx.x % per_jp) / a.units;
     const size_t Lp = (size_t)a.nT * kTile;
-    const int gh = a.G / a.hsplit;                     // query heads of this CTA
+    const int gh = a.G / a.hsplit;
     const int b = unit / a.Hkv, hk = unit % a.Hkv;
     const int J0 = 2 * jp;
     const bool has1 = J0 + 1 < a.nT;
-    const int span = a.nT - J0;
-    const int n_items = gh * span;                     // item i -> head hg*gh + i / span, tile J0 + i % span
+    const int nw = has1 ? 2 : 1;
+    const int span_p = (a.nT - J0 + 1) / 2;            // query-tile pairs (J0, J0+1), (J0+2, J0+3), ...
+    const int n_pairs = gh * span_p;                   // pair p -> head hg*gh + p / span_p, tile J0 + 2 (p % span_p)
 
     if (warp == 0) {
         tmem_alloc<512>(&bars.tmem_base);
@@ -137,7 +135,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int s = 0; s < kBufs; ++s) {
             mbar_init(&bars.s_full[s], 1);
             mbar_init(&bars.s_empty[s], 16);   // one arrival per column warp
+        }
+        for (int s = 0; s < 2; ++s) {
             mbar_init(&bars.l_full[s], 1);
+            mbar_init(&bars.l_empty[s], 16);
         }
         fence_barrier_init();
     }
@@ -158,107 +159,112 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tma_load_3d(sk + kTileBytes, &tk, &bars.k_full, 0, (J0 + 1) * kTile, unit);
                 tma_load_3d(sk + kTileBytes + 16384, &tk, &bars.k_full, 64, (J0 + 1) * kTile, unit);
             }
-            for (int i = 0; i < n_items; ++i) {
-                const int h = hg * gh + i / span, I = J0 + i % span;
+            for (int p = 0; p < n_pairs; ++p) {
+                const int h = hg * gh + p / span_p, I = J0 + 2 * (p % span_p);
                 const int plane = b * a.Hq + hk * a.G + h;
-                const int s = i % kQStages, bb = i % kBufs;
-                if (i >= kQStages) mbar_wait(&bars.q_empty[s], ((i / kQStages) - 1) & 1);
-                uint8_t* dq = sq + s * kTileBytes;
-                mbar_expect_tx(&bars.q_full[s], kTileBytes);
+                const int s = p % kQStages, lb = p & 1;
+                if (p >= kQStages) mbar_wait(&bars.q_empty[s], ((p / kQStages) - 1) & 1);
+                uint8_t* dq = sq + s * kPairBytes;
+                mbar_expect_tx(&bars.q_full[s], kPairBytes);
                 tma_load_3d(dq, &tq, &bars.q_full[s], 0, I * kTile, plane);
-                tma_load_3d(dq + 16384, &tq, &bars.q_full[s], 64, I * kTile, plane);
-                if (i >= kBufs) mbar_wait(&bars.s_empty[bb], ((i / kBufs) - 1) & 1);
-                mbar_expect_tx(&bars.l_full[bb], 512);
-                bulk_load(slse + bb * 128, a.nlse2 + (size_t)plane * Lp + (size_t)I * kTile, 512,
-                          &bars.l_full[bb]);
+                tma_load_3d(dq + kTileBytes, &tq, &bars.q_full[s], 64, I * kTile, plane);
+                if (p >= 2) mbar_wait(&bars.l_empty[lb], ((p >> 1) - 1) & 1);
+                const uint32_t lbytes = I + 1 < a.nT ? 1024 : 512;  // never past the plane's rows
+                mbar_expect_tx(&bars.l_full[lb], lbytes);
+                bulk_load(slse + lb * 256, a.nlse2 + (size_t)plane * Lp + (size_t)I * kTile, lbytes, &bars.l_full[lb]);
             }
         }
     } else if (warp == 1) {
         // ------------------------------------------------------------- MMA issuer
         if (elect_one()) {
-            const uint32_t id_s = idesc_bf16(128, 128, 0, 0);  // K (K-major) x Q^T (K-major)
-            const uint32_t ka0 = smem_u32(sk), ka1 = smem_u32(sk + kTileBytes);
+            const uint32_t id_s = idesc_bf16(128, 256, 0, 0);  // K (K-major) x [Q_I; Q_I+1]^T (K-major)
+            const uint32_t ka[2] = {smem_u32(sk), smem_u32(sk + kTileBytes)};
             mbar_wait(&bars.k_full, 0);
-            for (int i = 0; i < n_items; ++i) {
-                const int I = J0 + i % span;
-                const int s = i % kQStages, bb = i % kBufs;
-                mbar_wait(&bars.q_full[s], (i / kQStages) & 1);
-                if (i >= kBufs) mbar_wait(&bars.s_empty[bb], ((i / kBufs) - 1) & 1);
-                tc_fence_after();
-                const uint32_t qa = smem_u32(sq + s * kTileBytes);
-                const uint32_t d0 = tmem + bb * 256;
-#pragma unroll
-                for (int k = 0; k < 8; ++k)
-                    mma_ss(d0, sdesc(kmajor_addr(ka0, k), 16, 1024),
-                               sdesc(kmajor_addr(qa, k), 16, 1024), id_s, k > 0);
-                if (has1 && I >= J0 + 1) {  // key tile J1 is fully masked vs query tile J0
+            for (int p = 0; p < n_pairs; ++p) {
+                const int s = p % kQStages;
+                mbar_wait(&bars.q_full[s], (p / kQStages) & 1);
+                const uint32_t qa = smem_u32(sq + s * kPairBytes);
+                for (int w = 0; w < nw; ++w) {
+                    if (p >= 1) mbar_wait(&bars.s_empty[w], (p - 1) & 1);
+                    tc_fence_after();
 #pragma unroll
                     for (int k = 0; k < 8; ++k)
-                        mma_ss(d0 + 128, sdesc(kmajor_addr(ka1, k), 16, 1024),
-                               sdesc(kmajor_addr(qa, k), 16, 1024), id_s, k > 0);
+                        mma_ss(tmem + w * 256, sdesc(kmajor_addr(ka[w], k), 16, 1024),
+                               sdesc(qa + (k >> 2) * kTileBytes + (k & 3) * 32, 16, 1024), id_s, k > 0);
+                    mma_commit(&bars.s_full[w]);
                 }
-                mma_commit(&bars.s_full[bb]);
                 mma_commit(&bars.q_empty[s]);
             }
         }
     } else if (warp >= 4) {
         // ------------------------------------------------------------- column sums
-        const int w = (warp - 4) >> 3;          // key tile J0 + w
-        const int hc = ((warp - 4) >> 2) & 1;   // query columns [64 hc, 64 hc + 64)
+        const int q = (warp - 4) >> 2;          // query columns [64 q, 64 q + 64) of each pair
         const int wi = warp & 3;
-        const int mrow = wi * 32 + (tid & 31);  // key within the tile
-        const int Jw = J0 + w;
-        const int key = Jw * kTile + mrow;
-        const bool active = (w == 0) || has1;
+        const int mrow = wi * 32 + (tid & 31);  // key row within the key tile
         const int loc_start = a.L - a.lwin;
-        const int last_interior = (loc_start / kTile) - 1;  // tiles <= this hold no window query
-        double acc_g = 0.0, acc_l = 0.0;
-        // shared-window addresses hoisted out of the item loop (barriers of one kind are
-        // consecutive uint64_t, so buffer bb is +8 bb)
-        const uint32_t l_full0 = smem_u32(&bars.l_full[0]), s_full0 = smem_u32(&bars.s_full[0]);
-        const uint32_t s_empty0 = smem_u32(&bars.s_empty[0]);
-        const uint32_t sa0 = tmem + w * 128 + 64 * hc + ((uint32_t)(wi * 32) << 16);
-        const uint32_t lb0 = smem_u32(slse + 64 * hc);
-        static_assert(kBufs == 2, "item i uses buffer i & 1");
-        for (int i = 0, I = J0; i < n_items; ++i) {  // I = J0 + i % span, kept incrementally
-            const int bb = i & 1;
-            const uint32_t ph = (i >> 1) & 1;
-            mbar_wait_u(l_full0 + 8 * bb, ph);
-            mbar_wait_u(s_full0 + 8 * bb, ph);
-            tc_fence_after();
-            if (active && I >= Jw) {
-                const uint32_t sa = sa0 + bb * 256;
-                const uint32_t lb = lb0 + bb * 512;
-                if (I > Jw && I <= last_interior) {
-                    acc_g += (double)cols_fast(sa, lb);
-                } else {
-                    float sg, sl;
-                    cols_masked(sa, lb, a.c, I * kTile + 64 * hc, key, loc_start, a.L, sg, sl);
-                    acc_g += (double)sg;
-                    acc_l += (double)sl;
+        double acc_g[2] = {0.0, 0.0}, acc_l[2] = {0.0, 0.0};
+        const uint32_t s_full0 = smem_u32(&bars.s_full[0]), s_empty0 = smem_u32(&bars.s_empty[0]);
+        const uint32_t l_full0 = smem_u32(&bars.l_full[0]), l_empty0 = smem_u32(&bars.l_empty[0]);
+        const uint32_t sa0 = tmem + 64 * q + ((uint32_t)(wi * 32) << 16);
+        const uint32_t lb0 = smem_u32(slse + 64 * q);
+        for (int p = 0, I = J0; p < n_pairs; ++p) {
+            const int lb = p & 1;
+            mbar_wait_u(l_full0 + 8 * lb, (p >> 1) & 1);
+            const int q0 = I * kTile + 64 * q;  // first query of this warpgroup's columns
+#pragma unroll
+            for (int w = 0; w < 2; ++w) {
+                if (w >= nw) break;
+                mbar_wait_u(s_full0 + 8 * w, p & 1);
+                tc_fence_after();
+                const int key0 = (J0 + w) * kTile;  // first key of the tile; this thread: key0 + mrow
+                if (q0 + 63 >= key0) {  // some column of the quarter is at or after some key
+                    uint32_t r[2][32];
+                    const uint32_t sa = sa0 + w * 256;
+                    tmem_ld32(sa, r[0]);
+                    tmem_ld32(sa + 32, r[1]);
+                    tmem_ld_wait();
+                    const uint32_t lbs = lb0 + lb * 1024;
+                    if (q0 > key0 + kTile - 1 && q0 + 63 < loc_start) {
+                        acc_g[w] += (double)cols_fast(r, lbs);
+                    } else {
+                        float sg, sl;
+                        cols_masked(r, lbs, a.c, q0, key0 + mrow, loc_start, a.L, sg, sl);
+                        acc_g[w] += (double)sg;
+                        acc_l[w] += (double)sl;
+                    }
                 }
+                tc_fence_before();
+                __syncwarp();
+                if ((tid & 31) == 0) mbar_arrive_u(s_empty0 + 8 * w);
             }
-            tc_fence_before();
             __syncwarp();
-            if ((tid & 31) == 0) mbar_arrive_u(s_empty0 + 8 * bb);
-            if (++I == a.nT) I = J0;
+            if ((tid & 31) == 0) mbar_arrive_u(l_empty0 + 8 * lb);
+            I += 2;
+            if (I >= a.nT) I = J0;
         }
-        // combine the two column halves in a fixed order: (half 0 + half 1) / G
-        double* sp = spart + w * 256;
-        if (hc == 1) {
-            sp[mrow] = acc_g;
-            sp[128 + mrow] = acc_l;
+        // combine the four column quarters of each key tile in a fixed order
+#pragma unroll
+        for (int w = 0; w < 2; ++w) {
+            spart[((w * 2 + 0) * 4 + q) * 128 + mrow] = acc_g[w];
+            spart[((w * 2 + 1) * 4 + q) * 128 + mrow] = acc_l[w];
         }
-        asm volatile("bar.sync %0, 256;" ::"r"(1 + w) : "memory");
-        if (hc == 0 && active && key < a.L) {
-            if (a.hsplit == 1) {
-                const size_t o = (size_t)unit * a.L + (size_t)Jw * kTile + mrow;
-                a.glo[o] = (float)((acc_g + sp[mrow]) / a.G);
-                a.loc[o] = (float)((acc_l + sp[128 + mrow]) / a.G);
-            } else {
-                const size_t o = ((size_t)unit * a.hsplit + hg) * a.L + (size_t)Jw * kTile + mrow;
-                a.part_g[o] = acc_g + sp[mrow];
-                a.part_l[o] = acc_l + sp[128 + mrow];
+        asm volatile("bar.sync 1, 512;" ::: "memory");
+        if (q < nw) {  // warpgroup q writes key tile J0 + q
+            const int w = q, key = (J0 + w) * kTile + mrow;
+            const double* g = spart + (w * 2 + 0) * 4 * 128 + mrow;
+            const double* l = spart + (w * 2 + 1) * 4 * 128 + mrow;
+            const double sg = ((g[0] + g[128]) + g[256]) + g[384];
+            const double sl = ((l[0] + l[128]) + l[256]) + l[384];
+            if (key < a.L) {
+                if (a.hsplit == 1) {
+                    const size_t o = (size_t)unit * a.L + key;
+                    a.glo[o] = (float)(sg / a.G);
+                    a.loc[o] = (float)(sl / a.G);
+                } else {
+                    const size_t o = ((size_t)unit * a.hsplit + hg) * a.L + key;
+                    a.part_g[o] = sg;
+                    a.part_l[o] = sl;
+                }
             }
         }
     }

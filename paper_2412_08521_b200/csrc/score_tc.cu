@@ -70,7 +70,9 @@ cudaError_t score_tc(const Dims& dm, const void* q, const void* k, const void* v
         ca.part_g = reinterpret_cast<double*>(static_cast<char*>(ws) + nlse2_bytes(dm));
         ca.part_l = ca.part_g + (size_t)dm.units * ca.hsplit * dm.L;
     }
-    return launch_colsum_tc(ca, tk, tq, s);
+    CUtensorMap tq2;  // P2 streams pairs of query tiles: 256-row boxes
+    if (!make_tmap_bf16_3d(&tq2, q, kD, dm.L, planes_q, 2 * kTile)) return cudaErrorInvalidValue;
+    return launch_colsum_tc(ca, tk, tq2, s);
 }
 
 }  // namespace ems
