@@ -540,12 +540,14 @@ namespace {
 // public entry points and the chunked host pipeline).
 int run_path(const ems_desc* d, const void* q_rot, const void* k_rot, const void* k_raw,
              const void* v, void* out_o, float* lse, float* glo, float* loc, const ems_stage* st,
-             const ems_cache& c, void* ws, cudaStream_t s, int unit_base = 0) {
+             const ems_cache& c, void* ws, cudaStream_t s, int unit_base = 0,
+             cudaEvent_t after_score = nullptr) {
     const Layout l = layout(*d);
     float* g = glo ? glo : at<float>(ws, l.glo);
     float* lc = loc ? loc : at<float>(ws, l.loc);
     const ems_stage sg = st ? *st : default_stage(*d, ws);
     if (int rc = run_score(d, q_rot, k_rot, v, out_o, lse, g, lc, ws, s)) return rc;
+    if (after_score) EMS_CUDA_CHECK(cudaEventRecord(after_score, s));  // O (and the LSE) are final here
     if (d->seq_len > d->n_budget && d->policy != EMS_POLICY_FULL) {  // policies.cpp:136-138
         if (int rc = run_select(d, g, lc, sg, ws, s, unit_base)) return rc;
         if (int rc = run_merge(d, k_raw, v, sg, ws, s)) return rc;
@@ -715,6 +717,7 @@ struct HostPipeRes {
     int device = -1;
     cudaStream_t copy = nullptr;
     cudaStream_t comp2 = nullptr;  // second compute stream (two unit groups in flight)
+    cudaStream_t d2h = nullptr;    // device-to-host copies (the other PCIe direction than `copy`)
     std::vector<cudaEvent_t> ev;
 };
 
@@ -731,6 +734,8 @@ HostPipeRes* pipe_res(int nev) {
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return nullptr;
     HostPipeRes& r = g_pipe[dev];
     if (r.copy == nullptr && cudaStreamCreateWithFlags(&r.copy, cudaStreamNonBlocking) != cudaSuccess)
+        return nullptr;
+    if (r.d2h == nullptr && cudaStreamCreateWithFlags(&r.d2h, cudaStreamNonBlocking) != cudaSuccess)
         return nullptr;
     if (r.comp2 == nullptr && cudaStreamCreateWithFlags(&r.comp2, cudaStreamNonBlocking) != cudaSuccess)
         return nullptr;
@@ -781,13 +786,17 @@ extern "C" int ems_prefill_host(const ems_desc* d, double rope_base, const void*
     const Dims m = make_dims(*d);
     const int U = m.units, G = m.G;
     int nc = chunks < 1 ? 1 : (chunks > U ? U : chunks);
-    HostPipeRes* res = pipe_res(2 * nc + 4);
+    HostPipeRes* res = pipe_res(3 * nc + 4);
     if (!res) {
         set_error("ems_prefill_host: could not create copy stream / events");
         return EMS_CUDA_ERROR;
     }
     cudaStream_t cs = copy_stream ? copy_stream : res->copy;
-    cudaEvent_t* ev = res->ev.data();  // [0, nc): inputs of chunk c staged; [nc, 2nc): chunk c done
+    cudaStream_t ds = res->d2h;  // results go back on their own stream: both PCIe directions at once
+    // [0, nc): inputs of chunk c staged; [nc, 2nc): chunk c done; [2nc, 2nc + 3): start / copies
+    // done / second stream done; [2nc + 3, 3nc + 3): chunk c's score pass done (O final)
+    cudaEvent_t* ev = res->ev.data();
+    cudaEvent_t* ev_o = ev + 2 * nc + 3;
     const size_t row = (size_t)m.L * m.d * m.esize;  // one [L][d] plane
     const size_t cache_d = (size_t)m.d * m.esize;
     const CacheField fields[] = {
@@ -874,22 +883,29 @@ extern "C" int ems_prefill_host(const ems_desc* d, double rope_base, const void*
             for (const CacheField& f : fields) scache.*f.ptr = off(d_cache->*f.ptr, (size_t)u0 * f.per_unit);
             const size_t ol = (size_t)u0 * m.L;
             if (int rc = run_path(&sub, qr, kr, kraw, off(d_v, ok), off(out_o, oq), off(lse, (size_t)u0 * G * m.L * 4),
-                                  off(glo, ol * 4), off(loc, ol * 4), nullptr, scache, wsc, sc, u0))
+                                  off(glo, ol * 4), off(loc, ol * 4), nullptr, scache, wsc, sc, u0,
+                                  h_out_o ? ev_o[c] : nullptr))
                 return rc;
             EMS_CUDA_CHECK(cudaEventRecord(ev[nc + c], sc));
-            if (h_cache || h_out_o) EMS_CUDA_CHECK(cudaStreamWaitEvent(cs, ev[nc + c], 0));
-            if (h_cache)
+            if (h_out_o) {  // engine::prefill's PrefillResult.per_head outputs (engine.hpp:36-45): O is final
+                            // after the forward pass, so its copy overlaps this group's column sums and compress
+                EMS_CUDA_CHECK(cudaStreamWaitEvent(ds, ev_o[c], 0));
+                EMS_CUDA_CHECK(cudaMemcpyAsync(off(h_out_o, oq), off(out_o, oq), (size_t)n * G * row,
+                                               cudaMemcpyDeviceToHost, ds));
+            }
+            if (h_cache) {
+                EMS_CUDA_CHECK(cudaStreamWaitEvent(ds, ev[nc + c], 0));
                 for (const CacheField& f : fields)
                     EMS_CUDA_CHECK(cudaMemcpyAsync(off(h_cache->*f.ptr, (size_t)u0 * f.per_unit), scache.*f.ptr,
-                                                   (size_t)n * f.per_unit, cudaMemcpyDeviceToHost, cs));
-            if (h_out_o)  // engine::prefill's PrefillResult.per_head outputs (engine.hpp:36-45)
-                EMS_CUDA_CHECK(cudaMemcpyAsync(off(h_out_o, oq), off(out_o, oq), (size_t)n * G * row,
-                                               cudaMemcpyDeviceToHost, cs));
+                                                   (size_t)n * f.per_unit, cudaMemcpyDeviceToHost, ds));
+            }
         }
         return EMS_OK;
     }();
     cudaEventRecord(ev[2 * nc + 1], cs);
     cudaStreamWaitEvent(s, ev[2 * nc + 1], 0);
+    cudaEventRecord(ev[2 * nc], ds);  // the start event's slot is free again: reuse it for the D2H stream
+    cudaStreamWaitEvent(s, ev[2 * nc], 0);
     if (dual) {
         cudaEventRecord(ev[2 * nc + 2], s2);
         cudaStreamWaitEvent(s, ev[2 * nc + 2], 0);
