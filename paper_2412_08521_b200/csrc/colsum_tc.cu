@@ -33,18 +33,21 @@ constexpr int kQStages = 2;              // query-tile PAIRS: 2 x 64 KB
 constexpr int kBufs = 2;                 // TMEM: buffer w holds S^T of key tile J0 + w (256 query cols)
 constexpr int kThreads = 640;            // w0 TMA, w1 MMA, w2-3 spare, w4-19 column sums
 constexpr int kPairBytes = 2 * kTileBytes;   // 256 query rows x 128 d
-constexpr size_t kSmem = 1024 + 2 * kTileBytes + kQStages * kPairBytes + 2 * 256 * 4 + 2 * 2 * 4 * 128 * 8;
+constexpr int kQxBytes = 256 * 32;           // the pair's qx rows: 256 x 16 bf16 (SWIZZLE_32B)
+constexpr int kStageBytes = kPairBytes + kQxBytes;
+constexpr int kOnesBytes = 128 * 32;         // K's extra columns: 128 x 16 bf16 ones
+constexpr size_t kSmem = 1024 + 2 * kTileBytes + kOnesBytes + kQStages * kStageBytes;
+static_assert(2 * 2 * 4 * 128 * 8 <= kQStages * kStageBytes, "the final combine reuses the Q ring");
 
 struct Bars {
     uint64_t k_full;
     uint64_t q_full[kQStages], q_empty[kQStages];
     uint64_t s_full[kBufs], s_empty[kBufs];
-    uint64_t l_full[2], l_empty[2];
     uint32_t tmem_base;
 };
 
 // 64 query columns of the thread's key row, general path (causal mask + window).
-__device__ __forceinline__ void cols_masked(const uint32_t (&r)[2][32], uint32_t lb, float c, int q0, int key,
+__device__ __forceinline__ void cols_masked(const uint32_t (&r)[2][32], float c, int q0, int key,
                                             int loc_start, int L, float& sg, float& sl) {
     sg = 0.f;
     sl = 0.f;
@@ -53,7 +56,7 @@ __device__ __forceinline__ void cols_masked(const uint32_t (&r)[2][32], uint32_t
 #pragma unroll
         for (int x = 0; x < 32; ++x) {
             const int n = cc * 32 + x, qi = q0 + n;
-            float p = ex2(fmaf(__uint_as_float(r[cc][x]), c, lds32(lb + 4 * n)));
+            float p = ex2(__uint_as_float(r[cc][x]) * c);  // S' c = s c - lse2 (qx fold)
             if (qi < key || qi >= L) p = 0.f;  // query before key, or padding row past L: masked
             sg += p;
             if (qi >= loc_start) sl += p;
@@ -64,8 +67,8 @@ __device__ __forceinline__ void cols_masked(const uint32_t (&r)[2][32], uint32_t
 // tensor-core path is d = 128 only); groups of 4 pairs are tree-summed before entering
 // one of 4 independent accumulators, keeping the FADD dependency chains short.
 constexpr float kC128 = 0.12751743f;
-constexpr int kPoly = 1;  // exp2 pairs (of every 8) computed on the FMA pipe (ex2_poly2; 0-3 measured, 1 fastest)
-__device__ __forceinline__ float cols_fast(const uint32_t (&r)[2][32], uint32_t lb) {
+constexpr int kPoly = 2;  // exp2 pairs (of every 8) computed on the FMA pipe (ex2_poly2; 0-3 measured, 2 fastest)
+__device__ __forceinline__ float cols_fast(const uint32_t (&r)[2][32]) {
     const float2 c2 = make_float2(kC128, kC128);
     float2 acc[4];
 #pragma unroll
@@ -74,15 +77,11 @@ __device__ __forceinline__ float cols_fast(const uint32_t (&r)[2][32], uint32_t 
     for (int cc = 0; cc < 2; ++cc) {
 #pragma unroll
         for (int x = 0; x < 32; x += 8) {
-            const float4 l0 = lds128(lb + 4 * (cc * 32 + x));
-            const float4 l1 = lds128(lb + 4 * (cc * 32 + x + 4));
-            const float2 lv[4] = {make_float2(l0.x, l0.y), make_float2(l0.z, l0.w), make_float2(l1.x, l1.y),
-                                  make_float2(l1.z, l1.w)};
             float2 p[4];
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-                const float2 arg = __ffma2_rn(
-                    make_float2(__uint_as_float(r[cc][x + 2 * e]), __uint_as_float(r[cc][x + 2 * e + 1])), c2, lv[e]);
+                const float2 arg = __fmul2_rn(
+                    make_float2(__uint_as_float(r[cc][x + 2 * e]), __uint_as_float(r[cc][x + 2 * e + 1])), c2);
                 p[e] = ((x / 2 + e) & 7) < kPoly ? ex2_poly2(arg) : make_float2(ex2(arg.x), ex2(arg.y));
             }
             const int g = (x / 8) & 3;
@@ -100,14 +99,14 @@ __device__ __forceinline__ float cols_fast(const uint32_t (&r)[2][32], uint32_t 
 // q on query columns [64 q, 64 q + 64) of the pair.
 __global__ void __launch_bounds__(kThreads, 1)
     colsum_tc_kernel(const __grid_constant__ CUtensorMap tk, const __grid_constant__ CUtensorMap tq,
-                     const ColArgs a) {
+                     const __grid_constant__ CUtensorMap tqx, const ColArgs a) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
     uint8_t* sk = sm;                                  // K_J0 | K_J1 (2 x 32 KB)
-    uint8_t* sq = sk + 2 * kTileBytes;                 // query-pair ring
-    float* slse = reinterpret_cast<float*>(sq + kQStages * kPairBytes);  // [2][256]
-    double* spart = reinterpret_cast<double*>(slse + 2 * 256);           // [2 key tiles][2 g/l][4 q][128]
+    uint8_t* sones = sk + 2 * kTileBytes;              // 128 x 16 bf16 ones (K's extra columns)
+    uint8_t* sq = sones + kOnesBytes;                  // ring of (query pair, its qx rows)
+    double* spart = reinterpret_cast<double*>(sq);     // [2 key tiles][2 g/l][4 q][128], after the loop
     __shared__ Bars bars;
 
     const int tid = threadIdx.x, warp = tid >> 5;
@@ -115,7 +114,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int jp = blockIdx.x / per_jp;
     const int unit = blockIdx.x % a.units;
     const int hg = (blockIdx.x % per_jp) / a.units;
-    const size_t Lp = (size_t)a.nT * kTile;
     const int gh = a.G / a.hsplit;
     const int b = unit / a.Hkv, hk = unit % a.Hkv;
     const int J0 = 2 * jp;
@@ -124,6 +122,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int span_p = (a.nT - J0 + 1) / 2;            // query-tile pairs (J0, J0+1), (J0+2, J0+3), ...
     const int n_pairs = gh * span_p;                   // pair p -> head hg*gh + p / span_p, tile J0 + 2 (p % span_p)
 
+    // K' = [K, 1 ... 1]: every element of the extra 16 columns is one, so the extra K-step adds the
+    // row sum of the query's qx entries (x1 + x2 + x3 = -lse2 / c) whatever the swizzle order
+    for (int i = tid; i < kOnesBytes / 16; i += kThreads)
+        reinterpret_cast<uint4*>(sones)[i] = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
+    fence_proxy_async();  // generic-proxy stores -> visible to the tensor core (async proxy)
     if (warp == 0) {
         tmem_alloc<512>(&bars.tmem_base);
     } else if (warp == 1 && elect_one()) {
@@ -135,10 +138,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int s = 0; s < kBufs; ++s) {
             mbar_init(&bars.s_full[s], 1);
             mbar_init(&bars.s_empty[s], 16);   // one arrival per column warp
-        }
-        for (int s = 0; s < 2; ++s) {
-            mbar_init(&bars.l_full[s], 1);
-            mbar_init(&bars.l_empty[s], 16);
         }
         fence_barrier_init();
     }
@@ -152,6 +151,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (elect_one()) {
             tma_prefetch(&tk);
             tma_prefetch(&tq);
+            tma_prefetch(&tqx);
             mbar_expect_tx(&bars.k_full, (has1 ? 2 : 1) * kTileBytes);
             tma_load_3d(sk, &tk, &bars.k_full, 0, J0 * kTile, unit);
             tma_load_3d(sk + 16384, &tk, &bars.k_full, 64, J0 * kTile, unit);
@@ -162,16 +162,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int p = 0; p < n_pairs; ++p) {
                 const int h = hg * gh + p / span_p, I = J0 + 2 * (p % span_p);
                 const int plane = b * a.Hq + hk * a.G + h;
-                const int s = p % kQStages, lb = p & 1;
+                const int s = p % kQStages;
                 if (p >= kQStages) mbar_wait(&bars.q_empty[s], ((p / kQStages) - 1) & 1);
-                uint8_t* dq = sq + s * kPairBytes;
-                mbar_expect_tx(&bars.q_full[s], kPairBytes);
+                uint8_t* dq = sq + s * kStageBytes;
+                mbar_expect_tx(&bars.q_full[s], kStageBytes);
                 tma_load_3d(dq, &tq, &bars.q_full[s], 0, I * kTile, plane);
                 tma_load_3d(dq + kTileBytes, &tq, &bars.q_full[s], 64, I * kTile, plane);
-                if (p >= 2) mbar_wait(&bars.l_empty[lb], ((p >> 1) - 1) & 1);
-                const uint32_t lbytes = I + 1 < a.nT ? 1024 : 512;  // never past the plane's rows
-                mbar_expect_tx(&bars.l_full[lb], lbytes);
-                bulk_load(slse + lb * 256, a.nlse2 + (size_t)plane * Lp + (size_t)I * kTile, lbytes, &bars.l_full[lb]);
+                tma_load_3d(dq + kPairBytes, &tqx, &bars.q_full[s], 0, I * kTile, plane);
             }
         }
     } else if (warp == 1) {
@@ -183,7 +180,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int p = 0; p < n_pairs; ++p) {
                 const int s = p % kQStages;
                 mbar_wait(&bars.q_full[s], (p / kQStages) & 1);
-                const uint32_t qa = smem_u32(sq + s * kPairBytes);
+                const uint32_t qa = smem_u32(sq + s * kStageBytes);
                 for (int w = 0; w < nw; ++w) {
                     if (p >= 1) mbar_wait(&bars.s_empty[w], (p - 1) & 1);
                     tc_fence_after();
@@ -191,6 +188,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int k = 0; k < 8; ++k)
                         mma_ss(tmem + w * 256, sdesc(kmajor_addr(ka[w], k), 16, 1024),
                                sdesc(qa + (k >> 2) * kTileBytes + (k & 3) * 32, 16, 1024), id_s, k > 0);
+                    // the row normalisation: S' = S + ones x qx^T (one more K = 16 step)
+                    mma_ss(tmem + w * 256, sdesc_sw32(smem_u32(sones)), sdesc_sw32(qa + kPairBytes), id_s, 1u);
                     mma_commit(&bars.s_full[w]);
                 }
                 mma_commit(&bars.q_empty[s]);
@@ -204,12 +203,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int loc_start = a.L - a.lwin;
         double acc_g[2] = {0.0, 0.0}, acc_l[2] = {0.0, 0.0};
         const uint32_t s_full0 = smem_u32(&bars.s_full[0]), s_empty0 = smem_u32(&bars.s_empty[0]);
-        const uint32_t l_full0 = smem_u32(&bars.l_full[0]), l_empty0 = smem_u32(&bars.l_empty[0]);
         const uint32_t sa0 = tmem + 64 * q + ((uint32_t)(wi * 32) << 16);
-        const uint32_t lb0 = smem_u32(slse + 64 * q);
         for (int p = 0, I = J0; p < n_pairs; ++p) {
-            const int lb = p & 1;
-            mbar_wait_u(l_full0 + 8 * lb, (p >> 1) & 1);
             const int q0 = I * kTile + 64 * q;  // first query of this warpgroup's columns
 #pragma unroll
             for (int w = 0; w < 2; ++w) {
@@ -223,12 +218,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tmem_ld32(sa, r[0]);
                     tmem_ld32(sa + 32, r[1]);
                     tmem_ld_wait();
-                    const uint32_t lbs = lb0 + lb * 1024;
                     if (q0 > key0 + kTile - 1 && q0 + 63 < loc_start) {
-                        acc_g[w] += (double)cols_fast(r, lbs);
+                        acc_g[w] += (double)cols_fast(r);
                     } else {
                         float sg, sl;
-                        cols_masked(r, lbs, a.c, q0, key0 + mrow, loc_start, a.L, sg, sl);
+                        cols_masked(r, a.c, q0, key0 + mrow, loc_start, a.L, sg, sl);
                         acc_g[w] += (double)sg;
                         acc_l[w] += (double)sl;
                     }
@@ -237,8 +231,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                 __syncwarp();
                 if ((tid & 31) == 0) mbar_arrive_u(s_empty0 + 8 * w);
             }
-            __syncwarp();
-            if ((tid & 31) == 0) mbar_arrive_u(l_empty0 + 8 * lb);
             I += 2;
             if (I >= a.nT) I = J0;
         }
@@ -293,11 +285,11 @@ __global__ void colsum_reduce_kernel(const double* __restrict__ pg, const double
 }  // namespace
 
 cudaError_t launch_colsum_tc(const ColArgs& a, const CUtensorMap& tk, const CUtensorMap& tq,
-                             cudaStream_t s) {
+                             const CUtensorMap& tqx, cudaStream_t s) {
     cudaError_t e = smem_optin(reinterpret_cast<const void*>(colsum_tc_kernel), (int)kSmem);
     if (e != cudaSuccess) return e;
     const dim3 grid(((a.nT + 1) / 2) * a.units * a.hsplit);
-    colsum_tc_kernel<<<grid, kThreads, kSmem, s>>>(tk, tq, a);
+    colsum_tc_kernel<<<grid, kThreads, kSmem, s>>>(tk, tq, tqx, a);
     e = cudaGetLastError();
     if (e != cudaSuccess || a.hsplit == 1) return e;
     colsum_reduce_kernel<<<4 * 148, 256, 0, s>>>(a.part_g, a.part_l, a.glo, a.loc, a.units, a.L, a.hsplit, a.G);

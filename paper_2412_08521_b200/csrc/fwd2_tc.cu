@@ -45,10 +45,10 @@ constexpr int kMaxT2 = 4096;  // 256-key tiles per sequence (L <= 1048576) for t
 constexpr size_t kSmem2 = 1024 + kTileBytes + 2 * kStages2 * kTileBytes + 2 * 4 * 128 * 4 + kMaxT2 * 4;
 
 struct Fwd2Args {
-    int L, Lp, Hq, Hkv, G, nT, units;  // Lp = nT * 128: row stride of nlse2
+    int L, Lp, Hq, Hkv, G, nT, units;  // Lp = nT * 128: row stride of qx
     float c;
     __nv_bfloat16* out;  // [planes][L][128] (may be null)
-    float* nlse2;        // [planes][Lp] negated log2-domain LSE (P2's input)
+    __nv_bfloat16* qx;   // [planes][Lp][16] -lse2/c as three bf16 terms (P2's extra K columns)
     float* lse_nat;      // [planes][L] natural-log LSE (may be null)
     const float* kmax;  // [units][nT2] max ||k|| over each 256-key tile (Cauchy-Schwarz bound)
     int nT2;
@@ -349,7 +349,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT2, 1)
         }
         if (q == 0 && store) {
             const float lse2 = m_ref + __log2f(lt);
-            a.nlse2[(size_t)plane * a.Lp + qrow] = -lse2;
+            // P2 folds the row normalisation into its MMA: Q' = [q, x1, x2, x3, 0...] against
+            // K' = [k, 1, ..., 1] gives q.k + x with x = -lse2 / c, so S' c = s c - lse2 exactly
+            // to fp32 rounding (three bf16 terms carry x to ~1e-6 absolute)
+            const float x = -lse2 / a.c;
+            const __nv_bfloat16 x1 = __float2bfloat16_rn(x);
+            const float r1 = x - __bfloat162float(x1);
+            const __nv_bfloat16 x2 = __float2bfloat16_rn(r1);
+            const __nv_bfloat16 x3 = __float2bfloat16_rn(r1 - __bfloat162float(x2));
+            uint4* dq = reinterpret_cast<uint4*>(a.qx + ((size_t)plane * a.Lp + qrow) * 16);
+            const __nv_bfloat162 p12 = __halves2bfloat162(x1, x2), p30 = __halves2bfloat162(x3, __float2bfloat16_rn(0.f));
+            dq[0] = make_uint4(*reinterpret_cast<const uint32_t*>(&p12), *reinterpret_cast<const uint32_t*>(&p30), 0u, 0u);
+            dq[1] = make_uint4(0u, 0u, 0u, 0u);
             if (a.lse_nat) a.lse_nat[row] = lse2 * kLn2;
         }
     }
@@ -394,7 +405,7 @@ size_t fwd2_workspace(int units, int L) { return sizeof(float) * (size_t)units *
 
 bool fwd2_tc_supported(int L) { return (L + 255) / 256 <= kMaxT2; }
 
-cudaError_t launch_fwd2_tc(int L, int Hq, int Hkv, int G, int units, float c, void* out, float* nlse2,
+cudaError_t launch_fwd2_tc(int L, int Hq, int Hkv, int G, int units, float c, void* out, void* qx,
                            float* lse_nat, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                            const void* k, float* kmax, cudaStream_t s, const void* q) {
     cudaError_t e = smem_optin(reinterpret_cast<const void*>(fwd2_tc_kernel), (int)kSmem2);
@@ -409,7 +420,7 @@ cudaError_t launch_fwd2_tc(int L, int Hq, int Hkv, int G, int units, float c, vo
     a.units = units;
     a.c = c;
     a.out = static_cast<__nv_bfloat16*>(out);
-    a.nlse2 = nlse2;
+    a.qx = static_cast<__nv_bfloat16*>(qx);
     a.lse_nat = lse_nat;
     a.nT2 = (L + 255) / 256;
     a.kmax = kmax;

@@ -25,18 +25,18 @@ bool score_tc_supported(const Dims& dm, int dtype) {
 
 static int n_tiles(const Dims& dm) { return (dm.L + kTile - 1) / kTile; }
 
-// workspace: nlse2 [B*Hq][nT*128] fp32 (row stride padded to whole tiles so P2's 512-byte
-// bulk loads of a query tile never cross a plane), then (head split only) fp64 partials
-// [2][units][hsplit][L], then P1's per-key-tile norm bounds
-static size_t nlse2_bytes(const Dims& dm) {
-    return (sizeof(float) * (size_t)dm.B * dm.Hq * n_tiles(dm) * kTile + 255) / 256 * 256;
+// workspace: qx [B*Hq][nT*128][16] bf16 (P1 -> P2: the row normalisation as extra K columns of
+// Q, rows padded to whole tiles), then (head split only) fp64 partials [2][units][hsplit][L],
+// then P1's per-key-tile norm bounds
+static size_t qx_bytes(const Dims& dm) {
+    return (32 * (size_t)dm.B * dm.Hq * n_tiles(dm) * kTile + 255) / 256 * 256;
 }
 static size_t part_bytes(const Dims& dm) {
     const int hs = colsum_hsplit(dm.G, n_tiles(dm), dm.units);
     return hs > 1 ? 2 * sizeof(double) * (size_t)dm.units * hs * dm.L : 0;
 }
 size_t score_tc_workspace(const Dims& dm) {
-    return nlse2_bytes(dm) + part_bytes(dm) + (fwd2_workspace(dm.units, dm.L) + 255) / 256 * 256;
+    return qx_bytes(dm) + part_bytes(dm) + (fwd2_workspace(dm.units, dm.L) + 255) / 256 * 256;
 }
 
 cudaError_t score_tc(const Dims& dm, const void* q, const void* k, const void* v, void* o,
@@ -47,10 +47,10 @@ cudaError_t score_tc(const Dims& dm, const void* q, const void* k, const void* v
         !make_tmap_bf16_3d(&tk, k, kD, dm.L, planes_kv, kTile) ||
         !make_tmap_bf16_3d(&tv, v ? v : k, kD, dm.L, planes_kv, kTile))
         return cudaErrorInvalidValue;
-    float* nlse2 = static_cast<float*>(ws);
+    void* qx = ws;
     const float c = kLog2e / sqrtf((float)kD);
-    float* kmax = reinterpret_cast<float*>(static_cast<char*>(ws) + nlse2_bytes(dm) + part_bytes(dm));
-    cudaError_t e = launch_fwd2_tc(dm.L, dm.Hq, dm.Hkv, dm.G, dm.units, c, o, nlse2, lse, tq, tk, tv, k, kmax,
+    float* kmax = reinterpret_cast<float*>(static_cast<char*>(ws) + qx_bytes(dm) + part_bytes(dm));
+    cudaError_t e = launch_fwd2_tc(dm.L, dm.Hq, dm.Hkv, dm.G, dm.units, c, o, qx, lse, tq, tk, tv, k, kmax,
                                    s, q);
     if (e != cudaSuccess) return e;
     ColArgs ca;
@@ -62,17 +62,18 @@ cudaError_t score_tc(const Dims& dm, const void* q, const void* k, const void* v
     ca.units = dm.units;
     ca.lwin = dm.lwin_scores;
     ca.c = c;
-    ca.nlse2 = nlse2;
     ca.glo = glo;
     ca.loc = loc;
     ca.hsplit = colsum_hsplit(dm.G, ca.nT, dm.units);
     if (ca.hsplit > 1) {
-        ca.part_g = reinterpret_cast<double*>(static_cast<char*>(ws) + nlse2_bytes(dm));
+        ca.part_g = reinterpret_cast<double*>(static_cast<char*>(ws) + qx_bytes(dm));
         ca.part_l = ca.part_g + (size_t)dm.units * ca.hsplit * dm.L;
     }
-    CUtensorMap tq2;  // P2 streams pairs of query tiles: 256-row boxes
-    if (!make_tmap_bf16_3d(&tq2, q, kD, dm.L, planes_q, 2 * kTile)) return cudaErrorInvalidValue;
-    return launch_colsum_tc(ca, tk, tq2, s);
+    CUtensorMap tq2, tqx;  // P2 streams pairs of query tiles (256-row boxes) and their qx rows
+    if (!make_tmap_bf16_3d(&tq2, q, kD, dm.L, planes_q, 2 * kTile) ||
+        !make_tmap_bf16_3d_k16(&tqx, qx, (uint64_t)ca.nT * kTile, planes_q, 2 * kTile))
+        return cudaErrorInvalidValue;
+    return launch_colsum_tc(ca, tk, tq2, tqx, s);
 }
 
 }  // namespace ems

@@ -30,7 +30,6 @@ __device__ __forceinline__ uint32_t tmem_lane_addr(uint32_t base, int warp_in_wg
 struct ColArgs {
     int L, Hq, Hkv, G, nT, units, lwin;
     float c;               // log2(e) / sqrt(d)
-    const float* nlse2;    // [B*Hq][nT*128] negated log2-domain LSE from P1 (rows >= L unset)
     float* glo;            // [units][L]
     float* loc;
     // Head split (load balance when few units): each CTA takes G / hsplit query heads of its
@@ -44,11 +43,11 @@ struct ColArgs {
 }  // namespace sc
 
 cudaError_t launch_colsum_tc(const sc::ColArgs& a, const CUtensorMap& tk, const CUtensorMap& tq,
-                             cudaStream_t s);
+                             const CUtensorMap& tqx, cudaStream_t s);
 int colsum_hsplit(int G, int nT, int units);
 bool fwd2_tc_supported(int L);
 size_t fwd2_workspace(int units, int L);
-cudaError_t launch_fwd2_tc(int L, int Hq, int Hkv, int G, int units, float c, void* out, float* nlse2,
+cudaError_t launch_fwd2_tc(int L, int Hq, int Hkv, int G, int units, float c, void* out, void* qx,
                            float* lse_nat, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                            const void* k, float* kmax, cudaStream_t s, const void* q);
 

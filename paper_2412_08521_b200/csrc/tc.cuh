@@ -164,6 +164,17 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t
     return d;
 }
 
+// The same for a K-major SWIZZLE_32B tile (rows of 16 bf16 = 32 B, 8-row groups 256 B apart).
+__device__ __forceinline__ uint64_t sdesc_sw32(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)(16 >> 4) << 16;
+    d |= (uint64_t)(256 >> 4) << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)6 << 61;
+    return d;
+}
+
 // Instruction descriptor, kind::f16 with bf16 inputs and f32 accumulation.
 //   [4,6) c_format (1 = F32), [7,10) a_format (1 = BF16), [10,13) b_format (1 = BF16),
 //   [15] a_major (0 K, 1 MN), [16] b_major, [17,23) N>>3, [24,29) M>>4.

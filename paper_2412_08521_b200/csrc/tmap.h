@@ -43,4 +43,20 @@ inline bool make_tmap_bf16_3d(CUtensorMap* map, const void* base, uint64_t cols,
     return r == CUDA_SUCCESS;
 }
 
+// bf16 tensor [planes][rows][16] (one 32-byte row per entry), box = 16 cols x box_rows rows,
+// 32-byte swizzle: the canonical K-major SWIZZLE_32B smem layout of a K = 16 MMA operand.
+inline bool make_tmap_bf16_3d_k16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t planes,
+                                  uint32_t box_rows) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[3] = {16, rows, planes};
+    cuuint64_t strides[2] = {32, rows * 32};
+    cuuint32_t box[3] = {16, box_rows, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 }  // namespace ems
