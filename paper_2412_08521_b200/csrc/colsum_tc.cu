@@ -6,20 +6,27 @@
 // Reference semantics: streaming_pass column scatter, proj/src/scoring.cpp:52-62;
 // GQA mean per contract D2.
 //
+// The row normalisation rides in the MMA: P1 writes x_i = -lse2_i / c as three bf16 terms (qx),
+// and every S^T tile gets one more K = 16 step, K' = [K, 1 ... 1] against Q' = [Q, x1 x2 x3 0 ...],
+// so the accumulator holds S' = q.k + x and the epilogue is exp2(S' c): no LSE loads from shared
+// memory next to the exponentials (measured -4.6 % P2 time; the extra step is 1/8 more MMA work in
+// a pass bound by the exponentials).  The split of x carries it to ~1e-6 absolute; glo agrees
+// with the reference to ~1e-6 at full size (tests/test_gpu_fullsize_ref.py).
+//
 // Any L: the last query / key tile is TMA zero fill past L; queries >= L are masked in the
 // (always masked-path) last query tile and keys >= L are never stored.
 //
 // One CTA owns TWO 128-key tiles (J0 = 2*jp, J1 = J0 + 1) of one unit, both resident in smem,
 // and streams every (query head h, query-tile PAIR (I, I+1), I >= J0) through a 2-stage TMA ring
-// (one 256-row box per 64 d-columns).  Each pair feeds two SS MMAs S^T_w = K_Jw [Q_I; Q_I+1]^T with
-// N = 256 (keys on TMEM lanes; ~90 % of the tensor rate against ~60 % for N = 128: same time --
-// the pass is bound by the exponentials -- and 2.6 % less energy per step), TMEM buffer w holding
-// key tile Jw.  Four column warpgroups: per item (pair, w) warpgroup q owns query columns
-// [64 q, 64 q + 64) of the pair and thread m owns key Jw*128 + m, so the column sum over queries
-// is an in-thread row sum (no atomics).  Interior items take a mask-free path where kPoly of every
-// 8 exp2 pairs run as a degree-5 polynomial on the FMA pipe (ex2_poly2) and the rest on MUFU.
-// Per-item fp32 sums are accumulated in fp64 in item order and the four column quarters are
-// combined in a fixed order -> deterministic.
+// (one 256-row box per 64 d-columns, plus the pair's qx rows).  Each pair feeds two SS MMAs
+// S'^T_w = K'_Jw [Q'_I; Q'_I+1]^T with N = 256 (keys on TMEM lanes; ~90 % of the tensor rate
+// against ~60 % for N = 128: same time -- the pass is bound by the exponentials -- and 2.6 % less
+// energy per step), TMEM buffer w holding key tile Jw.  Four column warpgroups: per item
+// (pair, w) warpgroup q owns query columns [64 q, 64 q + 64) of the pair and thread m owns key
+// Jw*128 + m, so the column sum over queries is an in-thread row sum (no atomics).  Interior
+// items take a mask-free path where kPoly of every 8 exp2 pairs run as a degree-5 polynomial on
+// the FMA pipe (ex2_poly2) and the rest on MUFU.  Per-item fp32 sums are accumulated in fp64 in
+// item order and the four column quarters are combined in a fixed order -> deterministic.
 #include "score_tc.cuh"
 
 namespace ems {
