@@ -16,7 +16,7 @@ namespace ems {
 cudaError_t score_simt(const Dims& dm, int dtype, const void* q, const void* k, const void* v,
                        void* o, float* lse, float* glo, float* loc, cudaStream_t s);
 cudaError_t score_tc(const Dims& dm, const void* q, const void* k, const void* v, void* o,
-                     float* lse, float* glo, float* loc, void* ws, cudaStream_t s);
+                     float* lse, float* glo, float* loc, void* ws, cudaStream_t s, cudaEvent_t o_ready);
 size_t score_tc_workspace(const Dims& dm);
 size_t merge_tc_workspace(const Dims& dm);
 bool merge_tc_supported(const Dims& dm, int dtype);
@@ -213,14 +213,16 @@ bool use_tc(const ems_desc& d) {
     return score_tc_supported(m, d.dtype);
 }
 
+// o_ready (optional) is recorded on `s` as soon as O and the LSE are final: after the forward
+// pass, before the column sums of the tensor-core path.
 int run_score(const ems_desc* desc, const void* q, const void* k, const void* v, void* o,
-              float* lse, float* glo, float* loc, void* ws, cudaStream_t s) {
+              float* lse, float* glo, float* loc, void* ws, cudaStream_t s, cudaEvent_t o_ready = nullptr) {
     const Dims m = make_dims(*desc);
     const Layout l = layout(*desc);
     float* lse_buf = lse ? lse : at<float>(ws, l.lse);
     cudaError_t e;
     if (use_tc(*desc)) {
-        e = score_tc(m, q, k, v, o, lse_buf, glo, loc, at<void>(ws, l.tc), s);
+        e = score_tc(m, q, k, v, o, lse_buf, glo, loc, at<void>(ws, l.tc), s, o_ready);
     } else {
         // The SIMT kernels serve fp32 (no tcgen05 kind keeps the 1e-4 contract) and head_dim
         // != 128; bf16 at d = 128 always takes the tensor cores (any L up to 2^20) unless the
@@ -232,6 +234,7 @@ int run_score(const ems_desc* desc, const void* q, const void* k, const void* v,
             return EMS_UNSUPPORTED;
         }
         e = score_simt(m, desc->dtype, q, k, v, o, lse_buf, glo, loc, s);
+        if (e == cudaSuccess && o_ready) e = cudaEventRecord(o_ready, s);
     }
     if (e != cudaSuccess) {
         set_error("score launch: %s", cudaGetErrorString(e));
@@ -541,13 +544,12 @@ namespace {
 int run_path(const ems_desc* d, const void* q_rot, const void* k_rot, const void* k_raw,
              const void* v, void* out_o, float* lse, float* glo, float* loc, const ems_stage* st,
              const ems_cache& c, void* ws, cudaStream_t s, int unit_base = 0,
-             cudaEvent_t after_score = nullptr) {
+             cudaEvent_t o_ready = nullptr) {
     const Layout l = layout(*d);
     float* g = glo ? glo : at<float>(ws, l.glo);
     float* lc = loc ? loc : at<float>(ws, l.loc);
     const ems_stage sg = st ? *st : default_stage(*d, ws);
-    if (int rc = run_score(d, q_rot, k_rot, v, out_o, lse, g, lc, ws, s)) return rc;
-    if (after_score) EMS_CUDA_CHECK(cudaEventRecord(after_score, s));  // O (and the LSE) are final here
+    if (int rc = run_score(d, q_rot, k_rot, v, out_o, lse, g, lc, ws, s, o_ready)) return rc;
     if (d->seq_len > d->n_budget && d->policy != EMS_POLICY_FULL) {  // policies.cpp:136-138
         if (int rc = run_select(d, g, lc, sg, ws, s, unit_base)) return rc;
         if (int rc = run_merge(d, k_raw, v, sg, ws, s)) return rc;
@@ -717,7 +719,8 @@ struct HostPipeRes {
     int device = -1;
     cudaStream_t copy = nullptr;
     cudaStream_t comp2 = nullptr;  // second compute stream (two unit groups in flight)
-    cudaStream_t d2h = nullptr;    // device-to-host copies (the other PCIe direction than `copy`)
+    cudaStream_t d2h = nullptr;    // device-to-host copies of the caches (the other PCIe direction)
+    cudaStream_t d2h_o = nullptr;  // device-to-host copies of O (never queued behind a group's compress)
     std::vector<cudaEvent_t> ev;
 };
 
@@ -736,6 +739,8 @@ HostPipeRes* pipe_res(int nev) {
     if (r.copy == nullptr && cudaStreamCreateWithFlags(&r.copy, cudaStreamNonBlocking) != cudaSuccess)
         return nullptr;
     if (r.d2h == nullptr && cudaStreamCreateWithFlags(&r.d2h, cudaStreamNonBlocking) != cudaSuccess)
+        return nullptr;
+    if (r.d2h_o == nullptr && cudaStreamCreateWithFlags(&r.d2h_o, cudaStreamNonBlocking) != cudaSuccess)
         return nullptr;
     if (r.comp2 == nullptr && cudaStreamCreateWithFlags(&r.comp2, cudaStreamNonBlocking) != cudaSuccess)
         return nullptr;
@@ -792,9 +797,11 @@ extern "C" int ems_prefill_host(const ems_desc* d, double rope_base, const void*
         return EMS_CUDA_ERROR;
     }
     cudaStream_t cs = copy_stream ? copy_stream : res->copy;
-    cudaStream_t ds = res->d2h;  // results go back on their own stream: both PCIe directions at once
+    // results go back on their own streams (both PCIe directions at once): caches on `ds` after
+    // each group's compress, O on `dso` as soon as each group's forward pass is done
+    cudaStream_t ds = res->d2h, dso = res->d2h_o;
     // [0, nc): inputs of chunk c staged; [nc, 2nc): chunk c done; [2nc, 2nc + 3): start / copies
-    // done / second stream done; [2nc + 3, 3nc + 3): chunk c's score pass done (O final)
+    // done / second stream done; [2nc + 3, 3nc + 3): chunk c's O final; 3nc + 3: O copies done
     cudaEvent_t* ev = res->ev.data();
     cudaEvent_t* ev_o = ev + 2 * nc + 3;
     const size_t row = (size_t)m.L * m.d * m.esize;  // one [L][d] plane
@@ -889,9 +896,9 @@ extern "C" int ems_prefill_host(const ems_desc* d, double rope_base, const void*
             EMS_CUDA_CHECK(cudaEventRecord(ev[nc + c], sc));
             if (h_out_o) {  // engine::prefill's PrefillResult.per_head outputs (engine.hpp:36-45): O is final
                             // after the forward pass, so its copy overlaps this group's column sums and compress
-                EMS_CUDA_CHECK(cudaStreamWaitEvent(ds, ev_o[c], 0));
+                EMS_CUDA_CHECK(cudaStreamWaitEvent(dso, ev_o[c], 0));
                 EMS_CUDA_CHECK(cudaMemcpyAsync(off(h_out_o, oq), off(out_o, oq), (size_t)n * G * row,
-                                               cudaMemcpyDeviceToHost, ds));
+                                               cudaMemcpyDeviceToHost, dso));
             }
             if (h_cache) {
                 EMS_CUDA_CHECK(cudaStreamWaitEvent(ds, ev[nc + c], 0));
@@ -906,6 +913,8 @@ extern "C" int ems_prefill_host(const ems_desc* d, double rope_base, const void*
     cudaStreamWaitEvent(s, ev[2 * nc + 1], 0);
     cudaEventRecord(ev[2 * nc], ds);  // the start event's slot is free again: reuse it for the D2H stream
     cudaStreamWaitEvent(s, ev[2 * nc], 0);
+    cudaEventRecord(ev[3 * nc + 3], dso);
+    cudaStreamWaitEvent(s, ev[3 * nc + 3], 0);
     if (dual) {
         cudaEventRecord(ev[2 * nc + 2], s2);
         cudaStreamWaitEvent(s, ev[2 * nc + 2], 0);

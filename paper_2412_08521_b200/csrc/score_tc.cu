@@ -40,7 +40,7 @@ size_t score_tc_workspace(const Dims& dm) {
 }
 
 cudaError_t score_tc(const Dims& dm, const void* q, const void* k, const void* v, void* o,
-                     float* lse, float* glo, float* loc, void* ws, cudaStream_t s) {
+                     float* lse, float* glo, float* loc, void* ws, cudaStream_t s, cudaEvent_t o_ready) {
     const int planes_q = dm.B * dm.Hq, planes_kv = dm.B * dm.Hkv;
     CUtensorMap tq, tk, tv;
     if (!make_tmap_bf16_3d(&tq, q, kD, dm.L, planes_q, kTile) ||
@@ -53,6 +53,7 @@ cudaError_t score_tc(const Dims& dm, const void* q, const void* k, const void* v
     cudaError_t e = launch_fwd2_tc(dm.L, dm.Hq, dm.Hkv, dm.G, dm.units, c, o, qx, lse, tq, tk, tv, k, kmax,
                                    s, q);
     if (e != cudaSuccess) return e;
+    if (o_ready && (e = cudaEventRecord(o_ready, s)) != cudaSuccess) return e;  // O and the LSE are final
     ColArgs ca;
     ca.L = dm.L;
     ca.Hq = dm.Hq;
