@@ -93,6 +93,29 @@ cudaError_t smem_optin(const void* kernel, int bytes) {
     return e;
 }
 
+int active_clusters(const void* kernel, int threads, int smem_bytes, int cluster) {
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, int> done;  // (kernel, device) -> clusters
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+    std::lock_guard<std::mutex> lock(mu);
+    int& have = done[{kernel, dev}];
+    if (have > 0) return have;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)cluster, 1, 1);
+    cfg.blockDim = dim3((unsigned)threads, 1, 1);
+    cfg.dynamicSmemBytes = (size_t)smem_bytes;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kernel, &cfg) != cudaSuccess || n <= 0) {
+        cudaGetLastError();
+        int sms = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        n = sms / cluster;  // one CTA per SM
+    }
+    have = n;
+    return n;
+}
+
 Dims make_dims(const ems_desc& d) {
     Dims m;
     m.B = d.batch;

@@ -123,6 +123,9 @@ struct NvtxRange {
 // set it once per (kernel, device), so one process can drive several GPUs (one host thread
 // per device).  Thread-safe; returns the cudaFuncSetAttribute status.
 cudaError_t smem_optin(const void* kernel, int bytes);
+// Clusters of `cluster` CTAs of `kernel` (threads, dynamic smem) co-resident on the current
+// device (persistent grids); cached per kernel and device, after smem_optin.
+int active_clusters(const void* kernel, int threads, int smem_bytes, int cluster);
 
 #define EMS_CUDA_CHECK(expr)                                                          \
     do {                                                                              \
