@@ -18,7 +18,7 @@
 // TMEM allocation and pipeline fill (measured: 3.9 us to the first S and 1.8 us of teardown and
 // relaunch gap per pair, 6 % of config 3 and 29 % at L = 4096), since the next pair's Q (double
 // buffered) and first K/V tiles land while this pair computes and its first S runs under this
-// pair's epilogue.
+// pair's epilogue.  |q_row| for the logit bound is read from the Q tile in shared memory.
 //
 // The leader issues, per 256-key tile j of a pair,
 //   S_j  = Q K_j^T        tcgen05.mma.cta_group::2, M = 256, N = 256, K = 128 (SS): each CTA
@@ -30,9 +30,11 @@
 // and runs under the softmax of tile j; PV_j follows in two K-halves, each issued as soon as its
 // half of P_j is stored.  Softmax: four warpgroups per CTA, thread = (row, 32 keys of each
 // 128-key half); row maxima exchanged through shared memory; lazily updated reference max (O
-// rescaled only when a row max grows by > 8 in log2 units).  Warp roles: warps 0-15 softmax,
-// 16 TMA + scheduler, 17 MMA; setmaxnreg moves registers from the control warpgroup (16-19) to
-// the softmax warpgroups (the launch allows 96 per thread: 5 warps share an SM sub-partition).
+// rescaled only when a row max grows by > 8 in log2 units).  The normalised O tile is staged in
+// the pair's (then idle) Q buffer and written by two bulk tensor stores (per-thread 16-byte row
+// stores took 1.7 us per pair).  Warp roles: warps 0-15 softmax, 16 TMA + scheduler, 17 MMA,
+// 18 O stores; setmaxnreg moves registers from the control warpgroup (16-19) to the softmax
+// warpgroups (the launch allows 96 per thread: 5 warps share an SM sub-partition).
 #include <cuda.h>
 #include <stddef.h>
 #include <stdlib.h>
@@ -50,7 +52,7 @@ constexpr float kRescale2 = 8.0f;
 // A tile whose logits provably stay below m_ref + kSkip (|q.k| <= |q| max|k|) needs neither its
 // row max nor the max exchange: its p = 2^(s c - m_ref) <= 2^kSkip cannot overflow fp32/bf16.
 constexpr float kSkip = 64.0f;
-constexpr int kT2 = 640;  // w0-15 softmax (warpgroup q), w16 TMA + scheduler, w17 MMA (leader), w18-19 idle
+constexpr int kT2 = 640;  // w0-15 softmax (warpgroup q), w16 TMA + scheduler, w17 MMA (leader), w18 O stores
 constexpr int kWTma = 16, kWMma = 17;
 constexpr int kRegSoftmax = 104, kRegControl = 64;  // setmaxnreg per warpgroup (launch: 96)
 constexpr int kStages2 = 2;
@@ -78,14 +80,16 @@ struct Bars2 {
     uint64_t k_empty[kStages2], v_empty[kStages2];  // local (multicast commit)
     uint64_t s_full, o_full;                        // local (multicast commit)
     uint64_t s_free, p_full, p_full_hi;             // leader: 32 warp arrivals (16 per CTA)
+    uint64_t o_staged[2];                           // local: 16 softmax warps staged O (pair parity)
     uint64_t item_full[kRing];                      // local: the leader published the slot
     uint64_t item_empty[kRing];                     // leader: every consumer of both CTAs read it
     int item[kRing];
     uint32_t tmem_base;
 };
-// consumers of a scheduled pair: per CTA 16 softmax warps; the leader's MMA thread and the
-// partner's TMA thread
-constexpr int kItemConsumers = 2 * 16 + 2;
+// consumers of a scheduled pair: per CTA 16 softmax warps and the O store thread; the leader's
+// MMA thread and the partner's TMA thread
+constexpr int kItemConsumers = 2 * 17 + 2;
+constexpr int kWStore = 18;  // O store thread (TMA bulk tensor stores from the staged tile)
 
 struct Item {
     int plane, tile, unit, jmax;
@@ -126,7 +130,8 @@ __device__ __forceinline__ int take_pair(Bars2& bars, int n, bool release) {
 // pair's epilogue.
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT2, 1)
     fwd2_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
-                   const __grid_constant__ CUtensorMap tv, const Fwd2Args a) {
+                   const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap to,
+                   const Fwd2Args a) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sq = sm;                                   // 2 x 32 KB: this CTA's 128 query rows
@@ -143,7 +148,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT2, 1)
     } else if (warp == kWMma && elect_one()) {
         for (int b = 0; b < 2; ++b) {
             mbar_init(&bars.q_full[b], 1);
-            mbar_init(&bars.q_empty[b], 1 + 16);  // the pair's last S (MMA commit) + |q| reads of 16 warps
+            // the pair's last S (MMA commit) + its O staged in this buffer stored (store thread)
+            mbar_init(&bars.q_empty[b], 2);
+            mbar_init(&bars.o_staged[b], 16);
         }
         for (int s = 0; s < kStages2; ++s) {
             mbar_init(&bars.k_full[s], 1);
@@ -300,6 +307,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT2, 1)
                     }
                 }
             }
+        } else if (warp == kWStore) {
+            // ------------------------------------------------------------ O stores (both CTAs)
+            // The softmax warps stage each pair's normalised O tile in the pair's Q buffer (its
+            // last S is done once O is final) in the SWIZZLE_128B layout of the Q boxes; two bulk
+            // tensor stores write it (rows >= L clipped), then the buffer is released for the
+            // Q of pair n + 2.
+            if (elect_one()) {
+                for (int n = 0;; ++n) {
+                    const int idx = take_pair(bars, n, true);
+                    if (idx >= a.pairs) break;
+                    const Item it = pair_item(a, idx, (int)rank);
+                    const int qb = n & 1;
+                    mbar_wait(&bars.o_staged[qb], (n >> 1) & 1);
+                    if (a.out && it.real) {
+                        uint8_t* src = sq + qb * kTileBytes;
+                        tma_store_3d(&to, src, 0, it.tile * kTile, it.plane);
+                        tma_store_3d(&to, src + 16384, 64, it.tile * kTile, it.plane);
+                        bulk_commit_group();
+                        bulk_wait_group_read0();
+                    }
+                    mbar_arrive(&bars.q_empty[qb]);
+                }
+                bulk_wait_group0();
+            }
         }
         teardown();
     } else {
@@ -423,7 +454,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT2, 1)
                 l += rs2.x + rs2.y;
                 if (j == 0) {
                     // |q_row| for the logit bound of tiles >= 1, from this CTA's Q tile in shared
-                    // memory (resident: the Q buffer is released only after these reads): quarter q
+                    // memory (resident until this pair's O is stored from it): quarter q
                     // sums dims [32q, 32q + 32) (SWIZZLE_128B rows), the four partials combine in a
                     // fixed order.  Rows >= L are TMA zero fill.
                     const uint32_t qrow_a = smem_u32(sq + (n & 1) * kTileBytes) + (q >> 1) * 16384 + m * 128;
@@ -439,8 +470,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT2, 1)
                             ss = fmaf(lo, lo, fmaf(hi, hi, ss));
                         }
                     }
-                    __syncwarp();
-                    if ((tid & 31) == 0) mbar_arrive(&bars.q_empty[n & 1]);
                     const uint32_t xs = xch_a + (n_x++ & 1) * 2048;
                     sts32(xs + 4 * (q * 128 + m), ss);
                     asm volatile("bar.sync %0, 128;" ::"r"(1 + wi) : "memory");  // the 4 warps sharing these rows
@@ -463,21 +492,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT2, 1)
             it = pair_item(a, idx, (int)rank);
             const size_t row = (size_t)it.plane * a.L + qrow;
             const float inv = 1.f / lt;
-            if (a.out && __any_sync(0xffffffffu, store)) {  // tcgen05.ld is warp-collective: load
-                uint32_t o[32];                               // warp-uniformly, store per row
+            if (a.out) {  // O / l -> bf16, staged in this pair's Q buffer for the store thread
+                uint32_t o[32];
                 tmem_ld32(sO, o);
                 tmem_ld_wait();
-                uint4* dst = reinterpret_cast<uint4*>(a.out + row * kD + 32 * q);
+                const uint32_t srow = smem_u32(sq + (n & 1) * kTileBytes) + (q >> 1) * 16384 + m * 128;
 #pragma unroll
-                for (int x = 0; x < 4 && store; ++x) {
-                    uint4 v;
-                    v.x = pack_bf16(__uint_as_float(o[8 * x + 0]) * inv, __uint_as_float(o[8 * x + 1]) * inv);
-                    v.y = pack_bf16(__uint_as_float(o[8 * x + 2]) * inv, __uint_as_float(o[8 * x + 3]) * inv);
-                    v.z = pack_bf16(__uint_as_float(o[8 * x + 4]) * inv, __uint_as_float(o[8 * x + 5]) * inv);
-                    v.w = pack_bf16(__uint_as_float(o[8 * x + 6]) * inv, __uint_as_float(o[8 * x + 7]) * inv);
-                    dst[x] = v;
-                }
+                for (int x = 0; x < 4; ++x)
+                    sts128(srow + ((((q & 1) * 4 + x) ^ (m & 7)) << 4),
+                           pack_bf16(__uint_as_float(o[8 * x + 0]) * inv, __uint_as_float(o[8 * x + 1]) * inv),
+                           pack_bf16(__uint_as_float(o[8 * x + 2]) * inv, __uint_as_float(o[8 * x + 3]) * inv),
+                           pack_bf16(__uint_as_float(o[8 * x + 4]) * inv, __uint_as_float(o[8 * x + 5]) * inv),
+                           pack_bf16(__uint_as_float(o[8 * x + 6]) * inv, __uint_as_float(o[8 * x + 7]) * inv));
+                fence_proxy_async();  // generic-proxy stores -> visible to the bulk store (async proxy)
             }
+            __syncwarp();
+            if ((tid & 31) == 0) mbar_arrive(&bars.o_staged[n & 1]);
             tc_fence_before();
             if (q == 0 && store) {
                 const float lse2 = m_ref + __log2f(lt);
@@ -544,6 +574,7 @@ bool fwd2_tc_supported(int L) { return (L + 255) / 256 <= kMaxT2; }
 
 cudaError_t launch_fwd2_tc(int L, int Hq, int Hkv, int G, int units, float c, void* out, void* qx,
                            float* lse_nat, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+                           const CUtensorMap& to,
                            const void* k, float* kmax, cudaStream_t s) {
     cudaError_t e = smem_optin(reinterpret_cast<const void*>(fwd2_tc_kernel), (int)kSmem2);
     if (e != cudaSuccess) return e;
@@ -568,7 +599,7 @@ cudaError_t launch_fwd2_tc(int L, int Hq, int Hkv, int G, int units, float c, vo
     const int slots = active_clusters(reinterpret_cast<const void*>(fwd2_tc_kernel), kT2, (int)kSmem2, 2);
     const int clusters = (int)(pairs < slots ? pairs : slots);
     key_tile_norm_kernel<<<units * a.nT2, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(k), L, a.nT2, kmax, a.next);
-    fwd2_tc_kernel<<<(unsigned)(2 * clusters), kT2, kSmem2, s>>>(tq, tk, tv, a);
+    fwd2_tc_kernel<<<(unsigned)(2 * clusters), kT2, kSmem2, s>>>(tq, tk, tv, to, a);
     return cudaGetLastError();
 }
 

@@ -50,7 +50,9 @@ cudaError_t score_tc(const Dims& dm, const void* q, const void* k, const void* v
     void* qx = ws;
     const float c = kLog2e / sqrtf((float)kD);
     float* kmax = reinterpret_cast<float*>(static_cast<char*>(ws) + qx_bytes(dm) + part_bytes(dm));
-    cudaError_t e = launch_fwd2_tc(dm.L, dm.Hq, dm.Hkv, dm.G, dm.units, c, o, qx, lse, tq, tk, tv, k, kmax, s);
+    CUtensorMap to = tq;  // O: the Q layout (only read when O is wanted)
+    if (o && !make_tmap_bf16_3d(&to, o, kD, dm.L, planes_q, kTile)) return cudaErrorInvalidValue;
+    cudaError_t e = launch_fwd2_tc(dm.L, dm.Hq, dm.Hkv, dm.G, dm.units, c, o, qx, lse, tq, tk, tv, to, k, kmax, s);
     if (e != cudaSuccess) return e;
     if (o_ready && (e = cudaEventRecord(o_ready, s)) != cudaSuccess) return e;  // O and the LSE are final
     ColArgs ca;
