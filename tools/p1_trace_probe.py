@@ -1,4 +1,4 @@
-"""Per-pair phase times of P1 from an instrumented variant (tools/build_variant.py p1trace ...):
+"""Per-pair phase times of P1 from an instrumented variant (tools/make_trace_variants.py):
 start -> first S ready -> last PV done -> epilogue done -> exit, and the idle gap between
 consecutive pairs on one SM.  EMS_LIB_PATH=_variants/p1trace.so python tools/p1_trace_probe.py"""
 import ctypes as C

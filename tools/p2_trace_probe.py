@@ -1,4 +1,4 @@
-"""Per-CTA phase times of P2 from an instrumented variant (tools/build_variant.py p2trace ...):
+"""Per-CTA phase times of P2 from an instrumented variant (tools/make_trace_variants.py):
 start -> first S -> loop end -> combine done -> exit, and the gap between CTAs on one SM.
 EMS_LIB_PATH=_variants/p2trace.so python tools/p2_trace_probe.py"""
 import ctypes as C
