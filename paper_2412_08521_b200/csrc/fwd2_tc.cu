@@ -423,9 +423,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT2, 1)
                     for (int x = 0; x < 16; ++x) {
                         const float2 arg = __ffma2_rn(
                             make_float2(__uint_as_float(r[c][2 * x]), __uint_as_float(r[c][2 * x + 1])), c2, nm2);
-                        // all exponentials on MUFU: with the split PV the FMA pipe, not MUFU, was the
-                        // tighter resource (measured: 2 of 8 pairs as ex2_poly2 was 4% slower)
-                        const float2 p = make_float2(ex2(arg.x), ex2(arg.y));
+                        // 1 of 8 pairs as the FMA-pipe polynomial, the rest on MUFU (persistent kernel:
+                        // -1.5 % P1 time, -1 % sustained step; all-MUFU was best for the one-pair-per-
+                        // cluster kernel).  A masked key (-inf) comes out as 2^-125, not 0: < 1e-35 of
+                        // any row sum.
+                        const float2 p = (x & 7) == 0 ? ex2_poly2(arg) : make_float2(ex2(arg.x), ex2(arg.y));
                         rs2 = __fadd2_rn(rs2, p);
                         pk[x] = pack_bf16(p.x, p.y);
                     }
