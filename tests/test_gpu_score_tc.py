@@ -156,3 +156,14 @@ def test_tc_score_long_odd_lengths(L, G):
     assert el <= 2e-4, el
     assert abs(plan.glo.double().sum().item() - L) <= 1e-5 * L
     assert torch.isfinite(plan.out.float()).all()
+    # O on sampled rows (first / middle / the partial last query tile), every head: the persistent
+    # kernel stages each pair's O in a reused Q buffer and stores it with bulk tensor stores
+    rows = torch.tensor(sorted({0, 1, 127, 128, 255, L // 2, L - 300, L - 129, L - 128, L - 2, L - 1}), device=dev)
+    kk, vv = k[0, 0].float(), v[0, 0].float()
+    for h in range(G):
+        s = (q[0, h, rows].float() @ kk.T) / 128 ** 0.5
+        s.masked_fill_(torch.arange(L, device=dev)[None, :] > rows[:, None], float("-inf"))
+        o_t = torch.softmax(s, dim=1) @ vv
+        o = plan.out[0, h, rows].float()
+        err = ((o - o_t).abs().max(dim=1).values / o_t.abs().max(dim=1).values.clamp_min(1e-3)).max().item()
+        assert err <= 2e-2, (h, err)  # bf16 P and bf16 output
