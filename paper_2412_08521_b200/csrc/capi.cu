@@ -16,7 +16,8 @@ namespace ems {
 cudaError_t score_simt(const Dims& dm, int dtype, const void* q, const void* k, const void* v,
                        void* o, float* lse, float* glo, float* loc, cudaStream_t s);
 cudaError_t score_tc(const Dims& dm, const void* q, const void* k, const void* v, void* o,
-                     float* lse, float* glo, float* loc, void* ws, cudaStream_t s, cudaEvent_t o_ready);
+                     float* lse, float* glo, float* loc, void* ws, cudaStream_t s, cudaEvent_t o_ready,
+                     const ScoreParts* parts);
 size_t score_tc_workspace(const Dims& dm);
 size_t merge_tc_workspace(const Dims& dm);
 bool merge_tc_supported(const Dims& dm, int dtype);
@@ -239,13 +240,14 @@ bool use_tc(const ems_desc& d) {
 // o_ready (optional) is recorded on `s` as soon as O and the LSE are final: after the forward
 // pass, before the column sums of the tensor-core path.
 int run_score(const ems_desc* desc, const void* q, const void* k, const void* v, void* o,
-              float* lse, float* glo, float* loc, void* ws, cudaStream_t s, cudaEvent_t o_ready = nullptr) {
+              float* lse, float* glo, float* loc, void* ws, cudaStream_t s, cudaEvent_t o_ready = nullptr,
+              const ScoreParts* parts = nullptr) {
     const Dims m = make_dims(*desc);
     const Layout l = layout(*desc);
     float* lse_buf = lse ? lse : at<float>(ws, l.lse);
     cudaError_t e;
     if (use_tc(*desc)) {
-        e = score_tc(m, q, k, v, o, lse_buf, glo, loc, at<void>(ws, l.tc), s, o_ready);
+        e = score_tc(m, q, k, v, o, lse_buf, glo, loc, at<void>(ws, l.tc), s, o_ready, parts);
     } else {
         // The SIMT kernels serve fp32 (no tcgen05 kind keeps the 1e-4 contract) and head_dim
         // != 128; bf16 at d = 128 always takes the tensor cores (any L up to 2^20) unless the
@@ -256,7 +258,10 @@ int run_score(const ems_desc* desc, const void* q, const void* k, const void* v,
                       "got seq_len %d)", desc->seq_len);
             return EMS_UNSUPPORTED;
         }
-        e = score_simt(m, desc->dtype, q, k, v, o, lse_buf, glo, loc, s);
+        e = cudaSuccess;
+        if (parts)
+            for (int p = 0; p < parts->n && e == cudaSuccess; ++p) e = parts->before(p, s);
+        if (e == cudaSuccess) e = score_simt(m, desc->dtype, q, k, v, o, lse_buf, glo, loc, s);
         if (e == cudaSuccess && o_ready) e = cudaEventRecord(o_ready, s);
     }
     if (e != cudaSuccess) {
@@ -567,12 +572,12 @@ namespace {
 int run_path(const ems_desc* d, const void* q_rot, const void* k_rot, const void* k_raw,
              const void* v, void* out_o, float* lse, float* glo, float* loc, const ems_stage* st,
              const ems_cache& c, void* ws, cudaStream_t s, int unit_base = 0,
-             cudaEvent_t o_ready = nullptr) {
+             cudaEvent_t o_ready = nullptr, const ScoreParts* parts = nullptr) {
     const Layout l = layout(*d);
     float* g = glo ? glo : at<float>(ws, l.glo);
     float* lc = loc ? loc : at<float>(ws, l.loc);
     const ems_stage sg = st ? *st : default_stage(*d, ws);
-    if (int rc = run_score(d, q_rot, k_rot, v, out_o, lse, g, lc, ws, s, o_ready)) return rc;
+    if (int rc = run_score(d, q_rot, k_rot, v, out_o, lse, g, lc, ws, s, o_ready, parts)) return rc;
     if (d->seq_len > d->n_budget && d->policy != EMS_POLICY_FULL) {  // policies.cpp:136-138
         if (int rc = run_select(d, g, lc, sg, ws, s, unit_base)) return rc;
         if (int rc = run_merge(d, k_raw, v, sg, ws, s)) return rc;
@@ -814,7 +819,7 @@ extern "C" int ems_prefill_host(const ems_desc* d, double rope_base, const void*
     const Dims m = make_dims(*d);
     const int U = m.units, G = m.G;
     int nc = chunks < 1 ? 1 : (chunks > U ? U : chunks);
-    HostPipeRes* res = pipe_res(3 * nc + 4);
+    HostPipeRes* res = pipe_res(3 * nc + 5);
     if (!res) {
         set_error("ems_prefill_host: could not create copy stream / events");
         return EMS_CUDA_ERROR;
@@ -824,7 +829,8 @@ extern "C" int ems_prefill_host(const ems_desc* d, double rope_base, const void*
     // each group's compress, O on `dso` as soon as each group's forward pass is done
     cudaStream_t ds = res->d2h, dso = res->d2h_o;
     // [0, nc): inputs of chunk c staged; [nc, 2nc): chunk c done; [2nc, 2nc + 3): start / copies
-    // done / second stream done; [2nc + 3, 3nc + 3): chunk c's O final; 3nc + 3: O copies done
+    // done / second stream done; [2nc + 3, 3nc + 3): chunk c's O final; 3nc + 3: O copies done;
+    // 3nc + 4: the first half of chunk 0's query heads staged (split first group)
     cudaEvent_t* ev = res->ev.data();
     cudaEvent_t* ev_o = ev + 2 * nc + 3;
     const size_t row = (size_t)m.L * m.d * m.esize;  // one [L][d] plane
@@ -872,6 +878,11 @@ extern "C" int ems_prefill_host(const ems_desc* d, double rope_base, const void*
             u0 = c == 0 ? 0 : group_end(c - 1);
             n = group_end(c) - u0;
         };
+        // The first group's forward pass runs in two halves of the query heads, the first as soon
+        // as K, V and those heads' Q have landed: the pipeline fill shrinks from G + 2 to G / 2 + 2
+        // head planes per unit (config 3: 50 -> 34 MB, ~0.3 ms)
+        const bool split0 = nc >= 2 && G >= 2 && G % 2 == 0;
+        cudaEvent_t ev_half = ev[3 * nc + 4];
         // (1) H2D of every chunk, in chunk order (score inputs first, the raw K of a pre-rotated
         //     problem last since only the merge/compact stages read it)
         for (int c = 0; c < nc; ++c) {
@@ -879,9 +890,22 @@ extern "C" int ems_prefill_host(const ems_desc* d, double rope_base, const void*
             unit_range(c, u0, n);
             const size_t oq = (size_t)u0 * G * row, nq = (size_t)n * G * row;
             const size_t ok = (size_t)u0 * row, nk = (size_t)n * row;
-            EMS_CUDA_CHECK(cudaMemcpyAsync(off(d_q, oq), off(h_q, oq), nq, cudaMemcpyHostToDevice, cs));
-            EMS_CUDA_CHECK(cudaMemcpyAsync(off(d_k, ok), off(h_k, ok), nk, cudaMemcpyHostToDevice, cs));
-            EMS_CUDA_CHECK(cudaMemcpyAsync(off(d_v, ok), off(h_v, ok), nk, cudaMemcpyHostToDevice, cs));
+            if (c == 0 && split0) {  // K, V, then each unit's first half of the heads, then the rest
+                EMS_CUDA_CHECK(cudaMemcpyAsync(off(d_k, ok), off(h_k, ok), nk, cudaMemcpyHostToDevice, cs));
+                EMS_CUDA_CHECK(cudaMemcpyAsync(off(d_v, ok), off(h_v, ok), nk, cudaMemcpyHostToDevice, cs));
+                for (int half = 0; half < 2; ++half) {
+                    for (int u = 0; u < n; ++u) {
+                        const size_t o = oq + ((size_t)u * G + half * (G / 2)) * row;
+                        EMS_CUDA_CHECK(cudaMemcpyAsync(off(d_q, o), off(h_q, o), (size_t)(G / 2) * row,
+                                                       cudaMemcpyHostToDevice, cs));
+                    }
+                    if (half == 0) EMS_CUDA_CHECK(cudaEventRecord(ev_half, cs));
+                }
+            } else {
+                EMS_CUDA_CHECK(cudaMemcpyAsync(off(d_q, oq), off(h_q, oq), nq, cudaMemcpyHostToDevice, cs));
+                EMS_CUDA_CHECK(cudaMemcpyAsync(off(d_k, ok), off(h_k, ok), nk, cudaMemcpyHostToDevice, cs));
+                EMS_CUDA_CHECK(cudaMemcpyAsync(off(d_v, ok), off(h_v, ok), nk, cudaMemcpyHostToDevice, cs));
+            }
             if (!rope)
                 EMS_CUDA_CHECK(cudaMemcpyAsync(off(d_k_raw, ok), off(h_k_raw, ok), nk, cudaMemcpyHostToDevice, cs));
             EMS_CUDA_CHECK(cudaEventRecord(ev[c], cs));
@@ -897,24 +921,48 @@ extern "C" int ems_prefill_host(const ems_desc* d, double rope_base, const void*
             const size_t oq = (size_t)u0 * G * row, ok = (size_t)u0 * row;
             cudaStream_t sc = (c & 1) ? s2 : s;
             void* wsc = dual && (c & 1) ? ws2 : ws;
-            EMS_CUDA_CHECK(cudaStreamWaitEvent(sc, ev[c], 0));
+            const bool split = c == 0 && split0;
+            EMS_CUDA_CHECK(cudaStreamWaitEvent(sc, split ? ev_half : ev[c], 0));
             const void* qr = off(d_q, oq);
             const void* kr = off(d_k, ok);
             const void* kraw = rope ? kr : off(d_k_raw, ok);
+            // RoPE of query heads [h0, h0 + nh) of every unit of the group
+            auto rope_q = [&](int h0, int nh) -> cudaError_t {
+                if (nh == G)
+                    return launch_rope(d->dtype, n * G, m.L, m.d, rope_base, d->first_position, off(d_q, oq),
+                                       off(d_q_rot, oq), sc);
+                for (int u = 0; u < n; ++u) {
+                    const size_t o = oq + ((size_t)u * G + h0) * row;
+                    cudaError_t e = launch_rope(d->dtype, nh, m.L, m.d, rope_base, d->first_position, off(d_q, o),
+                                                off(d_q_rot, o), sc);
+                    if (e != cudaSuccess) return e;
+                }
+                return cudaSuccess;
+            };
             if (rope) {
-                EMS_CUDA_CHECK(launch_rope(d->dtype, n * G, m.L, m.d, rope_base, d->first_position, qr,
-                                           off(d_q_rot, oq), sc));
+                if (!split) EMS_CUDA_CHECK(rope_q(0, G));
                 EMS_CUDA_CHECK(launch_rope(d->dtype, n, m.L, m.d, rope_base, d->first_position, kr,
                                            off(d_k_rot, ok), sc));
                 qr = off(d_q_rot, oq);
                 kr = off(d_k_rot, ok);
+            }
+            ScoreParts parts;
+            if (split) {
+                parts.n = 2;
+                parts.before = [&](int part, cudaStream_t st) -> cudaError_t {
+                    if (part == 1) {  // the second half of the heads (and, pre-rotated, the raw K)
+                        cudaError_t e = cudaStreamWaitEvent(st, ev[0], 0);
+                        if (e != cudaSuccess) return e;
+                    }
+                    return rope ? rope_q(part * (G / 2), G / 2) : cudaSuccess;
+                };
             }
             ems_cache scache = *d_cache;
             for (const CacheField& f : fields) scache.*f.ptr = off(d_cache->*f.ptr, (size_t)u0 * f.per_unit);
             const size_t ol = (size_t)u0 * m.L;
             if (int rc = run_path(&sub, qr, kr, kraw, off(d_v, ok), off(out_o, oq), off(lse, (size_t)u0 * G * m.L * 4),
                                   off(glo, ol * 4), off(loc, ol * 4), nullptr, scache, wsc, sc, u0,
-                                  h_out_o ? ev_o[c] : nullptr))
+                                  h_out_o ? ev_o[c] : nullptr, split ? &parts : nullptr))
                 return rc;
             EMS_CUDA_CHECK(cudaEventRecord(ev[nc + c], sc));
             if (h_out_o) {  // engine::prefill's PrefillResult.per_head outputs (engine.hpp:36-45): O is final

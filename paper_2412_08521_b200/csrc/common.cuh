@@ -6,6 +6,8 @@
 #include <nvtx3/nvToolsExt.h>
 #include <stdint.h>
 
+#include <functional>
+
 #include "ems_b200.h"
 
 namespace ems {
@@ -106,6 +108,15 @@ struct Dims {
 };
 
 Dims make_dims(const ems_desc& d);
+
+// The forward pass of one problem in head parts whose Q lands in pieces (the first unit group of
+// ems_prefill_host): `before(p, s)` is enqueued ahead of part p's forward launch (the wait for
+// that part's host-to-device copy and its RoPE); part p covers query heads [p G/n, (p+1) G/n) of
+// every unit.  Paths that cannot split run every `before` first.
+struct ScoreParts {
+    int n = 0;
+    std::function<cudaError_t(int part, cudaStream_t s)> before;
+};
 
 void set_error(const char* fmt, ...);
 

@@ -64,6 +64,7 @@ constexpr int kMaxT2 = 4096;  // 256-key tiles per sequence (L <= 1048576)
 
 struct Fwd2Args {
     int L, Lp, Hq, Hkv, G, nT, units;  // Lp = nT * 128: row stride of qx
+    int h0, Gs;                        // this launch's query heads of every unit: h0 .. h0 + Gs - 1
     float c;
     __nv_bfloat16* out;  // [planes][L][128] (may be null)
     __nv_bfloat16* qx;   // [planes][Lp][16] -lse2/c as three bf16 terms (P2's extra K columns)
@@ -99,18 +100,18 @@ struct Item {
 // Unit by unit; within a unit item k = (tile nT-1 - k/G, head k%G), pairs (2p, 2p+1).
 __device__ __forceinline__ Item pair_item(const Fwd2Args& a, int pair, int rank) {
     Item it;
-    const int items = a.G * a.nT, per_unit = (items + 1) / 2;
+    const int items = a.Gs * a.nT, per_unit = (items + 1) / 2;
     it.unit = pair / per_unit;
     const int k0 = 2 * (pair % per_unit);
     int k = k0 + rank;
     it.real = k < items;
     if (!it.real) k = k0;  // dummy partner: rank 0's item again, nothing stored
-    it.tile = a.nT - 1 - k / a.G;
+    it.tile = a.nT - 1 - k / a.Gs;
     const int b = it.unit / a.Hkv, hk = it.unit % a.Hkv;
-    it.plane = b * a.Hq + hk * a.G + k % a.G;
+    it.plane = b * a.Hq + hk * a.G + a.h0 + k % a.Gs;
     // 256-key tiles 0 .. jmax cover every key <= the last query row of both CTAs (rank 0's
     // item has the larger or equal tile)
-    it.jmax = (a.nT - 1 - k0 / a.G) / 2;
+    it.jmax = (a.nT - 1 - k0 / a.Gs) / 2;
     return it;
 }
 
@@ -534,11 +535,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT2, 1)
 }
 
 // max ||k|| over each 256-key tile of each unit (fp32): the per-tile logit bound of fwd2
-// (and zeroes fwd2's scheduler counter: the two launches are stream-ordered)
+// (and zeroes fwd2's scheduler counters, one per head part: the launches are stream-ordered)
 __global__ void key_tile_norm_kernel(const __nv_bfloat16* __restrict__ k, int L, int nT2, float* __restrict__ kmax,
                                      int* __restrict__ next) {
     __shared__ float sh[8];
-    if (blockIdx.x == 0 && threadIdx.x == 0) *next = 0;
+    if (blockIdx.x == 0 && threadIdx.x < 4) next[threadIdx.x] = 0;
     const int t = blockIdx.x % nT2, u = blockIdx.x / nT2;
     const int key = t * 256 + threadIdx.x;
     float ss = 0.f;
@@ -577,7 +578,7 @@ bool fwd2_tc_supported(int L) { return (L + 255) / 256 <= kMaxT2; }
 cudaError_t launch_fwd2_tc(int L, int Hq, int Hkv, int G, int units, float c, void* out, void* qx,
                            float* lse_nat, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                            const CUtensorMap& to,
-                           const void* k, float* kmax, cudaStream_t s) {
+                           const void* k, float* kmax, cudaStream_t s, int h0, int Gs, int part) {
     cudaError_t e = smem_optin(reinterpret_cast<const void*>(fwd2_tc_kernel), (int)kSmem2);
     if (e != cudaSuccess) return e;
     Fwd2Args a;
@@ -587,6 +588,9 @@ cudaError_t launch_fwd2_tc(int L, int Hq, int Hkv, int G, int units, float c, vo
     a.Hq = Hq;
     a.Hkv = Hkv;
     a.G = G;
+    a.h0 = h0;
+    a.Gs = Gs > 0 ? Gs : G;
+    if (h0 < 0 || a.h0 + a.Gs > G || part < 0 || part >= 4) return cudaErrorInvalidValue;
     a.units = units;
     a.c = c;
     a.out = static_cast<__nv_bfloat16*>(out);
@@ -594,13 +598,14 @@ cudaError_t launch_fwd2_tc(int L, int Hq, int Hkv, int G, int units, float c, vo
     a.lse_nat = lse_nat;
     a.nT2 = (L + 255) / 256;
     a.kmax = kmax;
-    const long long pairs = (long long)units * ((G * a.nT + 1) / 2);
+    const long long pairs = (long long)units * ((a.Gs * a.nT + 1) / 2);
     if (pairs >= (1ll << 30)) return cudaErrorInvalidValue;
     a.pairs = (int)pairs;
-    a.next = reinterpret_cast<int*>(reinterpret_cast<char*>(kmax) + kmax_bytes(units, L));
+    a.next = reinterpret_cast<int*>(reinterpret_cast<char*>(kmax) + kmax_bytes(units, L)) + part;
     const int slots = active_clusters(reinterpret_cast<const void*>(fwd2_tc_kernel), kT2, (int)kSmem2, 2);
     const int clusters = (int)(pairs < slots ? pairs : slots);
-    key_tile_norm_kernel<<<units * a.nT2, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(k), L, a.nT2, kmax, a.next);
+    if (part == 0)  // the key bounds once per problem; it also zeroes the scheduler counters of every part
+        key_tile_norm_kernel<<<units * a.nT2, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(k), L, a.nT2, kmax, a.next);
     fwd2_tc_kernel<<<(unsigned)(2 * clusters), kT2, kSmem2, s>>>(tq, tk, tv, to, a);
     return cudaGetLastError();
 }

@@ -40,7 +40,8 @@ size_t score_tc_workspace(const Dims& dm) {
 }
 
 cudaError_t score_tc(const Dims& dm, const void* q, const void* k, const void* v, void* o,
-                     float* lse, float* glo, float* loc, void* ws, cudaStream_t s, cudaEvent_t o_ready) {
+                     float* lse, float* glo, float* loc, void* ws, cudaStream_t s, cudaEvent_t o_ready,
+                     const ScoreParts* parts) {
     const int planes_q = dm.B * dm.Hq, planes_kv = dm.B * dm.Hkv;
     CUtensorMap tq, tk, tv;
     if (!make_tmap_bf16_3d(&tq, q, kD, dm.L, planes_q, kTile) ||
@@ -52,7 +53,16 @@ cudaError_t score_tc(const Dims& dm, const void* q, const void* k, const void* v
     float* kmax = reinterpret_cast<float*>(static_cast<char*>(ws) + qx_bytes(dm) + part_bytes(dm));
     CUtensorMap to = tq;  // O: the Q layout (only read when O is wanted)
     if (o && !make_tmap_bf16_3d(&to, o, kD, dm.L, planes_q, kTile)) return cudaErrorInvalidValue;
-    cudaError_t e = launch_fwd2_tc(dm.L, dm.Hq, dm.Hkv, dm.G, dm.units, c, o, qx, lse, tq, tk, tv, to, k, kmax, s);
+    cudaError_t e = cudaSuccess;
+    const int np = parts && parts->n > 1 && dm.G % parts->n == 0 ? parts->n : 1;
+    if (parts && np == 1)
+        for (int p = 0; p < parts->n && e == cudaSuccess; ++p) e = parts->before(p, s);
+    for (int p = 0; p < np && e == cudaSuccess; ++p) {
+        if (np > 1) e = parts->before(p, s);
+        if (e == cudaSuccess)
+            e = launch_fwd2_tc(dm.L, dm.Hq, dm.Hkv, dm.G, dm.units, c, o, qx, lse, tq, tk, tv, to, k, kmax, s,
+                               p * (dm.G / np), dm.G / np, p);
+    }
     if (e != cudaSuccess) return e;
     if (o_ready && (e = cudaEventRecord(o_ready, s)) != cudaSuccess) return e;  // O and the LSE are final
     ColArgs ca;

@@ -50,6 +50,6 @@ size_t fwd2_workspace(int units, int L);
 cudaError_t launch_fwd2_tc(int L, int Hq, int Hkv, int G, int units, float c, void* out, void* qx,
                            float* lse_nat, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                            const CUtensorMap& to,
-                           const void* k, float* kmax, cudaStream_t s);
+                           const void* k, float* kmax, cudaStream_t s, int h0 = 0, int Gs = 0, int part = 0);
 
 }  // namespace ems
