@@ -260,8 +260,9 @@ EMS_API int ems_prefill(const ems_desc* desc, double rope_base, const void* q, c
  * on every error after the first enqueue -- `stream` is ordered after every copy and the second
  * compute stream, so synchronising it completes the call. */
 /* Workspace that lets ems_prefill_host keep two unit groups in flight (odd groups on a second,
- * library-owned stream with the second half of the workspace); with ems_workspace_bytes() the
- * groups run one at a time on `stream`. */
+ * library-owned stream with the second part of the workspace) and compute the RoPE (cos, sin)
+ * table once for every group (the last part); with ems_workspace_bytes() the groups run one at a
+ * time on `stream` and every RoPE launch evaluates its own sines. */
 EMS_API size_t ems_prefill_host_workspace_bytes(const ems_desc* desc);
 EMS_API int ems_prefill_host(const ems_desc* desc, double rope_base, const void* h_q, const void* h_k,
                      const void* h_k_raw, const void* h_v, void* d_q, void* d_k, void* d_k_raw,

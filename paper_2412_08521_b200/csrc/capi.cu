@@ -44,6 +44,10 @@ cudaError_t launch_keep_all(const Dims& dm, int dtype, const void* k, const void
 cudaError_t launch_rope(int dtype, int planes, int L, int d, double base, long long first_pos,
                         const void* x, void* y, cudaStream_t s);
 cudaError_t launch_rope_table(float2* table, int max_pos, int d, double base, cudaStream_t s);
+size_t rope_table64_bytes(int L, int d);
+cudaError_t launch_rope_table64(void* tab, int L, int d, double base, long long first_pos, cudaStream_t s);
+cudaError_t launch_rope_tab(int dtype, int planes, int L, int d, const void* tab, const void* x, void* y,
+                            cudaStream_t s);
 cudaError_t launch_decode_init(const Dims& m, int dtype, const ems_cache& c, const ems_decode_state& st,
                                int S, int W, int T, cudaStream_t s);
 cudaError_t launch_decode_step(const Dims& m, int dtype, int S, int W, int T, int R, int l_win, int lut_cap,
@@ -448,7 +452,8 @@ size_t ems_workspace_bytes(const ems_desc* d) {
 
 size_t ems_prefill_host_workspace_bytes(const ems_desc* d) {
     if (ems_validate(d) != EMS_OK) return 0;
-    return 2 * ems::align_up(ems::workspace_need(*d));
+    // two unit groups in flight + the RoPE (cos, sin) table of the problem
+    return 2 * ems::align_up(ems::workspace_need(*d)) + ems::align_up(ems::rope_table64_bytes(d->seq_len, d->head_dim));
 }
 
 int ems_score(const ems_desc* d, const void* q, const void* k, const void* v, void* out_o,
@@ -819,7 +824,7 @@ extern "C" int ems_prefill_host(const ems_desc* d, double rope_base, const void*
     const Dims m = make_dims(*d);
     const int U = m.units, G = m.G;
     int nc = chunks < 1 ? 1 : (chunks > U ? U : chunks);
-    HostPipeRes* res = pipe_res(3 * nc + 5);
+    HostPipeRes* res = pipe_res(3 * nc + 7);
     if (!res) {
         set_error("ems_prefill_host: could not create copy stream / events");
         return EMS_CUDA_ERROR;
@@ -830,7 +835,7 @@ extern "C" int ems_prefill_host(const ems_desc* d, double rope_base, const void*
     cudaStream_t ds = res->d2h, dso = res->d2h_o;
     // [0, nc): inputs of chunk c staged; [nc, 2nc): chunk c done; [2nc, 2nc + 3): start / copies
     // done / second stream done; [2nc + 3, 3nc + 3): chunk c's O final; 3nc + 3: O copies done;
-    // 3nc + 4: the first half of chunk 0's query heads staged (split first group)
+    // [3nc + 4, 3nc + 7): head parts 0 .. np-2 of chunk 0 staged (split first group)
     cudaEvent_t* ev = res->ev.data();
     cudaEvent_t* ev_o = ev + 2 * nc + 3;
     const size_t row = (size_t)m.L * m.d * m.esize;  // one [L][d] plane
@@ -852,8 +857,12 @@ extern "C" int ems_prefill_host(const ems_desc* d, double rope_base, const void*
     // two unit groups in flight (odd groups on a second stream and workspace) when the caller
     // passed ems_prefill_host_workspace_bytes(); one at a time otherwise
     const size_t one = align_up(workspace_need(*d));
+    // RoPE (cos, sin) computed once for every group when the workspace has room for the table
+    const size_t tab_bytes = align_up(rope_table64_bytes(m.L, m.d));
     const bool dual = nc >= 2 && ws_bytes >= 2 * one;
+    const bool use_tab = rope && ws_bytes >= (dual ? 2 : 1) * one + tab_bytes;
     void* ws2 = dual ? off(ws, one) : nullptr;
+    void* tab = use_tab ? off(ws, (dual ? 2 : 1) * one) : nullptr;
     cudaStream_t s2 = dual ? res->comp2 : s;
     // Everything below is stream-ordered.  Whatever happens (a failed launch part-way through the
     // groups included), `stream` is finally ordered after the copy stream and the second compute
@@ -878,11 +887,15 @@ extern "C" int ems_prefill_host(const ems_desc* d, double rope_base, const void*
             u0 = c == 0 ? 0 : group_end(c - 1);
             n = group_end(c) - u0;
         };
-        // The first group's forward pass runs in two halves of the query heads, the first as soon
-        // as K, V and those heads' Q have landed: the pipeline fill shrinks from G + 2 to G / 2 + 2
-        // head planes per unit (config 3: 50 -> 34 MB, ~0.3 ms)
-        const bool split0 = nc >= 2 && G >= 2 && G % 2 == 0;
-        cudaEvent_t ev_half = ev[3 * nc + 4];
+        // The first group's forward pass runs in two halves of the query heads, each as soon as K,
+        // V and its heads' Q have landed: the pipeline fill shrinks from G + 2 to G / 2 + 2 head
+        // planes per unit (config 3: 50 -> 34 MB) and the second half's copy runs under the first
+        // half's compute (four one-head parts were slower: 128-pair launches leave most of the last
+        // wave idle)
+        const int np = nc >= 2 && G >= 2 && G % 2 == 0 ? 2 : 1;
+        const bool split0 = np > 1;
+        const int hp = G / np;  // heads per part
+        const cudaEvent_t* ev_part = ev + 3 * nc + 4;
         // (1) H2D of every chunk, in chunk order (score inputs first, the raw K of a pre-rotated
         //     problem last since only the merge/compact stages read it)
         for (int c = 0; c < nc; ++c) {
@@ -890,16 +903,16 @@ extern "C" int ems_prefill_host(const ems_desc* d, double rope_base, const void*
             unit_range(c, u0, n);
             const size_t oq = (size_t)u0 * G * row, nq = (size_t)n * G * row;
             const size_t ok = (size_t)u0 * row, nk = (size_t)n * row;
-            if (c == 0 && split0) {  // K, V, then each unit's first half of the heads, then the rest
+            if (c == 0 && split0) {  // K, V, then each unit's heads part by part
                 EMS_CUDA_CHECK(cudaMemcpyAsync(off(d_k, ok), off(h_k, ok), nk, cudaMemcpyHostToDevice, cs));
                 EMS_CUDA_CHECK(cudaMemcpyAsync(off(d_v, ok), off(h_v, ok), nk, cudaMemcpyHostToDevice, cs));
-                for (int half = 0; half < 2; ++half) {
+                for (int pt = 0; pt < np; ++pt) {
                     for (int u = 0; u < n; ++u) {
-                        const size_t o = oq + ((size_t)u * G + half * (G / 2)) * row;
-                        EMS_CUDA_CHECK(cudaMemcpyAsync(off(d_q, o), off(h_q, o), (size_t)(G / 2) * row,
+                        const size_t o = oq + ((size_t)u * G + pt * hp) * row;
+                        EMS_CUDA_CHECK(cudaMemcpyAsync(off(d_q, o), off(h_q, o), (size_t)hp * row,
                                                        cudaMemcpyHostToDevice, cs));
                     }
-                    if (half == 0) EMS_CUDA_CHECK(cudaEventRecord(ev_half, cs));
+                    if (pt < np - 1) EMS_CUDA_CHECK(cudaEventRecord(ev_part[pt], cs));
                 }
             } else {
                 EMS_CUDA_CHECK(cudaMemcpyAsync(off(d_q, oq), off(h_q, oq), nq, cudaMemcpyHostToDevice, cs));
@@ -909,6 +922,13 @@ extern "C" int ems_prefill_host(const ems_desc* d, double rope_base, const void*
             if (!rope)
                 EMS_CUDA_CHECK(cudaMemcpyAsync(off(d_k_raw, ok), off(h_k_raw, ok), nk, cudaMemcpyHostToDevice, cs));
             EMS_CUDA_CHECK(cudaEventRecord(ev[c], cs));
+        }
+        // the RoPE table, enqueued after the copies so that they start first; it runs under the
+        // first group's copies, and the second compute stream waits for it too
+        if (use_tab) {
+            EMS_CUDA_CHECK(launch_rope_table64(tab, m.L, m.d, rope_base, d->first_position, s));
+            EMS_CUDA_CHECK(cudaEventRecord(ev[2 * nc + 2], s));
+            if (dual) EMS_CUDA_CHECK(cudaStreamWaitEvent(s2, ev[2 * nc + 2], 0));
         }
         // (2) compute chunk c once its inputs landed; (3) copy its cache back as soon as it is done
         for (int c = 0; c < nc; ++c) {
@@ -922,39 +942,39 @@ extern "C" int ems_prefill_host(const ems_desc* d, double rope_base, const void*
             cudaStream_t sc = (c & 1) ? s2 : s;
             void* wsc = dual && (c & 1) ? ws2 : ws;
             const bool split = c == 0 && split0;
-            EMS_CUDA_CHECK(cudaStreamWaitEvent(sc, split ? ev_half : ev[c], 0));
+            EMS_CUDA_CHECK(cudaStreamWaitEvent(sc, split ? ev_part[0] : ev[c], 0));
             const void* qr = off(d_q, oq);
             const void* kr = off(d_k, ok);
             const void* kraw = rope ? kr : off(d_k_raw, ok);
             // RoPE of query heads [h0, h0 + nh) of every unit of the group
+            auto rope_planes = [&](int planes, const void* x, void* y) -> cudaError_t {
+                return use_tab ? launch_rope_tab(d->dtype, planes, m.L, m.d, tab, x, y, sc)
+                               : launch_rope(d->dtype, planes, m.L, m.d, rope_base, d->first_position, x, y, sc);
+            };
             auto rope_q = [&](int h0, int nh) -> cudaError_t {
-                if (nh == G)
-                    return launch_rope(d->dtype, n * G, m.L, m.d, rope_base, d->first_position, off(d_q, oq),
-                                       off(d_q_rot, oq), sc);
+                if (nh == G) return rope_planes(n * G, off(d_q, oq), off(d_q_rot, oq));
                 for (int u = 0; u < n; ++u) {
                     const size_t o = oq + ((size_t)u * G + h0) * row;
-                    cudaError_t e = launch_rope(d->dtype, nh, m.L, m.d, rope_base, d->first_position, off(d_q, o),
-                                                off(d_q_rot, o), sc);
+                    cudaError_t e = rope_planes(nh, off(d_q, o), off(d_q_rot, o));
                     if (e != cudaSuccess) return e;
                 }
                 return cudaSuccess;
             };
             if (rope) {
                 if (!split) EMS_CUDA_CHECK(rope_q(0, G));
-                EMS_CUDA_CHECK(launch_rope(d->dtype, n, m.L, m.d, rope_base, d->first_position, kr,
-                                           off(d_k_rot, ok), sc));
+                EMS_CUDA_CHECK(rope_planes(n, kr, off(d_k_rot, ok)));
                 qr = off(d_q_rot, oq);
                 kr = off(d_k_rot, ok);
             }
             ScoreParts parts;
             if (split) {
-                parts.n = 2;
+                parts.n = np;
                 parts.before = [&](int part, cudaStream_t st) -> cudaError_t {
-                    if (part == 1) {  // the second half of the heads (and, pre-rotated, the raw K)
-                        cudaError_t e = cudaStreamWaitEvent(st, ev[0], 0);
+                    if (part > 0) {  // this part's heads (the last part: every input of the group)
+                        cudaError_t e = cudaStreamWaitEvent(st, part < np - 1 ? ev_part[part] : ev[0], 0);
                         if (e != cudaSuccess) return e;
                     }
-                    return rope ? rope_q(part * (G / 2), G / 2) : cudaSuccess;
+                    return rope ? rope_q(part * hp, hp) : cudaSuccess;
                 };
             }
             ems_cache scache = *d_cache;
