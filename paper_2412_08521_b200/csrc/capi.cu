@@ -946,11 +946,11 @@ extern "C" int ems_prefill_host(const ems_desc* d, double rope_base, const void*
             const void* qr = off(d_q, oq);
             const void* kr = off(d_k, ok);
             const void* kraw = rope ? kr : off(d_k_raw, ok);
-            // RoPE of query heads [h0, h0 + nh) of every unit of the group
             auto rope_planes = [&](int planes, const void* x, void* y) -> cudaError_t {
                 return use_tab ? launch_rope_tab(d->dtype, planes, m.L, m.d, tab, x, y, sc)
                                : launch_rope(d->dtype, planes, m.L, m.d, rope_base, d->first_position, x, y, sc);
             };
+            // RoPE of query heads [h0, h0 + nh) of every unit of the group
             auto rope_q = [&](int h0, int nh) -> cudaError_t {
                 if (nh == G) return rope_planes(n * G, off(d_q, oq), off(d_q_rot, oq));
                 for (int u = 0; u < n; ++u) {
