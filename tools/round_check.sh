@@ -15,7 +15,7 @@ python bench.py --config cfgM --steps 1 --warmup 0 --no-cpu-baseline --no-e2e > 
 ncu --set full --clock-control none --import-source on -k regex:"merge_bucket|merge_accum|select_kernel|compact_lut" -c 4 -o gpurun_out/full_cfgM \
     python bench.py --config cfgM --steps 1 --warmup 0 --no-cpu-baseline --no-e2e > gpurun_out/ncu_full_cfgM.log 2>&1
 python bench.py --steps 1 --warmup 0 --no-cpu-baseline > gpurun_out/plain_e2e.log 2>&1 && \
-ncu --set full --clock-control none -k regex:rope_kernel -c 1 -o gpurun_out/full_rope python bench.py --steps 1 --warmup 0 --no-cpu-baseline > gpurun_out/ncu_full_rope.log 2>&1
+ncu --set full --clock-control none -k regex:"rope_tab_kernel|rope_table64" -c 2 -o gpurun_out/full_rope python bench.py --steps 1 --warmup 0 --no-cpu-baseline > gpurun_out/ncu_full_rope.log 2>&1
 python tools/bench_decode.py --config cfg3 > gpurun_out/decode_cfg3.json 2>&1
 ncu --set full --clock-control none --import-source on -k regex:decode_step --launch-skip 10 -c 1 -o gpurun_out/full_decode_step \
     python tools/bench_decode.py --config cfg3 --steps 20 > gpurun_out/ncu_full_decode.log 2>&1
