@@ -536,34 +536,45 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT2, 1)
 
 // max ||k|| over each 256-key tile of each unit (fp32): the per-tile logit bound of fwd2
 // (and zeroes fwd2's scheduler counters, one per head part: the launches are stream-ordered)
-__global__ void key_tile_norm_kernel(const __nv_bfloat16* __restrict__ k, int L, int nT2, float* __restrict__ kmax,
-                                     int* __restrict__ next) {
+__global__ void __launch_bounds__(256) key_tile_norm_kernel(const __nv_bfloat16* __restrict__ k, int L, int nT2,
+                                                           float* __restrict__ kmax, int* __restrict__ next) {
     __shared__ float sh[8];
     if (blockIdx.x == 0 && threadIdx.x < 4) next[threadIdx.x] = 0;
     const int t = blockIdx.x % nT2, u = blockIdx.x / nT2;
-    const int key = t * 256 + threadIdx.x;
-    float ss = 0.f;
-    if (key < L) {
-        const uint4* row = reinterpret_cast<const uint4*>(k + ((size_t)u * L + key) * kD);
+    // a half-warp per key row (16 lanes x 16 bytes = the 256-byte row: fully coalesced), each
+    // warp 32 rows of the tile, 4 rows per lane in flight
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, half = lane >> 4, c = lane & 15;
+    const uint4* base = reinterpret_cast<const uint4*>(k + (size_t)u * L * kD) + c;
+    float mx = 0.f;
 #pragma unroll
-        for (int c = 0; c < kD / 8; ++c) {
-            const uint4 w = row[c];
-            const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
+    for (int it = 0; it < 16; it += 4) {
+        uint4 w[4];
 #pragma unroll
-            for (int x = 0; x < 4; ++x) {
-                const float lo = __uint_as_float(wv[x] << 16), hi = __uint_as_float(wv[x] & 0xFFFF0000u);
+        for (int x = 0; x < 4; ++x) {
+            const int key = t * 256 + warp * 32 + 2 * (it + x) + half;
+            w[x] = key < L ? base[(size_t)key * (kD / 8)] : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int x = 0; x < 4; ++x) {
+            const uint32_t wv[4] = {w[x].x, w[x].y, w[x].z, w[x].w};
+            float ss = 0.f;
+#pragma unroll
+            for (int y = 0; y < 4; ++y) {
+                const float lo = __uint_as_float(wv[y] << 16), hi = __uint_as_float(wv[y] & 0xFFFF0000u);
                 ss = fmaf(lo, lo, fmaf(hi, hi, ss));
             }
+#pragma unroll
+            for (int o = 8; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);  // within the half
+            mx = fmaxf(mx, sqrtf(ss));
         }
     }
-    float n = sqrtf(ss);
-    n = warp_max(n);
-    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = n;
+    mx = warp_max(mx);
+    if (lane == 0) sh[warp] = mx;
     __syncthreads();
     if (threadIdx.x == 0) {
-        float mx = sh[0];
-        for (int i = 1; i < 8; ++i) mx = fmaxf(mx, sh[i]);
-        kmax[blockIdx.x] = mx * 1.0001f;
+        float m = sh[0];
+        for (int i = 1; i < 8; ++i) m = fmaxf(m, sh[i]);
+        kmax[blockIdx.x] = m * 1.0001f;
     }
 }
 
