@@ -124,3 +124,26 @@ def test_host_pipeline_concurrent_groups_equal_sequential():
     for n in res[0][0]:
         assert torch.equal(res[0][0][n], res[1][0][n]), n
     assert torch.equal(res[0][1], res[1][1]) and torch.equal(res[0][2], res[1][2])
+
+
+def test_host_pipeline_split_first_group_odd_part():
+    """G = 6: the first group's forward pass runs in two parts of 3 heads (pairs straddle query
+    tiles, an odd item count gets a dummy partner); O, LSE-derived scores and caches equal the
+    device-resident path."""
+    w = CONFIGS["cfg3"]
+    rng = np.random.default_rng(6)
+    H, G, L = 3, 6, 1100
+    dt = torch.bfloat16
+    q = torch.tensor(rng.standard_normal((1, H * G, L, 128))).to(dt)
+    k = torch.tensor(rng.standard_normal((1, H, L, 128))).to(dt)
+    v = torch.tensor(rng.standard_normal((1, H, L, 128))).to(dt)
+    cfg = ems.EmsConfig(w.n_budget, w.l_win, w.tau, w.gamma, w.kernel_size)
+    plan = ems.prefill_host(q.pin_memory(), k.pin_memory(), v.pin_memory(), cfg, w.rope_base, chunks=3)
+    ref = ems.prefill(q.cuda(), k.cuda(), v.cuda(), cfg, w.rope_base)
+    torch.cuda.synchronize()
+    assert torch.equal(plan.q_rot, ref.q_rot) and torch.equal(plan.k_rot, ref.k_rot)
+    assert torch.equal(plan.out, ref.out)
+    np.testing.assert_allclose(plan.glo.cpu().numpy(), ref.glo.cpu().numpy(), rtol=1e-6)
+    hc = plan.host_cache()
+    for name in ("center_pos", "lut_pos", "lut_slot", "local_pos", "counts"):
+        assert torch.equal(hc[name], ref.cache[name].cpu()), name
