@@ -1,3 +1,5 @@
+"""Score-pass time drift: 40 back-to-back config-3 passes (the power cap engaging), then 10
+passes separated by 200 ms idle gaps (each starts unthrottled).  python tools/drift.py"""
 import torch, time, sys, os
 sys.path.insert(0, os.getcwd())
 from paper_2412_08521_b200 import ems

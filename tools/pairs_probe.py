@@ -1,3 +1,6 @@
+"""P1 / P2 kernel times at equal attention FLOPs and growing work-item counts (G = 4, 8 KV heads:
+B x L = 1 x 32768, 4 x 16384, 16 x 8192, 64 x 4096): separates per-item overhead from the
+per-key-tile loop (the measurement behind the persistent P1).  python tools/pairs_probe.py"""
 import torch, json, sys
 sys.path.insert(0, '/root/repo')
 from paper_2412_08521_b200 import ems
