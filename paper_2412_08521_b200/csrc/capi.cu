@@ -988,6 +988,9 @@ extern "C" int ems_prefill_host(const ems_desc* d, double rope_base, const void*
             if (h_out_o) {  // engine::prefill's PrefillResult.per_head outputs (engine.hpp:36-45): O is final
                             // after the forward pass, so its copy overlaps this group's column sums and compress
                 EMS_CUDA_CHECK(cudaStreamWaitEvent(dso, ev_o[c], 0));
+                // ... and after the next group's inputs landed: concurrent D2H slows the host-to-device
+                // copies the next group waits for (measured 55 -> 32 GB/s), O has slack
+                if (c + 1 < nc) EMS_CUDA_CHECK(cudaStreamWaitEvent(dso, ev[c + 1], 0));
                 EMS_CUDA_CHECK(cudaMemcpyAsync(off(h_out_o, oq), off(out_o, oq), (size_t)n * G * row,
                                                cudaMemcpyDeviceToHost, dso));
             }

@@ -58,7 +58,7 @@ def main():
     kb = sum(r[1] - r[0] for r in rows if r[2] == "kern")
     print(f"kernels busy (sum) {kb:.3f} ms")
     for r in rows:
-        if r[2] == "kern" or r[1] - r[0] > 0.1:
+        if r[2] == "kern" or r[1] - r[0] > 0.1 or r[0] > end - 1.0:
             print(f"{r[0]:8.3f} {r[1]:8.3f} {r[2]:4s} {r[3]}")
 
 
