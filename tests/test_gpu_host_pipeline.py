@@ -147,3 +147,22 @@ def test_host_pipeline_split_first_group_odd_part():
     hc = plan.host_cache()
     for name in ("center_pos", "lut_pos", "lut_slot", "local_pos", "counts"):
         assert torch.equal(hc[name], ref.cache[name].cpu()), name
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_host_pipeline_rope_table_first_position(dtype):
+    """The host pipeline's once-per-call RoPE table (positions first_position + l) rotates exactly
+    like the device-resident path's per-launch sines, for bf16 and fp32."""
+    w = CONFIGS["cfg3"]
+    rng = np.random.default_rng(8)
+    H, G, L, first = 2, 2, 700, 1234
+    q = torch.tensor(rng.standard_normal((1, H * G, L, 128))).to(dtype)
+    k = torch.tensor(rng.standard_normal((1, H, L, 128))).to(dtype)
+    v = torch.tensor(rng.standard_normal((1, H, L, 128))).to(dtype)
+    cfg = ems.EmsConfig(w.n_budget, w.l_win, w.tau, w.gamma, w.kernel_size)
+    plan = ems.prefill_host(q.pin_memory(), k.pin_memory(), v.pin_memory(), cfg, w.rope_base, chunks=2,
+                            first_position=first)
+    ref = ems.prefill(q.cuda(), k.cuda(), v.cuda(), cfg, w.rope_base, first_position=first)
+    torch.cuda.synchronize()
+    assert torch.equal(plan.q_rot, ref.q_rot) and torch.equal(plan.k_rot, ref.k_rot)
+    assert torch.equal(plan.out, ref.out)
