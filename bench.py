@@ -493,6 +493,7 @@ def main():
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
                          "frac": achieved / peak_tf, "traffic": traffic_bytes(w) if ws == 1 else None,
                          "frac_of_sustained_peak": achieved / pk.get("bf16_tflops_sustained", peak_tf),
+                         "frac_of_spec_peak": achieved / 2250.0,  # nominal dense bf16
                          "kernel": "score pass (O+LSE and glo/loc column sums)",
                          "peak_source": f"{pk['source']} bf16_tflops (burst)",
                          "algorithmic_flops_per_launch": f_alg(shard_w)},
