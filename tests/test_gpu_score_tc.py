@@ -167,3 +167,55 @@ def test_tc_score_long_odd_lengths(L, G):
         o = plan.out[0, h, rows].float()
         err = ((o - o_t).abs().max(dim=1).values / o_t.abs().max(dim=1).values.clamp_min(1e-3)).max().item()
         assert err <= 2e-2, (h, err)  # bf16 P and bf16 output
+
+
+def _fuzz_shapes(n=16, seed=2024):
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(n):
+        G = int(rng.choice([1, 2, 3, 4, 6, 8]))
+        Hkv = int(rng.integers(1, 4))
+        B = int(rng.integers(1, 3))
+        L = int(rng.integers(1, 3000))
+        lw = int(rng.integers(1, 65))
+        out.append((B, G * Hkv, Hkv, L, lw))
+    return out
+
+
+@pytest.mark.parametrize("shape", _fuzz_shapes())
+def test_tc_score_fuzz_vs_torch(shape):
+    """Seeded random shapes (any L from 1, G in {1, 2, 3, 4, 6, 8}, up to 3 KV heads, B up to 2):
+    the persistent forward pass's pair scheduling (pair counts below and above the resident
+    clusters, dummy partners, partial tiles) and the column sums against the torch streaming
+    pass -- glo, loc and O on every row."""
+    B, Hq, Hkv, L, lw = shape
+    dev = torch.device("cuda")
+    g = torch.Generator(device=dev)
+    g.manual_seed(L * 131 + Hq)
+    q = torch.randn((B, Hq, L, 128), generator=g, device=dev).to(torch.bfloat16)
+    k = torch.randn((B, Hkv, L, 128), generator=g, device=dev).to(torch.bfloat16)
+    v = torch.randn((B, Hkv, L, 128), generator=g, device=dev).to(torch.bfloat16)
+    cfg = ems.EmsConfig(n_budget=max(lw + 1, 2), l_win=lw, gamma=1.0, kernel_size=1)
+    plan = ems.Plan(B, Hq, Hkv, L, 128, torch.bfloat16, cfg, dev, "tcgen05", want_out=True, want_lse=True)
+    plan.score(q, k, v)
+    torch.cuda.synchronize()
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    try:
+        glo_t, loc_t = _torch_scores(q, k, min(lw, L))
+        G = Hq // Hkv
+        for b in range(B):
+            for h in range(Hq):
+                s = (q[b, h].float() @ k[b, h // G].float().T) / 128 ** 0.5
+                s.masked_fill_(torch.ones(L, L, device=dev, dtype=torch.bool).triu(1), float("-inf"))
+                o_t = torch.softmax(s, dim=1) @ v[b, h // G].float()
+                o = plan.out[b, h].float()
+                err = ((o - o_t).abs().max(dim=1).values / o_t.abs().max(dim=1).values.clamp_min(1e-3)).max()
+                assert err.item() <= 2e-2, (b, h, err.item())
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+    floor = 1e-4 * glo_t.mean()
+    assert ((plan.glo.double() - glo_t).abs() / (glo_t + floor)).max().item() <= 1e-5
+    m = loc_t > 1e-6
+    if m.any():
+        assert ((plan.loc.double() - loc_t).abs()[m] / loc_t[m]).max().item() <= 2e-4
