@@ -285,3 +285,38 @@ def test_gpu_corrupt_stage_raises_corruption_error():
     plan.compact(kw, v)
     with pytest.raises(ems.CorruptionError):
         plan.sync_status()
+
+
+def _path_fuzz_cases(n=8, seed=77):
+    rng = np.random.default_rng(seed)
+    out = []
+    for i in range(n):
+        L = int(rng.integers(200, 1400))
+        l_win = int(rng.integers(4, 48))
+        budget = int(rng.integers(l_win + 8, max(l_win + 9, L // 3)))
+        gamma = float(rng.choice([1.0, 1.5, 2.0, 4.0]))
+        tau = float(rng.choice([0.0, 0.3, 0.6, 0.9]))
+        k = int(rng.choice([1, 3, 7]))
+        G = int(rng.choice([1, 2, 4]))
+        out.append((i, L, l_win, budget, gamma, tau, k, G))
+    return out
+
+
+@pytest.mark.parametrize("case", _path_fuzz_cases())
+def test_gpu_path_fuzz_vs_oracle(case, oracle):
+    """Seeded random (L, l_win, budget, gamma, tau, pooling kernel, G) on redundant K/V (merges
+    and zero-class tokens both occur): the whole bf16 prefill-compress path against the C
+    restatement of the reference, with the D10 bands."""
+    i, L, l_win, budget, gamma, tau, k, G = case
+    w = CONFIGS["cfgM"]
+    rng = np.random.default_rng([i, L])
+    units = []
+    for u in range(2):
+        base = make_unit_np(w, seed=100 + i, seq_len=L, unit=u)
+        q = round_to(rng.standard_normal((G, L, base.q_rot.shape[-1])), "bf16")
+        units.append(U(q, base.k_rot, base.k_raw, base.v))
+    cfg = Config(n_budget=budget, l_win=l_win, tau=tau, gamma=gamma, kernel_size=k)
+    plan = run_gpu(units, "bf16", cfg)
+    for u, un in enumerate(units):
+        ref = oracle.prefill_unit(un.q_rot, un.k_rot, un.k_raw, un.v, cfg)
+        check_unit(plan, u, un, ref, ref.extra["glo"], ref.extra["loc"], "bf16", cfg, oracle)
